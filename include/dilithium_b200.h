@@ -1,0 +1,138 @@
+/*
+ * dilithium_b200.h -- C ABI of the B200-native batched CRYSTALS-Dilithium (round-3) engine.
+ *
+ * This is the drop-in boundary for the reference's batched hot path.  Each entry point
+ * names the reference interface it replaces (paths relative to the reference's
+ * proj/include/dilithium/).  Plain pointers and sizes only; the library owns device
+ * memory, pinned staging and streams.  All batch calls are synchronous at the API and
+ * internally asynchronous.  There is no CPU fallback: every call either runs on the
+ * GPU or returns a negative status.
+ *
+ * level is 2, 3 or 5 (params.hpp:53-55; runtime dispatch as with_params, params.hpp:91-106).
+ * Byte sizes per level: pk 1312/1952/2592, sk 2528/4000/4864, sig 2420/3293/4595.
+ *
+ * Status codes: 0 ok; DLB_E_ARG bad argument; DLB_E_LEVEL unsupported level;
+ * DLB_E_KEY malformed secret key (packing.hpp:79-86,215-233 -- the C++ shim turns this
+ * into std::invalid_argument / nullopt); <= -1000: -(1000 + cudaError_t).
+ */
+#ifndef DILITHIUM_B200_H
+#define DILITHIUM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DLB_OK 0
+#define DLB_E_ARG (-1)
+#define DLB_E_LEVEL (-2)
+#define DLB_E_KEY (-3)
+#define DLB_E_NOMEM (-4)
+
+typedef struct dlb_ctx dlb_ctx;
+
+/* BatchStats (batch.hpp:31-38) + device-scheduler counters. */
+typedef struct dlb_sign_stats {
+  uint64_t rounds;               /* scheduler rounds summed over all CTAs */
+  uint64_t attempts;             /* executed attempts incl. speculative waste */
+  uint64_t speculative;          /* attempts beyond a task's next unresolved nonce */
+  uint64_t idle_slot_rounds;     /* slot-rounds that ran no attempt */
+  uint64_t accepted_attempt_sum; /* sum over tasks of the winning attempt ordinal */
+  uint64_t failed_tasks;         /* nonce space exhausted (scheduler.hpp:52,122-128) */
+} dlb_sign_stats;
+
+/* Library / device ------------------------------------------------------------------ */
+
+/* Creates an engine on CUDA device `device`.  max_batch is a sizing hint (0 = grow on
+ * demand).  Replaces the per-call WorkerPool + MemoryPool construction of
+ * batch.hpp:62-67 with a context that is built once and reused. */
+int dlb_create(dlb_ctx** out, int device, size_t max_batch);
+void dlb_destroy(dlb_ctx* ctx);
+const char* dlb_version(void);
+/* Device time (ms, CUDA events on the engine's stream) of the kernels of the last batch
+ * call, excluding host<->device copies. */
+float dlb_last_kernel_ms(const dlb_ctx* ctx);
+/* Number of kernel launches issued by the last batch call. */
+unsigned dlb_last_launches(const dlb_ctx* ctx);
+/* Use an external CUDA stream (e.g. the caller's current stream) for the *_dev entry
+ * points; NULL restores the engine's own stream. */
+int dlb_set_stream(dlb_ctx* ctx, void* cuda_stream);
+
+/* Host-buffer batch API (what batch.hpp binds) ----------------------------------------- */
+
+/* batch_keygen<P>(zetas, workers)  batch.hpp:159-166 / keygen<P>  scheme.hpp:68-104.
+ * zetas: n*32 bytes.  pks: n*pk_bytes.  sks: n*sk_bytes. */
+int dlb_keygen_batch(dlb_ctx* ctx, int level, size_t n, const uint8_t* zetas, uint8_t* pks,
+                     uint8_t* sks);
+
+/* batch_sign<P>(jobs, cfg, stats)  batch.hpp:53-137 (+ make_precomp scheme.hpp:106-125,
+ * sign_with_precomp :253-266).
+ *   sks, sk_stride: secret keys; sk_stride == 0 means one key shared by all tasks
+ *                   (SignJob.key pointing at one SignPrecomp), else sks + i*sk_stride.
+ *   msgs, msg_off:  messages concatenated; task i signs msgs[msg_off[i] .. msg_off[i+1]).
+ *   rho_prime_override: NULL (deterministic signing) or n*64 bytes (scheme.hpp:253-258).
+ *   psi:       resident attempt slots, BatchConfig::psi (0 = engine default).
+ *   speculate: BatchConfig::speculate.
+ *   sigs:      n*sig_bytes out.  attempts (nullable): winning attempt ordinal per task
+ *              (SignOutput::attempts).  failed (nullable): 1 if the nonce space was
+ *              exhausted (BatchStats::failed_tasks).  stats nullable.
+ * Returns DLB_E_KEY if any secret key is malformed (no signature is produced). */
+int dlb_sign_batch(dlb_ctx* ctx, int level, size_t n, const uint8_t* sks, size_t sk_stride,
+                   const uint8_t* msgs, const uint64_t* msg_off,
+                   const uint8_t* rho_prime_override, size_t psi, int speculate, uint8_t* sigs,
+                   uint32_t* attempts, uint8_t* failed, dlb_sign_stats* stats);
+
+/* batch_verify<P>(jobs, workers)  batch.hpp:148-156 / verify<P>  scheme.hpp:277-318.
+ *   pks, pk_stride: pk_stride == 0 means one shared public key.
+ *   sigs: n*sig_bytes (sig_stride = sig_bytes).  Tasks whose pk/sig length is wrong are
+ *   the shim's business (flag 0 without touching the GPU, scheme.hpp:280-283); here
+ *   every task has full-size inputs.
+ *   flags: n bytes out, 1 accept / 0 reject.  Never fails per task otherwise. */
+int dlb_verify_batch(dlb_ctx* ctx, int level, size_t n, const uint8_t* pks, size_t pk_stride,
+                     const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* sigs,
+                     uint8_t* flags);
+
+/* Device-resident variants -------------------------------------------------------------
+ * Same contracts with every buffer already in device memory (HBM); no copies are made.
+ * Used for kernel-only timing and by callers that keep keys/messages on the GPU. */
+int dlb_keygen_batch_dev(dlb_ctx* ctx, int level, size_t n, const uint8_t* d_zetas,
+                         uint8_t* d_pks, uint8_t* d_sks);
+int dlb_sign_batch_dev(dlb_ctx* ctx, int level, size_t n, const uint8_t* d_sks, size_t sk_stride,
+                       const uint8_t* d_msgs, const uint64_t* d_msg_off,
+                       const uint8_t* d_rho_prime_override, size_t psi, int speculate,
+                       uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed,
+                       dlb_sign_stats* stats /* host */);
+int dlb_verify_batch_dev(dlb_ctx* ctx, int level, size_t n, const uint8_t* d_pks,
+                         size_t pk_stride, const uint8_t* d_msgs, const uint64_t* d_msg_off,
+                         const uint8_t* d_sigs, uint8_t* d_flags);
+
+/* Stage-level entry points (device parity tests; host buffers) --------------------------
+ * They run the same device functions the batch kernels use. */
+int dlb_dbg_keccak_f1600(dlb_ctx* ctx, size_t n, uint64_t* states /* n*25, in place */);
+int dlb_dbg_shake256(dlb_ctx* ctx, size_t n, const uint8_t* msgs, const uint64_t* msg_off,
+                     uint8_t* out64 /* n*64: first 64 output bytes */);
+int dlb_dbg_expand_a(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t* rhos /* n*32 */,
+                     int32_t* out /* n*K*L*256 */);
+int dlb_dbg_expand_s(dlb_ctx* ctx, int level, size_t n, const uint8_t* rho_primes /* n*64 */,
+                     int8_t* out /* n*(L+K)*256 */);
+int dlb_dbg_expand_mask(dlb_ctx* ctx, int level, size_t n, const uint8_t* rho_primes /* n*64 */,
+                        const uint32_t* kappas /* n */, int32_t* out /* n*L*256 */);
+int dlb_dbg_sample_in_ball(dlb_ctx* ctx, int level, size_t n, const uint8_t* c_tildes /* n*32 */,
+                           int8_t* out /* n*256 */);
+/* forward NTT (output canonical [0,q)) and inverse NTT of canonical input (output
+ * canonical): value-level parity with ntt.hpp:74-126 */
+int dlb_dbg_ntt(dlb_ctx* ctx, size_t n, int32_t* polys /* n*256 in place */, int inverse);
+/* sign_attempt<P> (scheme.hpp:225-230): one rejection-loop iteration per task at kappa[i].
+ * accepted[i] 0/1; c_tilde n*32; z n*L*256 centered; hints n*K*256 -- the latter two
+ * are meaningful for accepted attempts. */
+int dlb_dbg_sign_attempt(dlb_ctx* ctx, int level, size_t n, const uint8_t* sks, size_t sk_stride,
+                         const uint8_t* mus /* n*64 */, const uint8_t* rho_primes /* n*64 */,
+                         const uint32_t* kappas, uint8_t* accepted, uint8_t* c_tilde, int32_t* z,
+                         int32_t* hints);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,440 @@
+// engine.cu -- C ABI (include/dilithium_b200.h): context, host<->device marshalling,
+// level dispatch, and the stage-level entry points used by the device parity tests.
+#include "engine.cuh"
+#include "ntt.cuh"
+#include "samplers.cuh"
+
+using namespace dlb;
+
+namespace {
+
+template <class Fn>
+int with_level(int level, Fn&& fn) {
+  switch (level) {
+    case 2: return fn(Params<2>{});
+    case 3: return fn(Params<3>{});
+    case 5: return fn(Params<5>{});
+    default: return DLB_E_LEVEL;
+  }
+}
+
+struct LevelSizes {
+  size_t pk, sk, sig;
+  int k, l;
+};
+
+bool level_sizes(int level, LevelSizes* o) {
+  return with_level(level, [&](auto p) {
+           using P = decltype(p);
+           *o = {Sizes<P>::PK, Sizes<P>::SK, Sizes<P>::SIG, P::K, P::L};
+           return 0;
+         }) == 0;
+}
+
+struct Timed {
+  dlb_ctx* c;
+  explicit Timed(dlb_ctx* ctx) : c(ctx) {
+    c->launches = 0;
+    cudaEventRecord(c->ev0, c->s());
+  }
+  int finish() {
+    cudaEventRecord(c->ev1, c->s());
+    const cudaError_t e = cudaStreamSynchronize(c->s());
+    if (e != cudaSuccess) return -1000 - (int)e;
+    cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+    return 0;
+  }
+};
+
+int h2d(dlb_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return 0;
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->s());
+  return e == cudaSuccess ? 0 : -1000 - (int)e;
+}
+
+int d2h(dlb_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return 0;
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->s());
+  return e == cudaSuccess ? 0 : -1000 - (int)e;
+}
+
+int sync(dlb_ctx* c) {
+  const cudaError_t e = cudaStreamSynchronize(c->s());
+  return e == cudaSuccess ? 0 : -1000 - (int)e;
+}
+
+// ---- stage-level kernels (parity tests) ------------------------------------------
+
+__global__ void k_dbg_keccak(unsigned n, uint64_t* states) {
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  uint64_t s[25];
+#pragma unroll
+  for (int i = 0; i < 25; ++i) s[i] = states[(size_t)t * 25 + i];
+  keccak_f1600(s);
+#pragma unroll
+  for (int i = 0; i < 25; ++i) states[(size_t)t * 25 + i] = s[i];
+}
+
+__global__ void k_dbg_shake256(unsigned n, const uint8_t* msgs, const uint64_t* off, uint64_t* out) {
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  uint64_t s[25];
+  keccak_clear(s);
+  const uint8_t* m = msgs + off[t];
+  const size_t len = (size_t)(off[t + 1] - off[t]);
+  const size_t nblocks = len / kRate256 + 1;
+  for (size_t blk = 0; blk < nblocks; ++blk) {
+#pragma unroll
+    for (int w = 0; w < kWords256; ++w) s[w] ^= padded_word(m, len, blk * kRate256 + 8 * w);
+    if (blk == nblocks - 1) s[kWords256 - 1] ^= 0x8000000000000000ull;
+    keccak_f1600(s);
+  }
+#pragma unroll
+  for (int w = 0; w < 8; ++w) out[(size_t)t * 8 + w] = s[w];
+}
+
+template <class P, int WARPS>
+__global__ void k_dbg_expand_mask(unsigned n, const uint64_t* rho_primes, const uint32_t* kappas,
+                                  uint8_t* ybytes) {
+  const unsigned p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n * P::L) return;
+  const unsigned a = p / P::L, j = p % P::L;
+  expand_mask_stream<P>(rho_primes + (size_t)a * 8, kappas[a] + j,
+                        ybytes + (size_t)p * Sizes<P>::Z_POLY);
+}
+
+template <class P>
+__global__ void k_dbg_unpack_mask(unsigned n_polys, const uint8_t* ybytes, int32_t* out) {
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_polys * kN) return;
+  const unsigned p = i / kN, cidx = i % kN;
+  out[i] = P::GAMMA1 - (int32_t)load_bits(ybytes + (size_t)p * Sizes<P>::Z_POLY,
+                                           cidx * P::Z_BITS, P::Z_BITS);
+}
+
+__global__ void k_dbg_ntt(unsigned n, int32_t* polys, int inverse) {
+  __shared__ int2 zs[256], nzs[256];
+  __shared__ __align__(16) int32_t tiles[4][kTileWords];
+  load_twiddles(zs, nzs);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned t = blockIdx.x * 4 + warp;
+  if (t >= n) return;
+  int32_t* a = polys + (size_t)t * kN;
+  int32_t r[8];
+  if (!inverse) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = a[lane + 32 * i];
+    ntt_fwd(r, tiles[warp], zs, lane);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) a[8 * lane + m] = freeze(r[m]);
+  } else {
+    // the inverse carries an extra factor R (see ntt.cuh); undo it for the value test
+#pragma unroll
+    for (int m = 0; m < 8; ++m) r[m] = center(a[8 * lane + m]);
+    ntt_inv(r, tiles[warp], nzs, lane);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[lane + 32 * i] = freeze(mont_mul(r[i], 1));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dlb_version(void) { return "dilithium-b200 0.1 (sm_100a)"; }
+
+int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
+  (void)max_batch;
+  if (!out) return DLB_E_ARG;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess) return -1000 - (int)e;
+  if (device < 0 || device >= count) return DLB_E_ARG;
+  DLB_CUDA_CHECK(cudaSetDevice(device));
+  dlb_ctx* c = new dlb_ctx();
+  c->device = device;
+  DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
+  DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+  DLB_CUDA_CHECK(cudaEventCreate(&c->ev0));
+  DLB_CUDA_CHECK(cudaEventCreate(&c->ev1));
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  *out = c;
+  return 0;
+}
+
+void dlb_destroy(dlb_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->dev)
+    if (kv.second.p) cudaFree(kv.second.p);
+  for (auto& kv : c->pinned)
+    if (kv.second.p) cudaFreeHost(kv.second.p);
+  cudaEventDestroy(c->ev0);
+  cudaEventDestroy(c->ev1);
+  cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->copy_in);
+  cudaStreamDestroy(c->copy_out);
+  delete c;
+}
+
+float dlb_last_kernel_ms(const dlb_ctx* c) { return c ? c->last_ms : 0.f; }
+unsigned dlb_last_launches(const dlb_ctx* c) { return c ? c->launches : 0; }
+
+int dlb_set_stream(dlb_ctx* c, void* cuda_stream) {
+  if (!c) return DLB_E_ARG;
+  c->ext = static_cast<cudaStream_t>(cuda_stream);
+  return 0;
+}
+
+// ---- device-resident ---------------------------------------------------------------
+
+int dlb_keygen_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_zetas, uint8_t* d_pks,
+                         uint8_t* d_sks) {
+  if (!c || (n && (!d_zetas || !d_pks || !d_sks))) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  Timed tm(c);
+  DLB_TRY(with_level(level, [&](auto p) {
+    return keygen_dev<decltype(p)>(c, n, d_zetas, d_pks, d_sks);
+  }));
+  return tm.finish();
+}
+
+int dlb_verify_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_pks, size_t pk_stride,
+                         const uint8_t* d_msgs, const uint64_t* d_msg_off, const uint8_t* d_sigs,
+                         uint8_t* d_flags) {
+  if (!c || (n && (!d_pks || !d_msg_off || !d_sigs || !d_flags))) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  Timed tm(c);
+  DLB_TRY(with_level(level, [&](auto p) {
+    return verify_dev<decltype(p)>(c, n, d_pks, pk_stride, d_msgs, d_msg_off, d_sigs, d_flags);
+  }));
+  return tm.finish();
+}
+
+int dlb_sign_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_sks, size_t sk_stride,
+                       const uint8_t* d_msgs, const uint64_t* d_msg_off,
+                       const uint8_t* d_rho_prime, size_t psi, int speculate, uint8_t* d_sigs,
+                       uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats) {
+  if (!c || (n && (!d_sks || !d_msg_off || !d_sigs))) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  Timed tm(c);
+  DLB_TRY(with_level(level, [&](auto p) {
+    return sign_dev<decltype(p)>(c, n, d_sks, sk_stride, d_msgs, d_msg_off, d_rho_prime, psi,
+                                 speculate, d_sigs, d_attempts, d_failed, stats);
+  }));
+  return tm.finish();
+}
+
+// ---- host-buffer API -----------------------------------------------------------------
+
+int dlb_keygen_batch(dlb_ctx* c, int level, size_t n, const uint8_t* zetas, uint8_t* pks,
+                     uint8_t* sks) {
+  LevelSizes ls;
+  if (!c) return DLB_E_ARG;
+  if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
+  if (n == 0) return 0;
+  if (!zetas || !pks || !sks) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  uint8_t *dz, *dpk, *dsk;
+  DLB_TRY(dalloc(c, "io.zeta", n * 32, &dz));
+  DLB_TRY(dalloc(c, "io.pk", n * ls.pk, &dpk));
+  DLB_TRY(dalloc(c, "io.sk", n * ls.sk, &dsk));
+  DLB_TRY(h2d(c, dz, zetas, n * 32));
+  DLB_TRY(dlb_keygen_batch_dev(c, level, n, dz, dpk, dsk));
+  DLB_TRY(d2h(c, pks, dpk, n * ls.pk));
+  DLB_TRY(d2h(c, sks, dsk, n * ls.sk));
+  return sync(c);
+}
+
+int dlb_verify_batch(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_stride,
+                     const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* sigs,
+                     uint8_t* flags) {
+  LevelSizes ls;
+  if (!c) return DLB_E_ARG;
+  if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
+  if (n == 0) return 0;
+  if (!pks || !msg_off || !sigs || !flags) return DLB_E_ARG;
+  if (pk_stride != 0 && pk_stride != ls.pk) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  const size_t mbytes = msg_off[n];
+  const size_t nk = pk_stride ? n : 1;
+  uint8_t *dpk, *dm, *dsig, *dfl;
+  uint64_t* doff;
+  DLB_TRY(dalloc(c, "io.pk", nk * ls.pk, &dpk));
+  DLB_TRY(dalloc(c, "io.msg", mbytes + 8, &dm));
+  DLB_TRY(dalloc(c, "io.off", n + 1, &doff));
+  DLB_TRY(dalloc(c, "io.sig", n * ls.sig + 8, &dsig));
+  DLB_TRY(dalloc(c, "io.flag", n, &dfl));
+  DLB_TRY(h2d(c, dpk, pks, nk * ls.pk));
+  DLB_TRY(h2d(c, dm, msgs, mbytes));
+  DLB_TRY(h2d(c, doff, msg_off, (n + 1) * 8));
+  DLB_TRY(h2d(c, dsig, sigs, n * ls.sig));
+  DLB_TRY(dlb_verify_batch_dev(c, level, n, dpk, pk_stride, dm, doff, dsig, dfl));
+  DLB_TRY(d2h(c, flags, dfl, n));
+  return sync(c);
+}
+
+int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride,
+                   const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* rho_prime,
+                   size_t psi, int speculate, uint8_t* sigs, uint32_t* attempts, uint8_t* failed,
+                   dlb_sign_stats* stats) {
+  LevelSizes ls;
+  if (!c) return DLB_E_ARG;
+  if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
+  if (stats) memset(stats, 0, sizeof *stats);
+  if (n == 0) return 0;
+  if (!sks || !msg_off || !sigs) return DLB_E_ARG;
+  if (sk_stride != 0 && sk_stride != ls.sk) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  const size_t mbytes = msg_off[n];
+  const size_t nk = sk_stride ? n : 1;
+  uint8_t *dsk, *dm, *dsig, *dfail, *drp = nullptr;
+  uint64_t* doff;
+  uint32_t* datt;
+  DLB_TRY(dalloc(c, "io.sk", nk * ls.sk, &dsk));
+  DLB_TRY(dalloc(c, "io.msg", mbytes + 8, &dm));
+  DLB_TRY(dalloc(c, "io.off", n + 1, &doff));
+  DLB_TRY(dalloc(c, "io.sig", n * ls.sig + 8, &dsig));
+  DLB_TRY(dalloc(c, "io.att", n, &datt));
+  DLB_TRY(dalloc(c, "io.fail", n, &dfail));
+  DLB_TRY(h2d(c, dsk, sks, nk * ls.sk));
+  DLB_TRY(h2d(c, dm, msgs, mbytes));
+  DLB_TRY(h2d(c, doff, msg_off, (n + 1) * 8));
+  if (rho_prime) {
+    DLB_TRY(dalloc(c, "io.rp", n * 64, &drp));
+    DLB_TRY(h2d(c, drp, rho_prime, n * 64));
+  }
+  DLB_TRY(dlb_sign_batch_dev(c, level, n, dsk, sk_stride, dm, doff, drp, psi, speculate, dsig, datt,
+                             dfail, stats));
+  DLB_TRY(d2h(c, sigs, dsig, n * ls.sig));
+  if (attempts) DLB_TRY(d2h(c, attempts, datt, n * 4));
+  if (failed) DLB_TRY(d2h(c, failed, dfail, n));
+  return sync(c);
+}
+
+// ---- stage-level entry points -----------------------------------------------------------
+
+int dlb_dbg_keccak_f1600(dlb_ctx* c, size_t n, uint64_t* states) {
+  if (!c || !states) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  uint64_t* d;
+  DLB_TRY(dalloc(c, "dbg.a", n * 25, &d));
+  DLB_TRY(h2d(c, d, states, n * 200));
+  k_dbg_keccak<<<cdiv(n, 128), 128, 0, c->s()>>>((unsigned)n, d);
+  DLB_LAUNCH_CHECK();
+  DLB_TRY(d2h(c, states, d, n * 200));
+  return sync(c);
+}
+
+int dlb_dbg_shake256(dlb_ctx* c, size_t n, const uint8_t* msgs, const uint64_t* msg_off,
+                     uint8_t* out64) {
+  if (!c || !msg_off || !out64) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  uint8_t* dm;
+  uint64_t *doff, *dout;
+  DLB_TRY(dalloc(c, "dbg.a", msg_off[n] + 8, &dm));
+  DLB_TRY(dalloc(c, "dbg.b", n + 1, &doff));
+  DLB_TRY(dalloc(c, "dbg.c", n * 8, &dout));
+  DLB_TRY(h2d(c, dm, msgs, msg_off[n]));
+  DLB_TRY(h2d(c, doff, msg_off, (n + 1) * 8));
+  k_dbg_shake256<<<cdiv(n, 128), 128, 0, c->s()>>>((unsigned)n, dm, doff, dout);
+  DLB_LAUNCH_CHECK();
+  DLB_TRY(d2h(c, out64, dout, n * 64));
+  return sync(c);
+}
+
+int dlb_dbg_expand_a(dlb_ctx* c, int level, size_t n_keys, const uint8_t* rhos, int32_t* out) {
+  if (!c || !rhos || !out) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  return with_level(level, [&](auto p) {
+    using P = decltype(p);
+    const size_t streams = n_keys * P::K * P::L;
+    uint8_t* dr;
+    int32_t* dout;
+    DLB_TRY(dalloc(c, "dbg.a", n_keys * 32, &dr));
+    DLB_TRY(dalloc(c, "dbg.b", streams * kN, &dout));
+    DLB_TRY(h2d(c, dr, rhos, n_keys * 32));
+    k_expand_a<P, 4><<<cdiv(streams, 128), 128, 0, c->s()>>>(dr, 32, (unsigned)streams, dout);
+    DLB_LAUNCH_CHECK();
+    DLB_TRY(d2h(c, out, dout, streams * kN * 4));
+    return sync(c);
+  });
+}
+
+int dlb_dbg_expand_s(dlb_ctx* c, int level, size_t n, const uint8_t* rho_primes, int8_t* out) {
+  if (!c || !rho_primes || !out) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  return with_level(level, [&](auto p) {
+    using P = decltype(p);
+    const size_t streams = n * (P::K + P::L);
+    uint8_t* dr;
+    int8_t* dout;
+    DLB_TRY(dalloc(c, "dbg.a", n * 64, &dr));
+    DLB_TRY(dalloc(c, "dbg.b", streams * kN, &dout));
+    DLB_TRY(h2d(c, dr, rho_primes, n * 64));
+    k_expand_s<P, 4><<<cdiv(streams, 128), 128, 0, c->s()>>>(dr, 64, (unsigned)streams, dout);
+    DLB_LAUNCH_CHECK();
+    DLB_TRY(d2h(c, out, dout, streams * kN));
+    return sync(c);
+  });
+}
+
+int dlb_dbg_expand_mask(dlb_ctx* c, int level, size_t n, const uint8_t* rho_primes,
+                        const uint32_t* kappas, int32_t* out) {
+  if (!c || !rho_primes || !kappas || !out) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  return with_level(level, [&](auto p) {
+    using P = decltype(p);
+    const size_t polys = n * P::L;
+    uint64_t* dr;
+    uint32_t* dk;
+    uint8_t* dy;
+    int32_t* dout;
+    DLB_TRY(dalloc(c, "dbg.a", n * 8, &dr));
+    DLB_TRY(dalloc(c, "dbg.b", n, &dk));
+    DLB_TRY(dalloc(c, "dbg.c", polys * Sizes<P>::Z_POLY + 8, &dy));
+    DLB_TRY(dalloc(c, "dbg.d", polys * kN, &dout));
+    DLB_TRY(h2d(c, dr, rho_primes, n * 64));
+    DLB_TRY(h2d(c, dk, kappas, n * 4));
+    k_dbg_expand_mask<P, 4><<<cdiv(polys, 128), 128, 0, c->s()>>>((unsigned)n, dr, dk, dy);
+    k_dbg_unpack_mask<P><<<cdiv(polys * kN, 256), 256, 0, c->s()>>>((unsigned)polys, dy, dout);
+    DLB_LAUNCH_CHECK();
+    DLB_TRY(d2h(c, out, dout, polys * kN * 4));
+    return sync(c);
+  });
+}
+
+int dlb_dbg_sample_in_ball(dlb_ctx* c, int level, size_t n, const uint8_t* c_tildes, int8_t* out) {
+  if (!c || !c_tildes || !out) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  return with_level(level, [&](auto p) {
+    using P = decltype(p);
+    uint8_t* dc;
+    int8_t* dout;
+    DLB_TRY(dalloc(c, "dbg.a", n * 32, &dc));
+    DLB_TRY(dalloc(c, "dbg.b", n * kN, &dout));
+    DLB_TRY(h2d(c, dc, c_tildes, n * 32));
+    k_sample_in_ball<P, 4><<<cdiv(n, 128), 128, 0, c->s()>>>(dc, 32, (unsigned)n, dout);
+    DLB_LAUNCH_CHECK();
+    DLB_TRY(d2h(c, out, dout, n * kN));
+    return sync(c);
+  });
+}
+
+int dlb_dbg_ntt(dlb_ctx* c, size_t n, int32_t* polys, int inverse) {
+  if (!c || !polys) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  int32_t* d;
+  DLB_TRY(dalloc(c, "dbg.a", n * kN, &d));
+  DLB_TRY(h2d(c, d, polys, n * kN * 4));
+  k_dbg_ntt<<<cdiv(n, 4), 128, 0, c->s()>>>((unsigned)n, d, inverse);
+  DLB_LAUNCH_CHECK();
+  DLB_TRY(d2h(c, polys, d, n * kN * 4));
+  return sync(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// engine.cuh -- host-side context shared by the translation units of libdilithium_b200.
+//
+// Plays the role of the reference's MemoryPool + WorkerPool (memory_pool.hpp:25-100,
+// thread_pool.hpp) for the GPU: device arenas that are allocated once and grown on
+// demand, pinned host staging, streams and events.  Nothing here is per-call.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+
+#include "../../include/dilithium_b200.h"
+#include "common.cuh"
+
+namespace dlb {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+}  // namespace dlb
+
+struct dlb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;      // engine-owned compute stream
+  cudaStream_t copy_in = nullptr;     // H2D stream
+  cudaStream_t copy_out = nullptr;    // D2H stream
+  cudaStream_t ext = nullptr;         // caller's stream for *_dev calls (optional)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.f;
+  unsigned launches = 0;
+  int sm_count = 148;
+  std::map<std::string, dlb::DevBuf> dev;
+  std::map<std::string, dlb::HostBuf> pinned;
+
+  cudaStream_t s() const { return ext ? ext : stream; }
+
+  // 256-byte aligned device arena slot (memory_pool.hpp:27 kArenaAlign), grown geometrically
+  int dbuf(const char* name, size_t bytes, void** out) {
+    dlb::DevBuf& b = dev[name];
+    if (b.cap < bytes) {
+      if (b.p) {
+        cudaStreamSynchronize(s());
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+      }
+      size_t want = bytes + bytes / 4 + 256;
+      cudaError_t e = cudaMalloc(&b.p, want);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        e = cudaMalloc(&b.p, bytes + 256);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          return DLB_E_NOMEM;
+        }
+        want = bytes + 256;
+      }
+      b.cap = want;
+    }
+    *out = b.p;
+    return 0;
+  }
+
+  int hbuf(const char* name, size_t bytes, void** out) {
+    dlb::HostBuf& b = pinned[name];
+    if (b.cap < bytes) {
+      if (b.p) cudaFreeHost(b.p);
+      b.p = nullptr;
+      b.cap = 0;
+      const size_t want = bytes + bytes / 4 + 256;
+      if (cudaHostAlloc(&b.p, want, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return DLB_E_NOMEM;
+      }
+      b.cap = want;
+    }
+    *out = b.p;
+    return 0;
+  }
+};
+
+namespace dlb {
+
+template <class T>
+inline int dalloc(dlb_ctx* c, const char* name, size_t count, T** out) {
+  void* p = nullptr;
+  const int rc = c->dbuf(name, count * sizeof(T), &p);
+  *out = static_cast<T*>(p);
+  return rc;
+}
+
+inline unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
+
+#define DLB_TRY(x)            \
+  do {                        \
+    const int rc_ = (x);      \
+    if (rc_ != 0) return rc_; \
+  } while (0)
+
+#define DLB_LAUNCH_CHECK()                                   \
+  do {                                                       \
+    const cudaError_t e_ = cudaGetLastError();               \
+    if (e_ != cudaSuccess) return -1000 - (int)e_;           \
+  } while (0)
+
+// per-level device-resident implementations (keygen.cu / verify.cu / sign.cu)
+template <class P>
+int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uint8_t* d_sks);
+template <class P>
+int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, const uint8_t* d_msgs,
+               const uint64_t* d_msg_off, const uint8_t* d_sigs, uint8_t* d_flags);
+template <class P>
+int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, const uint8_t* d_msgs,
+             const uint64_t* d_msg_off, const uint8_t* d_rho_prime, size_t psi, int speculate,
+             uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats);
+
+}  // namespace dlb

@@ -1,0 +1,51 @@
+// keygen.cu -- batched key generation pipeline (scheme.hpp:68-104, batch.hpp:159-166).
+//
+//   k_keygen_seed   n sponges            zeta -> rho | rho' | K     (scheme.hpp:70-76)
+//   k_expand_s      n*(L+K) sponges      -> s1, s2 (int8)           (sampling.hpp:61-79)
+//   k_expand_a      n*K*L sponges        -> A                       (sampling.hpp:42-56)
+//   k_keygen_arith  one warp per task    -> pk, sk (minus tr)       (scheme.hpp:84-101,103)
+//   k_hash_tr       n sponges            pk -> tr into sk           (scheme.hpp:102)
+#include "engine.cuh"
+#include "samplers.cuh"
+#include "verify_keygen.cuh"
+
+namespace dlb {
+
+constexpr size_t kKeygenChunk = 16384;
+
+template <class P>
+int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uint8_t* d_sks) {
+  using S = Sizes<P>;
+  constexpr int KL = P::K * P::L, PV = P::K + P::L;
+  constexpr int HW = 4;
+  if (n == 0) return 0;
+  cudaStream_t st = c->s();
+  const size_t chunk = n < kKeygenChunk ? n : kKeygenChunk;
+  uint64_t* seeds;
+  int8_t* s8;
+  int32_t* A;
+  DLB_TRY(dalloc(c, "g.seeds", chunk * 16, &seeds));
+  DLB_TRY(dalloc(c, "g.s8", chunk * PV * kN, &s8));
+  DLB_TRY(dalloc(c, "g.A", chunk * KL * kN, &A));
+  const uint8_t* seedb = reinterpret_cast<const uint8_t*>(seeds);
+  for (size_t lo = 0; lo < n; lo += chunk) {
+    const size_t cnt = n - lo < chunk ? n - lo : chunk;
+    uint8_t* pks = d_pks + lo * S::PK;
+    uint8_t* sks = d_sks + lo * S::SK;
+    k_keygen_seed<<<cdiv(cnt, 128), 128, 0, st>>>(d_zetas + lo * 32, (unsigned)cnt, seeds);
+    k_expand_s<P, HW><<<cdiv(cnt * PV, HW * 32), HW * 32, 0, st>>>(seedb + 32, 128,
+                                                                    (unsigned)(cnt * PV), s8);
+    k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(seedb, 128, (unsigned)(cnt * KL), A);
+    k_keygen_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>((unsigned)cnt, seedb, s8, A, pks, sks);
+    k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, S::PK, S::PK, (unsigned)cnt, sks + 64, S::SK);
+    c->launches += 5;
+    DLB_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+template int keygen_dev<Params<2>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
+template int keygen_dev<Params<3>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
+template int keygen_dev<Params<5>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
+
+}  // namespace dlb

@@ -1,0 +1,124 @@
+"""Device parity of the building blocks, through the C ABI's stage-level entry points,
+against the CPU oracle (and the compiled reference where it travelled).  -m gpu."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from tests.cpu_checkers import PARAMS, Q, mt19937_64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_2211_12265_b200 import Engine
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+def test_keccak_permutation(eng, oracle, kat):
+    rng = np.random.default_rng(1)
+    states = rng.integers(0, 2**63, (300, 25), dtype=np.uint64) * 2 + rng.integers(0, 2, (300, 25), dtype=np.uint64)
+    states[0] = 0
+    states[1] = np.array(kat["kKeccakRandIn"], dtype=np.uint64)
+    out = eng.dbg_keccak_f1600(states)
+    assert [int(v) for v in out[0]] == kat["kKeccakZeroState"]
+    assert [int(v) for v in out[1]] == kat["kKeccakRandOut"]
+    for i in range(2, 300):
+        assert np.array_equal(out[i], oracle.keccak_f1600(states[i]))
+
+
+def test_shake256_lengths(eng, kat):
+    rng = mt19937_64(2)
+    lens = [0, 1, 7, 8, 9, 31, 32, 33, 63, 64, 100, 135, 136, 137, 200, 271, 272, 273, 407, 408, 1312, 2592, 5000]
+    msgs = [rng.bytes(n) for n in lens] + [b"\xa3" * 200]
+    out = eng.dbg_shake256(msgs)
+    for m, o in zip(msgs, out):
+        assert o.tobytes() == hashlib.shake_256(m).digest(64), len(m)
+    assert out[-1].tobytes().hex() == kat["kShake256Msg1600"]
+    assert out[0].tobytes().hex() == kat["kShake256Empty"]
+
+
+@pytest.mark.parametrize("level", [2, 3, 5])
+def test_expand_a(eng, oracle, kat, level):
+    P = PARAMS[level]
+    rng = mt19937_64(30 + level)
+    n = 11
+    rhos = np.frombuffer(rng.bytes(32 * n), np.uint8).reshape(n, 32).copy()
+    rhos[0] = 0
+    out = eng.dbg_expand_a(level, rhos)
+    assert out[0, 0, 0].tolist() == kat["kExpandA_r0_00"]
+    assert out[0, 1, 2].tolist() == kat["kExpandA_r0_12"]
+    for t in range(n):
+        for i in range(P["k"]):
+            for j in range(P["l"]):
+                assert np.array_equal(out[t, i, j], oracle.expand_a(rhos[t].tobytes(), i, j)), (t, i, j)
+
+
+@pytest.mark.parametrize("level", [2, 3, 5])
+def test_expand_s(eng, oracle, kat, level):
+    P = PARAMS[level]
+    rng = mt19937_64(40 + level)
+    n = 13
+    rps = np.frombuffer(rng.bytes(64 * n), np.uint8).reshape(n, 64).copy()
+    rps[0] = np.arange(64, dtype=np.uint8)
+    out = eng.dbg_expand_s(level, rps)
+    if P["eta"] == 2:
+        assert out[0, 0].tolist() == kat["kExpandS_eta2_n0"]
+        assert out[0, 7].tolist() == kat["kExpandS_eta2_n7"]
+    else:
+        assert out[0, 0].tolist() == kat["kExpandS_eta4_n0"]
+    for t in range(n):
+        for r in range(P["k"] + P["l"]):
+            assert np.array_equal(out[t, r], oracle.expand_s(rps[t].tobytes(), r, P["eta"])), (t, r)
+
+
+@pytest.mark.parametrize("level", [2, 3, 5])
+def test_expand_mask(eng, oracle, kat, level):
+    P = PARAMS[level]
+    rng = mt19937_64(50 + level)
+    n = 37
+    rps = np.frombuffer(rng.bytes(64 * n), np.uint8).reshape(n, 64).copy()
+    rps[0] = np.arange(64, dtype=np.uint8)
+    kappas = np.array([0, 65535, 65533] + [int(rng()) % 60000 for _ in range(n - 3)], np.uint32)
+    out = eng.dbg_expand_mask(level, rps, kappas)
+    if level == 2:
+        assert out[0, 0].tolist() == kat["kExpandMask_g17_n0"]
+        assert out[0, 3].tolist() == kat["kExpandMask_g17_n3"]
+    else:
+        assert out[0, 0].tolist() == kat["kExpandMask_g19_n0"]
+    for t in range(n):
+        for j in range(P["l"]):
+            exp = oracle.expand_mask(rps[t].tobytes(), (int(kappas[t]) + j) & 0xFFFF, P["gamma1"], P["z_bits"])
+            assert np.array_equal(out[t, j], exp), (t, j)
+
+
+@pytest.mark.parametrize("level", [2, 3, 5])
+def test_sample_in_ball(eng, oracle, kat, level):
+    P = PARAMS[level]
+    rng = mt19937_64(60 + level)
+    n = 200
+    cts = np.frombuffer(rng.bytes(32 * n), np.uint8).reshape(n, 32).copy()
+    cts[0] = np.arange(32, dtype=np.uint8)
+    out = eng.dbg_sample_in_ball(level, cts)
+    assert out[0].tolist() == kat["kBall_tau%d" % P["tau"]]
+    for t in range(n):
+        assert np.array_equal(out[t], oracle.sample_in_ball(cts[t].tobytes(), P["tau"])), t
+
+
+def test_ntt_values(eng, oracle):
+    rng = np.random.default_rng(7)
+    a = rng.integers(0, Q, (64, 256), dtype=np.int32)
+    a[0] = 0
+    a[1] = Q - 1
+    a[2] = np.arange(256)
+    f = eng.dbg_ntt(a)
+    for i in range(len(a)):
+        assert np.array_equal(f[i], oracle.ntt(a[i])), i
+    g = eng.dbg_ntt(f, inverse=True)
+    assert np.array_equal(g, a)
+    b = eng.dbg_ntt(a, inverse=True)
+    for i in range(len(a)):
+        assert np.array_equal(b[i], oracle.intt(a[i])), i
