@@ -184,12 +184,12 @@ __device__ __forceinline__ void expand_mask_stream(const uint64_t* __restrict__ 
 // memory.  Squeezed bytes are consumed straight from the state registers (static
 // indices; every lane walks all byte positions under predication).
 template <int TAU>
-__device__ __forceinline__ void sample_in_ball_stream(const uint8_t* __restrict__ c_tilde,
-                                                      int8_t* row /* smem, 256 entries */) {
+__device__ __forceinline__ void sample_in_ball_words(const uint64_t (&ct)[4],
+                                                     int8_t* row /* smem, 256 entries */) {
   uint64_t s[25];
   keccak_clear(s);
 #pragma unroll
-  for (int w = 0; w < 4; ++w) s[w] = load_u64_unaligned(c_tilde + 8 * w);
+  for (int w = 0; w < 4; ++w) s[w] = ct[w];
   s[4] = 0x1F;
   s[16] = 0x8000000000000000ull;
   uint32_t* row32 = reinterpret_cast<uint32_t*>(row);
@@ -219,6 +219,15 @@ __device__ __forceinline__ void sample_in_ball_stream(const uint8_t* __restrict_
     first = false;
     keccak_f1600(s);
   }
+}
+
+template <int TAU>
+__device__ __forceinline__ void sample_in_ball_stream(const uint8_t* __restrict__ c_tilde,
+                                                      int8_t* row) {
+  uint64_t ct[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) ct[w] = load_u64_unaligned(c_tilde + 8 * w);
+  sample_in_ball_words<TAU>(ct, row);
 }
 
 template <class P, int WARPS>

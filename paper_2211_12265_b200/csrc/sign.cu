@@ -1,13 +1,694 @@
-// sign.cu -- placeholder until the persistent signing kernel lands
+// sign.cu -- batched signing: per-key precomputation, message digests, and the
+// persistent rejection-loop kernel with its device-side nonce scheduler.
+//
+// Reference semantics: scheme.hpp:106-125 (make_precomp), :133-219 (one attempt),
+// :240-266 (mu, rho', the kappa loop); batch.hpp:53-137 (batch_sign);
+// scheduler.hpp:44-186 (NonceScheduler: one next-nonce attempt per open task, then
+// breadth-first speculation; smallest valid nonce wins once all smaller are resolved).
+//
+// GPU design.  One persistent kernel; every CTA owns SLOTS attempt slots and a small
+// table of open tasks pulled from a global device work queue (atomic head counter).
+// A CTA round runs all its slots through four stages, each with the thread mapping
+// that suits it:
+//   S1  ExpandMask         one sponge per thread, L passes      (sampling.hpp:83-92)
+//   S2  w = A y, w1        one warp per slot                    (scheme.hpp:144-156)
+//   S3  c~ = H(mu||w1), c  one sponge per thread                (scheme.hpp:158-165)
+//   S4  z, r0, ct0, hints  one warp per slot, early abort       (scheme.hpp:167-215)
+// then commits: per task the smallest valid attempt of the round wins (all smaller
+// attempts of that task ran in this or earlier rounds and failed), its staged
+// signature is copied out, rejected tasks stay in the CTA's table with their nonce
+// advanced, and freed capacity is refilled from the global queue.  Slots left over
+// when the queue runs dry run speculative future nonces of the CTA's open tasks,
+// breadth first, exactly the reference's pass 2.  CTAs never wait on each other, so
+// variable repetition counts cannot idle an SM while work remains.
 #include "engine.cuh"
+#include "samplers.cuh"
+#include "verify_keygen.cuh"
+
 namespace dlb {
+
+constexpr int kSignThreads = 128;          // threads = attempt slots per CTA
+constexpr int kSignWarps = kSignThreads / 32;
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+
+// ---- per-key precomputation -----------------------------------------------------------
+// One warp per (key, polynomial): s1 (L), s2 (K), t0 (K) unpacked from the secret key,
+// range-checked (packing.hpp:79-86), transformed; stored reduced, natural order.
+template <class P, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    k_sign_unpack(unsigned n_keys, const uint8_t* __restrict__ sks, size_t sk_stride,
+                  int32_t* __restrict__ shat, unsigned* __restrict__ key_bad) {
+  using S = Sizes<P>;
+  constexpr int PV = P::L + 2 * P::K;
+  __shared__ int2 zs[256], nzs[256];
+  __shared__ __align__(16) int32_t tiles[WARPS][kTileWords];
+  load_twiddles(zs, nzs);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned id = blockIdx.x * WARPS + warp;
+  if (id >= n_keys * PV) return;
+  const unsigned key = id / PV, p = id % PV;
+  const uint8_t* sk = sks + (size_t)key * sk_stride;
+  int32_t r[8];
+  bool bad = false;
+  if (p < (unsigned)(P::L + P::K)) {
+    const uint8_t* src = sk + S::SK_S1 + p * S::ETA_POLY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t raw = load_bits(src, (lane + 32 * e) * P::ETA_BITS, P::ETA_BITS);
+      bad = bad || raw > 2u * P::ETA;
+      r[e] = P::ETA - (int32_t)raw;
+    }
+  } else {
+    const uint8_t* src = sk + S::SK_T0 + (p - P::L - P::K) * S::T0_POLY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      r[e] = 4096 - (int32_t)load_bits(src, (lane + 32 * e) * 13, 13);
+  }
+  ntt_fwd(r, tiles[warp], zs, lane);
+  int4* dst = reinterpret_cast<int4*>(shat + (size_t)id * kN) + 2 * lane;
+  dst[0] = make_int4(reduce32(r[0]), reduce32(r[1]), reduce32(r[2]), reduce32(r[3]));
+  dst[1] = make_int4(reduce32(r[4]), reduce32(r[5]), reduce32(r[6]), reduce32(r[7]));
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(key_bad, 1u);
+}
+
+// ---- device-side scheduler state -----------------------------------------------------
+
+struct SignQueue {
+  unsigned head;          // next unclaimed task of the batch (the device work queue)
+  unsigned key_bad;       // some secret key failed the eta range check
+  unsigned long long rounds, attempts, speculative, idle_slots, accepted_sum, failed;
+};
+
+struct SignArgs {
+  unsigned n;                 // tasks
+  unsigned tcap;              // max open tasks per CTA (<= slots)
+  unsigned max_attempt;       // (65535 - (L-1)) / L   (scheduler.hpp:52)
+  int speculate;
+  int single_round;           // stage-test mode: exactly one round, then fail open tasks
+  const uint64_t* mu;         // n * 8
+  const uint64_t* rho_prime;  // n * 8
+  const uint32_t* kappa0;     // nullable: first nonce per task (stage tests)
+  const int32_t* A;           // keys * K*L*256
+  const int32_t* shat;        // keys * (L+2K)*256
+  unsigned key_stride;        // 0 shared key, 1 per-task keys
+  // per-CTA scratch in HBM/L2, indexed [cta][slot]
+  uint8_t* ybytes;
+  int32_t* wbuf;
+  uint8_t* w1buf;
+  uint64_t* ctbuf;
+  int8_t* c8buf;
+  uint8_t* staging;
+  // outputs
+  uint8_t* sigs;
+  uint32_t* attempts_out;     // nullable
+  uint8_t* failed_out;        // nullable
+  uint8_t* dbg_ctilde;        // nullable: n*32, c~ of each task's first executed attempt
+  SignQueue* q;
+};
+
 template <class P>
-int sign_dev(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*, const uint64_t*,
-             const uint8_t*, size_t, int, uint8_t*, uint32_t*, uint8_t*, dlb_sign_stats*) {
-  return DLB_E_ARG;
+struct SignSizes {
+  using S = Sizes<P>;
+  static constexpr int Y_SLOT = P::L * S::Z_POLY;           // bytes
+  static constexpr int W_SLOT = P::K * kN;                  // int32
+  static constexpr int SIG_PAD = (S::SIG + 15) / 16 * 16;   // staging stride
+};
+
+template <class P>
+struct SignSmem {
+  int2 zs[256], nzs[256];
+  union {
+    WarpScratch<P> ws[kSignWarps];
+    int8_t rows[kSignThreads][kByteRowStride];
+  } u;
+  uint32_t utask[kSignThreads];    // open tasks of this CTA (compact)
+  uint32_t unext[kSignThreads];    // their next unresolved attempt ordinal
+  uint32_t slot_task[kSignThreads];     // global task id or kNoSlot
+  uint32_t slot_attempt[kSignThreads];
+  uint8_t slot_valid[kSignThreads];
+  int32_t winner[kSignThreads];    // per open task: winning slot, -1 none, -2 failed
+  uint32_t keep_pos[kSignThreads];
+  uint32_t warp_sums[kSignWarps];
+  unsigned U, newU, got, base;
+};
+
+// S2: w = INTT(A * NTT(y)), w1 = HighBits(w) packed (scheme.hpp:141-156)
+template <class P>
+__device__ __forceinline__ void stage_w(WarpScratch<P>& ws, const int2* zs, const int2* nzs,
+                                        int lane, const uint8_t* ybytes, const int32_t* A,
+                                        int32_t* wout, uint8_t* w1out) {
+  using S = Sizes<P>;
+  int32_t r[8];
+#pragma unroll 1
+  for (int j = 0; j < P::L; ++j) {
+    const uint8_t* yb = ybytes + j * S::Z_POLY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      r[e] = P::GAMMA1 - (int32_t)load_bits(yb, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
+    ntt_fwd(r, ws.tile, zs, lane);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) ws.vhat[j][m][lane] = r[m];
+  }
+#pragma unroll 1
+  for (int i = 0; i < P::K; ++i) {
+    int32_t acc[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) acc[m] = 0;
+#pragma unroll 1
+    for (int j = 0; j < P::L; ++j) {
+      const int4* ap = reinterpret_cast<const int4*>(A + (size_t)(i * P::L + j) * kN) + 2 * lane;
+      const int4 a0 = __ldg(ap), a1 = __ldg(ap + 1);
+      const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int m = 0; m < 8; ++m) acc[m] += mont_mul(a[m], ws.vhat[j][m][lane]);
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) acc[m] = reduce32(acc[m]);
+    ntt_inv(acc, ws.tile, nzs, lane);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int32_t w = caddq(acc[e]);
+      wout[i * kN + lane + 32 * e] = w;
+      ws.tile[lane + 36 * e] = highbits<P::GAMMA2>(w);
+    }
+    __syncwarp();
+    pack_tile<P::W1_BITS>(ws.tile, ws.bytes, w1out + i * S::W1_POLY, lane);
+  }
 }
-template int sign_dev<Params<2>>(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*, const uint64_t*, const uint8_t*, size_t, int, uint8_t*, uint32_t*, uint8_t*, dlb_sign_stats*);
-template int sign_dev<Params<3>>(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*, const uint64_t*, const uint8_t*, size_t, int, uint8_t*, uint32_t*, uint8_t*, dlb_sign_stats*);
-template int sign_dev<Params<5>>(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*, const uint64_t*, const uint8_t*, size_t, int, uint8_t*, uint32_t*, uint8_t*, dlb_sign_stats*);
+
+// c * shat_p -> INTT, result at coefficient lane + 32 e, in (-q, q)
+__device__ __forceinline__ void mul_challenge(int32_t (&out)[8], const int32_t (&ch)[8],
+                                              const int32_t* shat_poly, int32_t* tile,
+                                              const int2* nzs, int lane) {
+  const int4* sp = reinterpret_cast<const int4*>(shat_poly) + 2 * lane;
+  const int4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
+  const int32_t s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+  for (int m = 0; m < 8; ++m) out[m] = mont_mul(ch[m], s[m]);
+  ntt_inv(out, tile, nzs, lane);
 }
-extern "C" int dlb_dbg_sign_attempt(dlb_ctx*, int, size_t, const uint8_t*, size_t, const uint8_t*, const uint8_t*, const uint32_t*, uint8_t*, uint8_t*, int32_t*, int32_t*) { return DLB_E_ARG; }
+
+// S4: everything after the challenge (scheme.hpp:165-215) + signature packing into the
+// slot's staging buffer (packing.hpp:236-254).  Warp-uniform return: accepted?
+template <class P>
+__device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, const int2* zs, const int2* nzs,
+                                             int lane, const uint8_t* ybytes, const int32_t* win,
+                                             const int8_t* c8, const uint64_t* ct,
+                                             const int32_t* shat, uint8_t* stage_sig) {
+  using S = Sizes<P>;
+  constexpr unsigned FULL = 0xffffffffu;
+  int32_t ch[8], t[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) ch[e] = c8[lane + 32 * e];
+  ntt_fwd(ch, ws.tile, zs, lane);
+
+  // z = y + c s1, ||z|| < gamma1 - beta  (scheme.hpp:167-174)
+#pragma unroll 1
+  for (int j = 0; j < P::L; ++j) {
+    mul_challenge(t, ch, shat + (size_t)j * kN, ws.tile, nzs, lane);
+    const uint8_t* yb = ybytes + j * S::Z_POLY;
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int32_t y = P::GAMMA1 - (int32_t)load_bits(yb, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
+      const int32_t z = center(freeze(y + t[e]));
+      bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
+      ws.vhat[j][e][lane] = z;
+    }
+    if (__any_sync(FULL, bad)) return false;
+  }
+  // r0 = LowBits(w - c s2), c t0, hints  (scheme.hpp:177-215), row by row
+  unsigned weight = 0;
+#pragma unroll 1
+  for (int i = 0; i < P::K; ++i) {
+    mul_challenge(t, ch, shat + (size_t)(P::L + i) * kN, ws.tile, nzs, lane);
+    int32_t wcs2[8], hb0[8];
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      wcs2[e] = freeze(win[i * kN + lane + 32 * e] - t[e]);
+      int32_t r0;
+      hb0[e] = decompose<P::GAMMA2>(wcs2[e], r0);
+      bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
+    }
+    if (__any_sync(FULL, bad)) return false;
+    mul_challenge(t, ch, shat + (size_t)(P::L + P::K + i) * kN, ws.tile, nzs, lane);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int32_t vt = center(caddq(t[e]));
+      bad = bad || abs(vt) >= P::GAMMA2;
+      const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != hb0[e];
+      const unsigned mask = __ballot_sync(FULL, h);
+      if (lane == 0) ws.hbits[i][e] = mask;
+      weight += __popc(mask);
+    }
+    if (__any_sync(FULL, bad)) return false;
+  }
+  if (weight > (unsigned)P::OMEGA) return false;
+
+  // accepted: c~ | z | hints into the staging slot
+  if (lane < 8) reinterpret_cast<uint32_t*>(stage_sig)[lane] =
+      reinterpret_cast<const uint32_t*>(ct)[lane];
+#pragma unroll 1
+  for (int j = 0; j < P::L; ++j) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ws.tile[lane + 36 * e] = P::GAMMA1 - ws.vhat[j][e][lane];
+    __syncwarp();
+    pack_tile<P::Z_BITS>(ws.tile, ws.bytes, stage_sig + 32 + j * S::Z_POLY, lane);
+  }
+  uint8_t* hint = stage_sig + 32 + P::L * S::Z_POLY;
+  for (int b = lane; b < S::HINT; b += 32) hint[b] = 0;
+  __syncwarp();
+  unsigned count = 0;
+#pragma unroll 1
+  for (int i = 0; i < P::K; ++i) {
+#pragma unroll 1
+    for (int e = 0; e < 8; ++e) {
+      const unsigned mask = ws.hbits[i][e];
+      if ((mask >> lane) & 1) hint[count + __popc(mask & ((1u << lane) - 1))] = (uint8_t)(32 * e + lane);
+      count += __popc(mask);
+    }
+    if (lane == 0) hint[P::OMEGA + i] = (uint8_t)count;
+  }
+  return true;
+}
+
+template <class P>
+__global__ void __launch_bounds__(kSignThreads, 4) k_sign_persistent(SignArgs a) {
+  using S = Sizes<P>;
+  using Z = SignSizes<P>;
+  __shared__ __align__(16) SignSmem<P> sm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t cta = blockIdx.x;
+  uint8_t* ybytes = a.ybytes + cta * kSignThreads * Z::Y_SLOT;
+  int32_t* wbuf = a.wbuf + cta * kSignThreads * Z::W_SLOT;
+  uint8_t* w1buf = a.w1buf + cta * kSignThreads * S::W1_ALL;
+  uint64_t* ctbuf = a.ctbuf + cta * kSignThreads * 4;
+  int8_t* c8buf = a.c8buf + cta * kSignThreads * kN;
+  uint8_t* staging = a.staging + cta * kSignThreads * Z::SIG_PAD;
+
+  load_twiddles(sm.zs, sm.nzs);
+  if (tid == 0) sm.U = 0;
+  unsigned long long st_rounds = 0, st_attempts = 0, st_spec = 0, st_idle = 0;  // thread 0 only
+  __syncthreads();
+
+  while (true) {
+    // ---- refill from the device work queue -----------------------------------------
+    if (tid == 0) {
+      const unsigned U = sm.U;
+      unsigned got = 0, base = 0;
+      if (U < a.tcap && !(a.single_round && st_rounds > 0)) {
+        const unsigned want = a.tcap - U;
+        if (*(volatile unsigned*)&a.q->head < a.n) {
+          base = atomicAdd(&a.q->head, want);
+          if (base < a.n) got = min(want, a.n - base);
+        }
+      }
+      sm.got = got;
+      sm.base = base;
+    }
+    __syncthreads();
+    {
+      const unsigned U = sm.U, got = sm.got;
+      if ((unsigned)tid < got) {
+        sm.utask[U + tid] = sm.base + tid;
+        sm.unext[U + tid] = 0;
+      }
+      __syncthreads();
+      if (tid == 0) sm.U = U + got;
+      __syncthreads();
+    }
+    const unsigned U = sm.U;
+    if (U == 0) break;
+
+    // ---- schedule: slot s -> open task s % U, depth s / U (scheduler.hpp:58-92) ------
+    {
+      const unsigned u = tid % U, depth = tid / U;
+      const unsigned att = sm.unext[u] + depth;
+      const bool on = (depth == 0 || a.speculate) && att <= a.max_attempt;
+      sm.slot_task[tid] = on ? sm.utask[u] : kNoSlot;
+      sm.slot_attempt[tid] = att;
+      sm.slot_valid[tid] = 0;
+      const unsigned n_on = __syncthreads_count(on);
+      const unsigned n_spec = __syncthreads_count(on && depth > 0);
+      if (tid == 0) {
+        st_rounds += 1;
+        st_attempts += n_on;
+        st_spec += n_spec;
+        st_idle += kSignThreads - n_on;
+      }
+    }
+    const unsigned my_task = sm.slot_task[tid];
+
+    // ---- S1: masks ---------------------------------------------------------------
+    if (my_task != kNoSlot) {
+      const unsigned k0 = a.kappa0 ? a.kappa0[my_task] : 0u;
+      const unsigned kappa = k0 + sm.slot_attempt[tid] * P::L;
+#pragma unroll 1
+      for (int j = 0; j < P::L; ++j)
+        expand_mask_stream<P>(a.rho_prime + (size_t)my_task * 8, kappa + j,
+                              ybytes + (size_t)tid * Z::Y_SLOT + j * S::Z_POLY);
+    }
+    __syncthreads();
+
+    // ---- S2: w, w1 ---------------------------------------------------------------
+#pragma unroll 1
+    for (int s = warp; s < kSignThreads; s += kSignWarps) {
+      const unsigned task = sm.slot_task[s];
+      if (task == kNoSlot) continue;
+      const size_t key = (size_t)task * a.key_stride;
+      stage_w<P>(sm.u.ws[warp], sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
+                 a.A + key * (P::K * P::L * kN), wbuf + (size_t)s * Z::W_SLOT,
+                 w1buf + (size_t)s * S::W1_ALL);
+    }
+    __syncthreads();
+
+    // ---- S3: challenge -----------------------------------------------------------
+    {
+      if (my_task != kNoSlot) {
+        uint64_t ct[4];
+        hash_ctilde_stream<S::W1_ALL>(a.mu + (size_t)my_task * 8,
+                                      reinterpret_cast<const uint64_t*>(w1buf + (size_t)tid * S::W1_ALL),
+                                      ct);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) ctbuf[tid * 4 + w] = ct[w];
+        sample_in_ball_words<P::TAU>(ct, sm.u.rows[tid]);
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int src = 0; src < 32; ++src) {
+        const int s = warp * 32 + src;
+        if (sm.slot_task[s] == kNoSlot) continue;
+        const uint32_t* srow = reinterpret_cast<const uint32_t*>(sm.u.rows[s]);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(c8buf + (size_t)s * kN);
+        dst[lane] = srow[lane];
+        dst[lane + 32] = srow[lane + 32];
+      }
+    }
+    __syncthreads();
+
+    // ---- S4: finish --------------------------------------------------------------
+#pragma unroll 1
+    for (int s = warp; s < kSignThreads; s += kSignWarps) {
+      const unsigned task = sm.slot_task[s];
+      if (task == kNoSlot) continue;
+      const size_t key = (size_t)task * a.key_stride;
+      const bool ok = stage_finish<P>(sm.u.ws[warp], sm.zs, sm.nzs, lane,
+                                      ybytes + (size_t)s * Z::Y_SLOT, wbuf + (size_t)s * Z::W_SLOT,
+                                      c8buf + (size_t)s * kN, ctbuf + s * 4,
+                                      a.shat + key * ((P::L + 2 * P::K) * kN),
+                                      staging + (size_t)s * Z::SIG_PAD);
+      if (lane == 0) sm.slot_valid[s] = ok ? 1 : 0;
+    }
+    __syncthreads();
+
+    // ---- commit: smallest valid attempt per task wins (scheduler.hpp:97-136) --------
+    bool keep = false;
+    unsigned my_u_task = 0, my_u_next = 0;
+    if ((unsigned)tid < U) {
+      const unsigned task = sm.utask[tid];
+      unsigned next = sm.unext[tid];
+      int win = -1;
+      unsigned ran = 0;
+      for (unsigned s = tid; s < (unsigned)kSignThreads; s += U) {
+        if (sm.slot_task[s] == kNoSlot) break;
+        ++ran;
+        if (sm.slot_valid[s]) {
+          win = (int)s;
+          break;
+        }
+      }
+      if (a.dbg_ctilde) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(ctbuf + tid * 4);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(a.dbg_ctilde + (size_t)task * 32);
+        for (int w = 0; w < 8; ++w) dst[w] = src[w];
+      }
+      if (win >= 0) {
+        const unsigned ordinal = sm.slot_attempt[win] + 1;
+        if (a.attempts_out) a.attempts_out[task] = ordinal;
+        if (a.failed_out) a.failed_out[task] = 0;
+        atomicAdd(&a.q->accepted_sum, (unsigned long long)ordinal);
+      } else {
+        next += ran;
+        if (next > a.max_attempt || a.single_round) {
+          win = -2;  // nonce space exhausted (scheduler.hpp:122-128)
+          if (a.attempts_out) a.attempts_out[task] = 0;
+          if (a.failed_out) a.failed_out[task] = 1;
+          atomicAdd(&a.q->failed, 1ull);
+        }
+      }
+      sm.winner[tid] = win;
+      keep = win == -1;
+      my_u_task = task;
+      my_u_next = next;
+    }
+    // compact the open-task table
+    {
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) sm.warp_sums[warp] = __popc(bal);
+      __syncthreads();
+      unsigned off = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < kSignWarps; ++w) {
+        if (w < warp) off += sm.warp_sums[w];
+        total += sm.warp_sums[w];
+      }
+      const unsigned pos = off + __popc(bal & ((1u << lane) - 1));
+      // copy winners' staged signatures out before the table is overwritten
+#pragma unroll 1
+      for (unsigned u = warp; u < U; u += kSignWarps) {
+        const int win = sm.winner[u];
+        if (win < 0) continue;
+        const uint8_t* src = staging + (size_t)win * Z::SIG_PAD;
+        uint8_t* dst = a.sigs + (size_t)sm.utask[u] * S::SIG;
+        if ((S::SIG & 3) == 0) {
+          for (int w = lane; w < S::SIG / 4; w += 32)
+            reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(src)[w];
+        } else {
+          for (int b = lane; b < S::SIG; b += 32) dst[b] = src[b];
+        }
+      }
+      __syncthreads();
+      if (keep) {
+        sm.utask[pos] = my_u_task;
+        sm.unext[pos] = my_u_next;
+      }
+      if (tid == 0) sm.U = total;
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    atomicAdd(&a.q->rounds, st_rounds);
+    atomicAdd(&a.q->attempts, st_attempts);
+    atomicAdd(&a.q->speculative, st_spec);
+    atomicAdd(&a.q->idle_slots, st_idle);
+  }
+}
+
+// ---- host side ---------------------------------------------------------------------
+
+template <class P>
+static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride,
+                     const uint8_t* d_msgs, const uint64_t* d_msg_off, const uint64_t* d_mu_in,
+                     const uint8_t* d_rho_prime, const uint32_t* d_kappa0, size_t psi,
+                     int speculate, int single_round, uint8_t* d_sigs, uint32_t* d_attempts,
+                     uint8_t* d_failed, uint8_t* d_dbg_ct, dlb_sign_stats* stats) {
+  using S = Sizes<P>;
+  using Z = SignSizes<P>;
+  constexpr int KL = P::K * P::L, PV = P::L + 2 * P::K;
+  if (n == 0) return 0;
+  if (n > 0x7fffffffu) return DLB_E_ARG;
+  cudaStream_t st = c->s();
+  const size_t nk = sk_stride ? n : 1;
+
+  int32_t *A, *shat;
+  uint64_t *mu, *rp;
+  SignQueue* q;
+  DLB_TRY(dalloc(c, "s.A", nk * KL * kN, &A));
+  DLB_TRY(dalloc(c, "s.shat", nk * PV * kN, &shat));
+  DLB_TRY(dalloc(c, "s.mu", n * 8, &mu));
+  DLB_TRY(dalloc(c, "s.rp", n * 8, &rp));
+  DLB_TRY(dalloc(c, "s.q", 1, &q));
+  DLB_CUDA_CHECK(cudaMemsetAsync(q, 0, sizeof(SignQueue), st));
+
+  // per-key precomputation (scheme.hpp:106-125)
+  k_expand_a<P, 4><<<cdiv(nk * KL, 128), 128, 0, st>>>(d_sks, sk_stride, (unsigned)(nk * KL), A);
+  k_sign_unpack<P, 4><<<cdiv(nk * PV, 4), 128, 0, st>>>((unsigned)nk, d_sks, sk_stride, shat,
+                                                        &q->key_bad);
+  c->launches += 2;
+  // mu = H(tr || M), rho' = H(K || mu)  (scheme.hpp:240-248)
+  const uint64_t* mu_use = mu;
+  const uint64_t* rp_use = rp;
+  if (d_mu_in) {
+    mu_use = d_mu_in;  // stage tests supply mu and rho' directly
+    rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
+  } else {
+    k_hash_mu<<<cdiv(n, 128), 128, 0, st>>>(d_sks + 64, sk_stride, d_sks + 32, sk_stride, d_msgs,
+                                            d_msg_off, (unsigned)n, mu, d_rho_prime ? nullptr : rp);
+    c->launches += 1;
+    if (d_rho_prime) rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
+  }
+
+  // grid: resident CTAs of the persistent kernel
+  int occ = 0;
+  DLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sign_persistent<P>,
+                                                               kSignThreads, 0));
+  if (occ < 1) occ = 1;
+  const size_t grid_max = (size_t)c->sm_count * occ;
+  size_t grid;
+  if (psi) {
+    grid = (psi + kSignThreads - 1) / kSignThreads;
+  } else {
+    // default Psi: about two slots per open task while the batch is smaller than the
+    // machine, all resident slots otherwise
+    const size_t want_slots = speculate ? 2 * n : n;
+    grid = (want_slots + kSignThreads - 1) / kSignThreads;
+  }
+  if (grid > grid_max) grid = grid_max;
+  if (grid < 1) grid = 1;
+  size_t tcap = (n + grid - 1) / grid;
+  if (tcap > (size_t)kSignThreads) tcap = kSignThreads;
+  if (single_round) {
+    tcap = kSignThreads;
+    grid = (n + kSignThreads - 1) / kSignThreads;
+  }
+
+  SignArgs a;
+  memset(&a, 0, sizeof a);
+  a.n = (unsigned)n;
+  a.tcap = (unsigned)tcap;
+  a.max_attempt = (65535u - (P::L - 1)) / P::L;
+  a.speculate = single_round ? 0 : speculate;
+  a.single_round = single_round;
+  a.mu = mu_use;
+  a.rho_prime = rp_use;
+  a.kappa0 = d_kappa0;
+  a.A = A;
+  a.shat = shat;
+  a.key_stride = sk_stride ? 1u : 0u;
+  const size_t slots = grid * kSignThreads;
+  DLB_TRY(dalloc(c, "s.y", slots * Z::Y_SLOT + 16, &a.ybytes));
+  DLB_TRY(dalloc(c, "s.w", slots * Z::W_SLOT, &a.wbuf));
+  DLB_TRY(dalloc(c, "s.w1", slots * S::W1_ALL, &a.w1buf));
+  DLB_TRY(dalloc(c, "s.ct", slots * 4, &a.ctbuf));
+  DLB_TRY(dalloc(c, "s.c8", slots * kN, &a.c8buf));
+  DLB_TRY(dalloc(c, "s.stage", slots * Z::SIG_PAD, &a.staging));
+  a.sigs = d_sigs;
+  a.attempts_out = d_attempts;
+  a.failed_out = d_failed;
+  a.dbg_ctilde = d_dbg_ct;
+  a.q = q;
+  k_sign_persistent<P><<<(unsigned)grid, kSignThreads, 0, st>>>(a);
+  c->launches += 1;
+  DLB_LAUNCH_CHECK();
+
+  SignQueue hq;
+  DLB_CUDA_CHECK(cudaMemcpyAsync(&hq, q, sizeof hq, cudaMemcpyDeviceToHost, st));
+  DLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (stats) {
+    stats->rounds = hq.rounds;
+    stats->attempts = hq.attempts;
+    stats->speculative = hq.speculative;
+    stats->idle_slot_rounds = hq.idle_slots;
+    stats->accepted_attempt_sum = hq.accepted_sum;
+    stats->failed_tasks = hq.failed;
+  }
+  if (hq.key_bad) return DLB_E_KEY;
+  return 0;
+}
+
+template <class P>
+int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, const uint8_t* d_msgs,
+             const uint64_t* d_msg_off, const uint8_t* d_rho_prime, size_t psi, int speculate,
+             uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats) {
+  return sign_core<P>(c, n, d_sks, sk_stride, d_msgs, d_msg_off, nullptr, d_rho_prime, nullptr, psi,
+                      speculate, 0, d_sigs, d_attempts, d_failed, nullptr, stats);
+}
+
+#define DLB_INST(LV)                                                                            \
+  template int sign_dev<Params<LV>>(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*,   \
+                                    const uint64_t*, const uint8_t*, size_t, int, uint8_t*,     \
+                                    uint32_t*, uint8_t*, dlb_sign_stats*);
+DLB_INST(2)
+DLB_INST(3)
+DLB_INST(5)
+
+}  // namespace dlb
+
+using namespace dlb;
+
+// sign_attempt<P> for n independent (key, mu, rho', kappa) tuples: one scheduler round
+// with one attempt per task; z and hints are decoded back from the staged signature.
+extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8_t* sks,
+                                    size_t sk_stride, const uint8_t* mus, const uint8_t* rho_primes,
+                                    const uint32_t* kappas, uint8_t* accepted, uint8_t* c_tilde,
+                                    int32_t* z, int32_t* hints) {
+  if (!c || !sks || !mus || !rho_primes || !kappas || !accepted || !c_tilde || !z || !hints)
+    return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  auto run = [&](auto p) -> int {
+    using P = decltype(p);
+    using S = Sizes<P>;
+    const size_t nk = sk_stride ? n : 1;
+    uint8_t *dsk, *dsig, *dfail, *dct, *drp;
+    uint64_t* dmu;
+    uint32_t *dk, *datt;
+    DLB_TRY(dalloc(c, "io.sk", nk * S::SK, &dsk));
+    DLB_TRY(dalloc(c, "dbg.a", n * 8, &dmu));
+    DLB_TRY(dalloc(c, "dbg.b", n * 64, &drp));
+    DLB_TRY(dalloc(c, "dbg.c", n, &dk));
+    DLB_TRY(dalloc(c, "io.sig", n * S::SIG + 8, &dsig));
+    DLB_TRY(dalloc(c, "io.att", n, &datt));
+    DLB_TRY(dalloc(c, "io.fail", n, &dfail));
+    DLB_TRY(dalloc(c, "dbg.d", n * 32, &dct));
+    cudaStream_t st = c->s();
+    DLB_CUDA_CHECK(cudaMemcpyAsync(dsk, sks, nk * S::SK, cudaMemcpyHostToDevice, st));
+    DLB_CUDA_CHECK(cudaMemcpyAsync(dmu, mus, n * 64, cudaMemcpyHostToDevice, st));
+    DLB_CUDA_CHECK(cudaMemcpyAsync(drp, rho_primes, n * 64, cudaMemcpyHostToDevice, st));
+    DLB_CUDA_CHECK(cudaMemcpyAsync(dk, kappas, n * 4, cudaMemcpyHostToDevice, st));
+    DLB_CUDA_CHECK(cudaMemsetAsync(dsig, 0, n * S::SIG, st));
+    DLB_TRY(sign_core<P>(c, n, dsk, sk_stride, nullptr, nullptr, dmu, drp, dk, 0, 0, 1, dsig, datt,
+                         dfail, dct, nullptr));
+    uint8_t* hsig = new uint8_t[n * S::SIG];
+    uint8_t* hfail = new uint8_t[n];
+    cudaMemcpyAsync(hsig, dsig, n * S::SIG, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hfail, dfail, n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(c_tilde, dct, n * 32, cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) {
+      memset(z, 0, n * P::L * kN * 4);
+      memset(hints, 0, n * P::K * kN * 4);
+      for (size_t t = 0; t < n; ++t) {
+        accepted[t] = hfail[t] ? 0 : 1;
+        if (!accepted[t]) continue;
+        const uint8_t* sg = hsig + t * S::SIG;
+        for (int j = 0; j < P::L; ++j)
+          for (int m = 0; m < kN; ++m) {
+            const size_t bit = (size_t)m * P::Z_BITS;
+            uint32_t raw = 0;
+            for (int b = 0; b < P::Z_BITS; ++b)
+              raw |= (uint32_t)((sg[32 + j * S::Z_POLY + ((bit + b) >> 3)] >> ((bit + b) & 7)) & 1) << b;
+            z[(t * P::L + j) * kN + m] = P::GAMMA1 - (int32_t)raw;
+          }
+        const uint8_t* h = sg + 32 + P::L * S::Z_POLY;
+        unsigned prev = 0;
+        for (int i = 0; i < P::K; ++i) {
+          const unsigned cnt = h[P::OMEGA + i];
+          for (unsigned k = prev; k < cnt && k < (unsigned)P::OMEGA; ++k)
+            hints[(t * P::K + i) * kN + h[k]] = 1;
+          prev = cnt;
+        }
+      }
+    }
+    delete[] hsig;
+    delete[] hfail;
+    return e == cudaSuccess ? 0 : -1000 - (int)e;
+  };
+  switch (level) {
+    case 2: return run(Params<2>{});
+    case 3: return run(Params<3>{});
+    case 5: return run(Params<5>{});
+    default: return DLB_E_LEVEL;
+  }
+}
