@@ -1,0 +1,524 @@
+#!/usr/bin/env python3
+"""bench.py -- Dilithium2 batched sign / verify / keygen throughput on B200.
+
+Contract (driver):  python bench.py --gpus N --steps K --warmup W   (torchrun for N>1)
+prints ONE JSON line on rank 0.  A step is one pass of the hot path over one batch of
+synthetic input on every GPU: the paper's headline shape, 10 in-flight batches of 10,000
+sign tasks = 100,000 tasks per GPU per step, one shared key, 32-byte messages,
+deterministic signing (BASELINE.json configs[1]).
+
+  value     whole-job signatures/s with inputs resident in HBM (CUDA events)
+  e2e       the same through the host-buffer C ABI (dlb_sign_batch): pinned host memory,
+            H2D of messages and D2H of signatures inside the timed region
+  ops       verify / keygen numbers measured the same way + batch-10k latencies
+  roofline  the dominant kernel (k_sign_persistent) against the INT32 issue rate
+            measured live on this GPU (dlb_measure_int32_peak), plus the HBM view
+  cpu_baseline  the unmodified reference (oracle/_ref) timed on this box's host cores
+
+--impl reference times the reference's own CPU batch_sign / batch_verify with all
+host threads on a bounded sample of the same workload.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LEVEL = 2
+PAPER_A100 = {"sign": 574953, "verify": 1408703, "keygen": 1400257}
+
+# Algorithmic work per unit (SURVEY.md 8d / BASELINE.md section 2):
+# Keccak-f[1600] = 4320 INT32 ops, forward NTT = 7168, inverse = 7800, mul-acc = 6/coeff.
+W_PERM, W_NTT, W_INTT, W_MAC = 4320, 7168, 7800, 6
+WORK = {  # level: perms, NTTs, INTTs, mul-acc polys
+    2: dict(attempt=(28, 5, 9.75, 16 + 5.75), keygen=(103.3, 4, 4, 16), verify=(99, 9, 4, 20),
+            bytes=dict(sign=2452, verify=2453, verify_pk=2453 + 1312, keygen=3872)),
+    3: dict(attempt=(33, 6, 13.73, 30 + 7.73), keygen=(188.0, 5, 6, 30), verify=(174, 12, 6, 36),
+            bytes=dict(sign=3325, verify=3326, verify_pk=3326 + 1952, keygen=5984)),
+    5: dict(attempt=(45, 8, 19.57, 56 + 11.57), keygen=(324.0, 7, 8, 56), verify=(311, 16, 8, 64),
+            bytes=dict(sign=4627, verify=4628, verify_pk=4628 + 2592, keygen=7488)),
+}
+
+
+def int_ops(t):
+    perms, ntt, intt, mac = t
+    return perms * W_PERM + ntt * W_NTT + intt * W_INTT + mac * 256 * W_MAC
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        try:
+            os.unlink(self.f.name)
+        except OSError:
+            pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = [s for s, p in zip(sm, power) if p > 0.5 * max(power)] or sm
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power)}
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, use_cuda):
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29500")
+            if use_cuda:
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group("gloo")
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x, use_cuda=True):
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if use_cuda else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x, use_cuda=True):
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if use_cuda else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def done(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def make_inputs(n, seed):
+    """32-byte messages drawn as static_cast<uint8_t>(mt19937_64()) like the reference's
+    tests (tests/acceptance.cpp:34-38,159-160)."""
+    from tests.cpu_checkers import mt19937_64
+    rng = mt19937_64(seed)
+    msgs = np.frombuffer(rng.bytes(32 * n), np.uint8).reshape(n, 32).copy()
+    off = np.arange(n + 1, dtype=np.uint64) * 32
+    return msgs, off
+
+
+# ----------------------------------------------------------------------------------------
+def run_reference(args, dist):
+    """The reference's own CPU implementation (oracle/_ref), all host threads."""
+    from tests.cpu_checkers import load_ref, ref_available, load_oracle, PARAMS
+    if dist.rank != 0:
+        return
+    kind = "reference" if ref_available() else "port"
+    if kind == "reference":
+        ref = load_ref()
+        cores = max(1, ref.hw_threads())
+    else:
+        ref = None
+        cores = 1
+    oracle = load_oracle()
+    pk, sk = oracle.keygen(LEVEL, bytes(range(32)))
+    n = min(args.tasks, (256 if kind == "reference" else 64) * cores)
+    msgs, off = make_inputs(n, 20221112)
+    sk_a, pk_a = np.frombuffer(sk, np.uint8), np.frombuffer(pk, np.uint8)
+
+    def sign_step():
+        if ref:
+            return ref.batch_sign(LEVEL, sk_a, msgs.reshape(-1), off, workers=cores)[0]
+        return np.stack([np.frombuffer(oracle.sign(LEVEL, sk, m.tobytes())[0], np.uint8) for m in msgs])
+
+    def verify_step(sigs):
+        if ref:
+            return ref.batch_verify(LEVEL, pk_a, msgs.reshape(-1), off, sigs, workers=cores)
+        return np.array([oracle.verify(LEVEL, pk, m.tobytes(), s.tobytes()) for m, s in zip(msgs, sigs)])
+
+    sigs = None
+    for _ in range(args.warmup):
+        sigs = sign_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sigs = sign_step()
+    t_sign = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fl = verify_step(sigs)
+    t_ver = time.perf_counter() - t0
+    assert fl.all()
+    v = n * args.steps / t_sign
+    vv = n * args.steps / t_ver
+    sample = "%d tasks/step (of the %d-task workload), %d steps, %s, %d threads" % (
+        n, args.tasks, args.steps, "reference batch_sign via oracle/_ref" if ref else "oracle port", cores)
+    line = {
+        "impl": "reference", "metric": "dilithium2_sign_ops_per_s", "value": v, "unit": "ops/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_sign / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": v, "unit": "ops/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": "ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ops": {"verify": {"value": vv, "unit": "ops/s"}},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    return {"workload": "Dilithium2 batch sign: 10 in-flight batches x 10,000 = %d tasks per GPU per "
+                        "step, one shared key, 32-byte messages, deterministic signing (paper headline "
+                        "shape); verify/keygen/batch-10k latency reported under 'ops'" % args.tasks,
+            "level": LEVEL, "tasks_per_gpu_per_step": args.tasks,
+            "l2": "inputs larger than L2: each step streams %.0f MB of signatures plus ~0.7 GB of "
+                  "scheduler scratch through the 126 MB L2" % (args.tasks * 2420 / 1e6)}
+
+
+# ----------------------------------------------------------------------------------------
+def run_ours(args, dist):
+    import torch
+    from paper_2211_12265_b200 import Engine, LEVELS
+    from paper_2211_12265_b200.engine import SignStats
+
+    dev_index = dist.local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    eng = Engine(dev_index)  # raises if the CUDA library is missing: no fallback
+    lib, ctx = eng.lib, eng.ctx
+    k, l, pkb, skb, sgb = LEVELS[LEVEL]
+    n = args.tasks
+    K, W = args.steps, max(args.warmup, 0)
+
+    # ---- inputs ---------------------------------------------------------------------
+    pk1, sk1 = eng.batch_keygen(LEVEL, np.arange(32, dtype=np.uint8))
+    msgs, off = make_inputs(n, 20221112 + dist.rank)
+    zetas, _ = make_inputs(n, 777 + dist.rank)
+    p = lambda t: C.c_void_p(t.data_ptr())
+    d_msgs = torch.from_numpy(msgs).to(dev)
+    d_off = torch.from_numpy(off.astype(np.int64)).to(dev)
+    d_zetas = torch.from_numpy(zetas).to(dev)
+    d_sk = torch.from_numpy(sk1[0].copy()).to(dev)
+    d_pk = torch.from_numpy(pk1[0].copy()).to(dev)
+    d_pk_rep = d_pk.unsqueeze(0).repeat(n, 1).contiguous()  # per-task public keys (no sharing)
+    d_sigs = torch.zeros((n, sgb), dtype=torch.uint8, device=dev)
+    d_att = torch.zeros(n, dtype=torch.int32, device=dev)
+    d_fail = torch.zeros(n, dtype=torch.uint8, device=dev)
+    d_flags = torch.zeros(n, dtype=torch.uint8, device=dev)
+    d_pks = torch.zeros((n, pkb), dtype=torch.uint8, device=dev)
+    d_sks = torch.zeros((n, skb), dtype=torch.uint8, device=dev)
+    stats = SignStats()
+    side = torch.cuda.Stream(device=dev)  # the engine launches on this stream; so do the events
+    torch.cuda.set_stream(side)
+    eng.set_stream(side.cuda_stream)
+
+    def sign_dev():
+        rc = lib.dlb_sign_batch_dev(ctx, LEVEL, n, p(d_sk), 0, p(d_msgs), p(d_off), None, 0, 1,
+                                    p(d_sigs), p(d_att), p(d_fail), C.byref(stats))
+        assert rc == 0, rc
+
+    def verify_dev(shared):
+        rc = lib.dlb_verify_batch_dev(ctx, LEVEL, n, p(d_pk if shared else d_pk_rep), 0 if shared else pkb,
+                                      p(d_msgs), p(d_off), p(d_sigs), p(d_flags))
+        assert rc == 0, rc
+
+    def keygen_dev():
+        rc = lib.dlb_keygen_batch_dev(ctx, LEVEL, n, p(d_zetas), p(d_pks), p(d_sks))
+        assert rc == 0, rc
+
+    # ---- parity gate before any timing (rank 0): sample vs the CPU oracle --------------
+    if dist.rank == 0:
+        from tests.cpu_checkers import load_oracle
+        oracle = load_oracle()
+        m = 48
+        s_sigs, s_att, _, _ = eng.batch_sign(LEVEL, sk1[0], (msgs[:m].reshape(-1), off[:m + 1]),
+                                             return_info=True)
+        for i in range(m):
+            es, ea = oracle.sign(LEVEL, sk1[0].tobytes(), msgs[i].tobytes())
+            assert s_sigs[i].tobytes() == es and int(s_att[i]) == ea, "parity gate failed (sign)"
+        assert oracle.keygen(LEVEL, bytes(range(32))) == (pk1[0].tobytes(), sk1[0].tobytes())
+
+    peaks = eng.measure_int32_peak()
+
+    def timed(fn, steps, warm):
+        """K steps between barrier+synchronize on both sides, CUDA events, max over ranks."""
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches, main_ms = 0, 0.0
+        e0.record()
+        for _ in range(steps):
+            fn()
+            launches += eng.last_launches
+            main_ms += eng.last_main_kernel_ms
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = dist.max(e0.elapsed_time(e1))
+        return ms, launches, main_ms / max(steps, 1)
+
+    sampler = ClockSampler(dev_index)
+    sampler.start()
+    # ---- headline: sign, inputs resident in HBM -------------------------------------------
+    ms_sign, launches, main_ms = timed(sign_dev, K, max(W, 3))
+    useful_attempts = stats.accepted_attempt_sum / n
+    executed_attempts = stats.attempts / n
+    assert bool((d_fail == 0).all().item())
+    ms_ver, l_ver, _ = timed(lambda: verify_dev(False), K, max(W, 3))
+    assert bool(d_flags.all().item()), "device verify rejected a device signature"
+    ms_ver_sh, _, _ = timed(lambda: verify_dev(True), K, max(W, 3))
+    ms_kg, l_kg, _ = timed(keygen_dev, K, max(W, 3))
+    clocks = sampler.stop()
+
+    world = dist.world
+    value = world * n * K / (ms_sign * 1e-3)
+    ver_value = world * n * K / (ms_ver * 1e-3)
+    ver_sh_value = world * n * K / (ms_ver_sh * 1e-3)
+    kg_value = world * n * K / (ms_kg * 1e-3)
+
+    # ---- e2e: host-buffer C ABI, pinned host memory, copies inside the timed region ----
+    eng.set_stream(0)
+    h_msgs = torch.from_numpy(msgs).pin_memory()
+    h_off = torch.from_numpy(off.astype(np.int64)).pin_memory()
+    h_sk = torch.from_numpy(sk1[0].copy()).pin_memory()
+    h_pk = torch.from_numpy(pk1[0].copy()).pin_memory()
+    h_sigs = torch.zeros((n, sgb), dtype=torch.uint8).pin_memory()
+    h_flags = torch.zeros(n, dtype=torch.uint8).pin_memory()
+    h_zetas = torch.from_numpy(zetas).pin_memory()
+    h_pks = torch.zeros((n, pkb), dtype=torch.uint8).pin_memory()
+    h_sks = torch.zeros((n, skb), dtype=torch.uint8).pin_memory()
+    h_pk_rep = h_pk.unsqueeze(0).repeat(n, 1).contiguous().pin_memory()
+    u8 = lambda t: C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_uint8))
+    u64 = lambda t: C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_uint64))
+
+    def sign_host(cnt=n):
+        rc = lib.dlb_sign_batch(ctx, LEVEL, cnt, u8(h_sk), 0, u8(h_msgs), u64(h_off), None, 0, 1,
+                                u8(h_sigs), None, None, None)
+        assert rc == 0, rc
+
+    def verify_host(cnt=n):
+        rc = lib.dlb_verify_batch(ctx, LEVEL, cnt, u8(h_pk_rep), pkb, u8(h_msgs), u64(h_off), u8(h_sigs),
+                                  u8(h_flags))
+        assert rc == 0, rc
+
+    def keygen_host(cnt=n):
+        rc = lib.dlb_keygen_batch(ctx, LEVEL, cnt, u8(h_zetas), u8(h_pks), u8(h_sks))
+        assert rc == 0, rc
+
+    def timed_host(fn, steps, warm):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter() - t0
+        dist.barrier()
+        return dist.max(t)
+
+    t_e2e_sign = timed_host(sign_host, K, 3)
+    t_e2e_ver = timed_host(verify_host, K, 3)
+    assert bool(h_flags.all().item())
+    assert torch.equal(h_sigs, d_sigs.cpu()), "e2e and device-resident signatures differ"
+    t_e2e_kg = timed_host(keygen_host, K, 3)
+    e2e_sign = world * n * K / t_e2e_sign
+    e2e_ver = world * n * K / t_e2e_ver
+    e2e_kg = world * n * K / t_e2e_kg
+
+    # batch-10k latency (ms), e2e, median of 11 (sign < 32 ms, verify < 15 ms)
+    def lat(fn):
+        for _ in range(3):
+            fn(10000)
+        xs = []
+        for _ in range(11):
+            t0 = time.perf_counter()
+            fn(10000)
+            xs.append((time.perf_counter() - t0) * 1e3)
+        return float(np.median(xs))
+
+    lat_sign, lat_ver, lat_kg = lat(sign_host), lat(verify_host), lat(keygen_host)
+
+    # ---- roofline of the dominant kernel -------------------------------------------------
+    wk = WORK[LEVEL]
+    w_attempt = int_ops(wk["attempt"])
+    ops_per_launch = n * useful_attempts * w_attempt  # useful work only; speculation = overhead
+    achieved = ops_per_launch / (main_ms * 1e-3) / 1e12
+    peak_single = peaks["lop3"]
+    peaks_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_file):
+        hbm_peak, hbm_src = float(json.load(open(peaks_file))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    hbm_achieved = n * wk["bytes"]["sign"] / (main_ms * 1e-3) / 1e9
+    roofline = {
+        "bound": "int32-alu", "kernel": "k_sign_persistent", "achieved": achieved, "peak": peak_single,
+        "unit": "Tint32-op/s", "frac": achieved / peak_single,
+        "peak_src": "measured live: LOP3 issue rate (alu pipe), dlb_measure_int32_peak",
+        "peak_dual_pipe": peaks["lop3_imad_mix"], "frac_dual_pipe": achieved / peaks["lop3_imad_mix"],
+        "traffic": None, "launch_ms": main_ms,
+        "model": {"int32_ops_per_attempt": w_attempt, "useful_attempts_per_sig": useful_attempts,
+                  "executed_attempts_per_sig": executed_attempts},
+        "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_achieved / hbm_peak,
+                "peak_src": hbm_src, "algorithmic_bytes_per_sig": wk["bytes"]["sign"]},
+        "per_op_frac": {
+            "keygen": kg_value / world * int_ops(wk["keygen"]) / 1e12 / peak_single,
+            "verify": ver_value / world * int_ops(wk["verify"]) / 1e12 / peak_single,
+            "sign_whole_call": value / world * (useful_attempts * w_attempt + 2 * W_PERM) / 1e12 / peak_single,
+        },
+        "int32_peaks_measured": peaks,
+    }
+
+    # ---- CPU baseline on this box's host cores (rank 0, N == 1 only) ---------------------
+    cpu = None
+    if dist.rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(sk1[0], pk1[0], msgs, off)
+
+    if dist.rank == 0:
+        line = {
+            "metric": "dilithium2_sign_ops_per_s", "value": value, "unit": "ops/s", "n_gpus": world,
+            "steps": K, "warmup": max(W, 3), "ms_per_step": ms_sign / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": value / PAPER_A100["sign"],
+            "vs_baseline_note": "value / 574,953 (paper's A100 D2 sign/s, BASELINE.md 1.1; other hardware)",
+            "dtype": "int32", "data": "synthetic", "config": workload_config(args),
+            "e2e": {"value": e2e_sign, "unit": "ops/s", "h2d_bytes_per_step": int(n * 32 + (n + 1) * 8 + skb),
+                    "d2h_bytes_per_step": int(n * sgb)},
+            "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline,
+            "cpu_baseline": cpu,
+            "ops": {
+                "sign": {"value": value, "e2e": e2e_sign, "unit": "ops/s",
+                         "attempts_per_sig": useful_attempts, "executed_attempts_per_sig": executed_attempts},
+                "verify": {"value": ver_value, "e2e": e2e_ver, "unit": "ops/s", "ms_per_step": ms_ver / K,
+                           "note": "one public key per task (no key sharing assumed): 99 permutations/op",
+                           "gpu_launches": int(l_ver)},
+                "verify_shared_key": {"value": ver_sh_value, "unit": "ops/s",
+                                      "note": "pk_stride=0 fast path: A and tr expanded once per batch"},
+                "keygen": {"value": kg_value, "e2e": e2e_kg, "unit": "ops/s", "ms_per_step": ms_kg / K,
+                           "gpu_launches": int(l_kg)},
+                "batch10k_latency_ms": {"sign": lat_sign, "verify": lat_ver, "keygen": lat_kg,
+                                        "note": "host buffers in -> host buffers out, median of 11"},
+            },
+            "context": {"paper_a100_ops_per_s": PAPER_A100},
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+
+
+def cpu_baseline(sk, pk, msgs, off):
+    """Reference CPU path on this box: all cores and single thread, bounded sample."""
+    from tests.cpu_checkers import load_ref, ref_available, load_oracle
+    if ref_available():
+        ref = load_ref()
+        cores = max(1, ref.hw_threads())
+        n_all = min(len(msgs), 384 * cores)
+        m, o = msgs[:n_all].reshape(-1), off[:n_all + 1]
+        ref.batch_sign(LEVEL, sk, m[:32 * 64], o[:65], workers=cores)  # warm
+        t0 = time.perf_counter()
+        sigs, _ = ref.batch_sign(LEVEL, sk, m, o, workers=cores)
+        t_all = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        fl = ref.batch_verify(LEVEL, pk, m, o, sigs, workers=cores)
+        t_ver = time.perf_counter() - t0
+        assert fl.all()
+        n1 = min(n_all, 1500)
+        t0 = time.perf_counter()
+        ref.batch_sign(LEVEL, sk, m[:32 * n1], o[:n1 + 1], workers=1)
+        t_one = time.perf_counter() - t0
+        return {"value": n_all / t_all, "unit": "ops/s", "cores": cores, "kind": "reference",
+                "sample": "%d of the step's tasks: reference batch_sign (oracle/_ref), workers=%d" % (n_all, cores),
+                "single_thread": {"value": n1 / t_one, "cores": 1, "sample": "%d tasks" % n1},
+                "verify": {"value": n_all / t_ver, "cores": cores}}
+    oracle = load_oracle()
+    n1 = 400
+    t0 = time.perf_counter()
+    for i in range(n1):
+        oracle.sign(LEVEL, sk.tobytes(), msgs[i].tobytes())
+    t = time.perf_counter() - t0
+    return {"value": n1 / t, "unit": "ops/s", "cores": 1, "kind": "port",
+            "sample": "%d tasks, scalar oracle port (oracle/_ref absent)" % n1}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tasks", type=int, default=100000, help="tasks per GPU per step")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    dist = Dist()
+    if args.impl == "reference":
+        # rank 0 alone works; the others exit 0 without joining anything
+        run_reference(args, dist)
+        return
+    dist.init(use_cuda=True)
+    try:
+        run_ours(args, dist)
+    finally:
+        dist.done()
+
+
+if __name__ == "__main__":
+    main()

@@ -54,11 +54,22 @@ const char* dlb_version(void);
 /* Device time (ms, CUDA events on the engine's stream) of the kernels of the last batch
  * call, excluding host<->device copies. */
 float dlb_last_kernel_ms(const dlb_ctx* ctx);
+/* Device time (ms) of the dominant kernel of the last sign call (k_sign_persistent). */
+float dlb_last_main_kernel_ms(const dlb_ctx* ctx);
 /* Number of kernel launches issued by the last batch call. */
 unsigned dlb_last_launches(const dlb_ctx* ctx);
 /* Use an external CUDA stream (e.g. the caller's current stream) for the *_dev entry
  * points; NULL restores the engine's own stream. */
 int dlb_set_stream(dlb_ctx* ctx, void* cuda_stream);
+
+/* INT32 issue-rate microbenchmark (roofline denominator for this path): out[0] LOP3,
+ * out[1] IMAD, out[2] SHF, out[3] LOP3+IMAD interleaved, in 10^12 lane-operations/s. */
+int dlb_measure_int32_peak(dlb_ctx* ctx, double out[4]);
+
+/* Pinned host memory for callers that want zero-staging transfers (the engine copies
+ * straight from/to these buffers with cudaMemcpyAsync). */
+void* dlb_host_alloc(size_t bytes);
+void dlb_host_free(void* p);
 
 /* Host-buffer batch API (what batch.hpp binds) ----------------------------------------- */
 

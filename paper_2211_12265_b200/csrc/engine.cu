@@ -160,6 +160,8 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev0));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev1));
+  DLB_CUDA_CHECK(cudaEventCreate(&c->ev2));
+  DLB_CUDA_CHECK(cudaEventCreate(&c->ev3));
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   *out = c;
   return 0;
@@ -175,6 +177,8 @@ void dlb_destroy(dlb_ctx* c) {
     if (kv.second.p) cudaFreeHost(kv.second.p);
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
+  cudaEventDestroy(c->ev2);
+  cudaEventDestroy(c->ev3);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->copy_in);
   cudaStreamDestroy(c->copy_out);
@@ -182,12 +186,26 @@ void dlb_destroy(dlb_ctx* c) {
 }
 
 float dlb_last_kernel_ms(const dlb_ctx* c) { return c ? c->last_ms : 0.f; }
+float dlb_last_main_kernel_ms(const dlb_ctx* c) { return c ? c->last_main_ms : 0.f; }
 unsigned dlb_last_launches(const dlb_ctx* c) { return c ? c->launches : 0; }
 
 int dlb_set_stream(dlb_ctx* c, void* cuda_stream) {
   if (!c) return DLB_E_ARG;
   c->ext = static_cast<cudaStream_t>(cuda_stream);
   return 0;
+}
+
+void* dlb_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dlb_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 // ---- device-resident ---------------------------------------------------------------

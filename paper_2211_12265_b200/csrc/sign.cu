@@ -579,13 +579,16 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   a.failed_out = d_failed;
   a.dbg_ctilde = d_dbg_ct;
   a.q = q;
+  cudaEventRecord(c->ev2, st);
   k_sign_persistent<P><<<(unsigned)grid, kSignThreads, 0, st>>>(a);
+  cudaEventRecord(c->ev3, st);
   c->launches += 1;
   DLB_LAUNCH_CHECK();
 
   SignQueue hq;
   DLB_CUDA_CHECK(cudaMemcpyAsync(&hq, q, sizeof hq, cudaMemcpyDeviceToHost, st));
   DLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaEventElapsedTime(&c->last_main_ms, c->ev2, c->ev3);
   if (stats) {
     stats->rounds = hq.rounds;
     stats->attempts = hq.attempts;

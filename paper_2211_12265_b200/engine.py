@@ -51,8 +51,12 @@ def load_library():
         "dlb_destroy": (None, [vp]),
         "dlb_version": (C.c_char_p, []),
         "dlb_last_kernel_ms": (C.c_float, [vp]),
+        "dlb_last_main_kernel_ms": (C.c_float, [vp]),
         "dlb_last_launches": (C.c_uint, [vp]),
         "dlb_set_stream": (C.c_int, [vp, vp]),
+        "dlb_measure_int32_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "dlb_host_alloc": (vp, [sz]),
+        "dlb_host_free": (None, [vp]),
         "dlb_keygen_batch": (C.c_int, [vp, C.c_int, sz, _u8p, _u8p, _u8p]),
         "dlb_sign_batch": (C.c_int, [vp, C.c_int, sz, _u8p, sz, _u8p, _u64p, _u8p, sz, C.c_int,
                                      _u8p, _u32p, _u8p, C.POINTER(SignStats)]),
@@ -79,8 +83,8 @@ def load_library():
 
 
 EXPORTED_SYMBOLS = [
-    "dlb_create", "dlb_destroy", "dlb_version", "dlb_last_kernel_ms", "dlb_last_launches",
-    "dlb_set_stream", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
+    "dlb_create", "dlb_destroy", "dlb_version", "dlb_last_kernel_ms", "dlb_last_main_kernel_ms", "dlb_last_launches",
+    "dlb_set_stream", "dlb_measure_int32_peak", "dlb_host_alloc", "dlb_host_free", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
     "dlb_keygen_batch_dev", "dlb_sign_batch_dev", "dlb_verify_batch_dev", "dlb_dbg_keccak_f1600",
     "dlb_dbg_shake256", "dlb_dbg_expand_a", "dlb_dbg_expand_s", "dlb_dbg_expand_mask",
     "dlb_dbg_sample_in_ball", "dlb_dbg_ntt", "dlb_dbg_sign_attempt",
@@ -136,11 +140,20 @@ class Engine:
         return float(self.lib.dlb_last_kernel_ms(self.ctx))
 
     @property
+    def last_main_kernel_ms(self):
+        return float(self.lib.dlb_last_main_kernel_ms(self.ctx))
+
+    @property
     def last_launches(self):
         return int(self.lib.dlb_last_launches(self.ctx))
 
     def set_stream(self, handle):
         self._chk(self.lib.dlb_set_stream(self.ctx, C.c_void_p(handle)), "dlb_set_stream")
+
+    def measure_int32_peak(self):
+        out = (C.c_double * 4)()
+        self._chk(self.lib.dlb_measure_int32_peak(self.ctx, out), "dlb_measure_int32_peak")
+        return {"lop3": out[0], "imad": out[1], "shf": out[2], "lop3_imad_mix": out[3]}
 
     # ---- batch.hpp:159-166
     def batch_keygen(self, level, zetas):
