@@ -11,6 +11,8 @@ print("int32 peaks (Tlane-op/s):", eng.measure_int32_peak())
 lib, ctx = eng.lib, eng.ctx
 levels = [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["2"])]
 sizes = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["10000", "100000"])]
+only = sys.argv[3].split(",") if len(sys.argv) > 3 else ["keygen", "sign", "verify"]
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 for level in levels:
     k, l, pkb, skb, sgb = LEVELS[level]
     rng = np.random.default_rng(1)
@@ -34,10 +36,13 @@ for level in levels:
         def kg(): return lib.dlb_keygen_batch_dev(ctx, level, n, P(zetas), P(pks), P(sks))
         def sg(): return lib.dlb_sign_batch_dev(ctx, level, n, P(sk_d), 0, P(msgs), P(off), None, 0, 1, P(sigs), P(att), P(fl), C.byref(st))
         def vf(): return lib.dlb_verify_batch_dev(ctx, level, n, P(pk_d), 0, P(msgs), P(off), P(sigs), P(fl))
+        if "sign" not in only and "verify" in only:
+            assert sg() == 0
         for name, fn in (("keygen", kg), ("sign", sg), ("verify", vf)):
-            for _ in range(2): assert fn() == 0
+            if name not in only: continue
+            for _ in range(min(2, reps)): assert fn() == 0
             ms = []
-            for _ in range(5):
+            for _ in range(reps):
                 assert fn() == 0
                 ms.append(eng.last_kernel_ms)
             best, med = min(ms), sorted(ms)[len(ms) // 2]

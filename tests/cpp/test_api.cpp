@@ -1,0 +1,76 @@
+// Exercises include/dilithium_b200/api.hpp the way the reference's own tests exercise
+// scheme.hpp / batch.hpp (tests/test_scheme.cpp:27-108,195-202; tests/test_batch.cpp:190-297).
+// Needs a GPU at run time; compiled (not run) by the CPU test-suite.
+#include <cstdio>
+#include <random>
+
+#include "dilithium_b200/api.hpp"
+
+using namespace dilithium::b200;
+
+static int fails = 0;
+#define CHECK(x) do { if (!(x)) { std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #x); ++fails; } } while (0)
+
+template <Params P>
+void level_test(std::mt19937_64& rng) {
+  SeedArray zeta;
+  for (auto& b : zeta) b = static_cast<uint8_t>(rng());
+  auto [pk, sk] = keygen<P>(zeta);
+  std::vector<uint8_t> msg(1 + rng() % 100);
+  for (auto& b : msg) b = static_cast<uint8_t>(rng());
+  auto sig = sign<P>(sk, msg);
+  CHECK(verify<P>(pk, msg, sig));
+  auto bad = sig;
+  bad[rng() % bad.size()] ^= 1;
+  CHECK(!verify<P>(pk, msg, bad));
+  CHECK(!verify<P>(pk, msg, std::span<const uint8_t>(sig.data(), sig.size() - 1)));
+  CHECK(!verify<P>(std::span<const uint8_t>(pk.data(), pk.size() - 1), msg, sig));
+  // determinism + precomp path + attempts
+  auto pre = make_precomp<P>(sk);
+  CHECK(pre.has_value());
+  auto out = sign_with_precomp<P>(*pre, msg);
+  CHECK(out.sig == sig && out.attempts >= 1);
+  // malformed key
+  auto badsk = sk;
+  badsk[96] = 0xFF;
+  CHECK(!make_precomp<P>(badsk).has_value());
+  bool threw = false;
+  try { sign<P>(badsk, msg); } catch (const std::invalid_argument&) { threw = true; }
+  CHECK(threw);
+  // batch == sequential, independent of psi / speculate
+  const size_t n = 40;
+  std::vector<std::vector<uint8_t>> msgs(n);
+  std::vector<SignJob<P>> jobs(n);
+  for (size_t i = 0; i < n; ++i) {
+    msgs[i].resize(rng() % 64);
+    for (auto& b : msgs[i]) b = static_cast<uint8_t>(rng());
+    jobs[i] = {&*pre, msgs[i]};
+  }
+  BatchStats st;
+  auto sigs = batch_sign<P>(std::span<const SignJob<P>>(jobs), {}, &st);
+  BatchConfig c2; c2.psi = 128; c2.speculate = false;
+  auto sigs2 = batch_sign<P>(std::span<const SignJob<P>>(jobs), c2);
+  CHECK(sigs == sigs2 && st.failed_tasks.empty());
+  for (size_t i = 0; i < n; i += 13) CHECK(sigs[i] == sign<P>(sk, msgs[i]));
+  std::vector<VerifyJob<P>> vj(n);
+  for (size_t i = 0; i < n; ++i) vj[i] = {pk, msgs[i], sigs[i]};
+  auto corrupted = sigs[5];
+  corrupted[40] ^= 0x20;
+  vj[5].sig = corrupted;
+  vj[6].sig = std::span<const uint8_t>(sigs[6].data(), 10);  // wrong length
+  auto flags = batch_verify<P>(std::span<const VerifyJob<P>>(vj));
+  for (size_t i = 0; i < n; ++i) CHECK(flags[i] == ((i == 5 || i == 6) ? 0 : 1));
+  std::vector<SeedArray> zs(9);
+  for (auto& z : zs) for (auto& b : z) b = static_cast<uint8_t>(rng());
+  auto keys = batch_keygen<P>(std::span<const SeedArray>(zs));
+  CHECK(keys[3] == keygen<P>(zs[3]));
+}
+
+int main() {
+  std::mt19937_64 rng(4242);
+  level_test<kDilithium2>(rng);
+  level_test<kDilithium3>(rng);
+  level_test<kDilithium5>(rng);
+  std::printf(fails ? "api test: %d failures\n" : "api test: all passed\n", fails);
+  return fails ? 1 : 0;
+}

@@ -1,0 +1,87 @@
+"""C++ shim on the device, the sharded multi-engine front end, and BASELINE configs 2-4 at
+full batch size through size-independent properties (sign -> verify round trip, corruption
+flags, determinism, a sampled byte compare against the CPU oracle).  -m gpu."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from tests.cpu_checkers import PARAMS, mt19937_64
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_2211_12265_b200 import Engine
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+def test_cpp_shim_runs():
+    out = "/tmp/dlb_test_api_gpu"
+    lib = os.path.join(ROOT, "paper_2211_12265_b200")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "test_api.cpp"), "-o", out, "-L" + lib,
+                        "-ldilithium_b200", "-Wl,-rpath," + lib], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([out], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "all passed" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("level", [2, 3, 5])
+def test_batch_10k_properties(eng, oracle, level):
+    """configs[1..3]: batch-10k keygen / sign / verify."""
+    n = 10000
+    rng = mt19937_64(900 + level)
+    zetas = np.frombuffer(rng.bytes(32 * n), np.uint8).reshape(n, 32)
+    msgs = np.frombuffer(rng.bytes(32 * n), np.uint8)
+    off = np.arange(n + 1, dtype=np.uint64) * 32
+    pks, sks = eng.batch_keygen(level, zetas)
+    for i in range(0, n, 997):  # sampled byte compare
+        assert (pks[i].tobytes(), sks[i].tobytes()) == oracle.keygen(level, zetas[i].tobytes())
+    assert np.array_equal(pks[:, :32], sks[:, :32])  # rho shared between pk and sk
+    # shared key: all signatures verify; deterministic; attempts mean in the expected band
+    sigs, att, failed, st = eng.batch_sign(level, sks[0], (msgs, off), return_info=True)
+    assert not failed.any()
+    exp_mean = {2: 4.25, 3: 5.1, 5: 3.85}[level]  # PAPER.md:269; acceptance.cpp:149-182 (+-10 %)
+    assert abs(att.mean() / exp_mean - 1) < 0.10
+    for i in range(0, n, 1999):
+        assert (sigs[i].tobytes(), int(att[i])) == oracle.sign(level, sks[0].tobytes(), msgs[32 * i:32 * i + 32].tobytes())
+    assert np.array_equal(eng.batch_sign(level, sks[0], (msgs, off), psi=4096, speculate=False), sigs)
+    flags = eng.batch_verify(level, pks[0], (msgs, off), sigs)
+    assert flags.all()
+    # 1 % corrupted signatures: flags must match the oracle's verdicts
+    bad = sigs.copy()
+    idx = np.arange(0, n, 100)
+    for i in idx:
+        bad[i, int(rng()) % bad.shape[1]] ^= np.uint8(1 << (int(rng()) % 8))
+    f2 = eng.batch_verify(level, pks[0], (msgs, off), bad)
+    assert f2[np.setdiff1d(np.arange(n), idx)].all()
+    for i in idx[::10]:
+        assert f2[i] == oracle.verify(level, pks[0].tobytes(), msgs[32 * i:32 * i + 32].tobytes(), bad[i].tobytes())
+    # per-task keys at full size: round trip
+    sigs_k = eng.batch_sign(level, sks, (msgs, off))
+    assert eng.batch_verify(level, pks, (msgs, off), sigs_k).all()
+    assert not eng.batch_verify(level, np.roll(pks, 1, axis=0), (msgs, off), sigs_k).any()
+
+
+def test_multi_engine_sharded_stream(eng, oracle):
+    """configs[4] shape at reduced size: chunked, sharded execution keeps order and bytes."""
+    from paper_2211_12265_b200.sharding import MultiEngine
+    level, n = 2, 5000
+    rng = mt19937_64(77)
+    pk, sk = oracle.keygen(level, rng.bytes(32))
+    lens = [int(rng()) % 60 for _ in range(n)]
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    flat = np.frombuffer(rng.bytes(int(off[-1]) + 1), np.uint8)
+    me = MultiEngine([0])
+    sk_a, pk_a = np.frombuffer(sk, np.uint8), np.frombuffer(pk, np.uint8)
+    sigs = me.batch_sign(level, sk_a, flat, off, chunk=1024)
+    assert np.array_equal(sigs, eng.batch_sign(level, sk_a, (flat, off)))
+    assert me.batch_verify(level, pk_a, flat, off, sigs, chunk=777).all()
+    me.close()
