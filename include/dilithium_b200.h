@@ -65,6 +65,8 @@ int dlb_set_stream(dlb_ctx* ctx, void* cuda_stream);
 /* INT32 issue-rate microbenchmark (roofline denominator for this path): out[0] LOP3,
  * out[1] IMAD, out[2] SHF, out[3] LOP3+IMAD interleaved, in 10^12 lane-operations/s. */
 int dlb_measure_int32_peak(dlb_ctx* ctx, double out[4]);
+/* out[0] mul.hi.s32 (IMAD.HI), out[1] mul.wide.s32 (IMAD.WIDE), same unit. */
+int dlb_measure_imad_hi_peak(dlb_ctx* ctx, double out[2]);
 
 /* Pinned host memory for callers that want zero-staging transfers (the engine copies
  * straight from/to these buffers with cudaMemcpyAsync). */

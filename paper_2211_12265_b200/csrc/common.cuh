@@ -63,19 +63,40 @@ static_assert(Sizes<Params<5>>::PK == 2592 && Sizes<Params<5>>::SK == 4864 &&
 
 // ---- Montgomery arithmetic, R = 2^32 (values as reduce.hpp:44-51) ---------------
 
-// a*b*R^-1 mod q in (-q, q); needs |a*b| < 2^31 q.  lo(a*b - t*q) == 0 by
-// construction, so the quotient is just the difference of the two high words.
-__device__ __forceinline__ int32_t mont_mul(int32_t a, int32_t b) {
-  const int32_t lo = a * b;
-  const int32_t hi = __mulhi(a, b);
-  const int32_t t = lo * (int32_t)kQInv;
-  return hi - __mulhi(t, kQ);
+// a*b*R^-1 mod q in (-q, q); needs |a*b| < 2^31 q.  Written on 64-bit products so it
+// compiles to IMAD.WIDE / IMAD / IMAD.WIDE: on sm_100a IMAD.WIDE issues at the full
+// fma-pipe rate while IMAD.HI (mul.hi) runs at half rate (measured: 18.5 vs 9.25
+// Tlane-op/s, dlb_measure_imad_hi_peak), so the high word is taken from a wide
+// multiply-add whose low word cancels by construction.
+#ifndef DLB_MONT_WIDE
+#define DLB_MONT_WIDE 0
+#endif
+__device__ __forceinline__ int32_t mont_fold(int64_t p, int32_t t) {
+  int64_t r;  // p - t*q as one wide multiply-add (kept opaque so it is not split into IMAD.HI)
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(t), "r"(-kQ), "l"(p));
+  // The low word is zero by construction; OR-ing it in keeps both halves live so the
+  // full-rate IMAD.WIDE is emitted instead of the half-rate IMAD.HI (one LOP3 on the
+  // otherwise idle alu pipe buys back one fma-pipe slot per product).
+#if DLB_MONT_WIDE
+  return (int32_t)(r >> 32) | (int32_t)r;
+#else
+  return (int32_t)(r >> 32);
+#endif
 }
 
-// same with the constant operand's b*qinv supplied (twiddles): 3 IMAD + 1 IADD
+__device__ __forceinline__ int32_t mont_mul(int32_t a, int32_t b) {
+  int64_t p;
+  asm("mul.wide.s32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+  const int32_t t = (int32_t)p * (int32_t)kQInv;
+  return mont_fold(p, t);
+}
+
+// same with the constant operand's b*qinv supplied (twiddles): IMAD + 2 IMAD.WIDE
 __device__ __forceinline__ int32_t mont_mul_pre(int32_t a, int32_t b, int32_t bq) {
   const int32_t t = a * bq;
-  return __mulhi(a, b) - __mulhi(t, kQ);
+  int64_t p;
+  asm("mul.wide.s32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+  return mont_fold(p, t);
 }
 
 // a mod q, |result| <= 2^22 + 2^8*8191 < q, for any int32 a (cf. reduce.hpp:58-65
@@ -148,17 +169,35 @@ __device__ __forceinline__ uint32_t load_u32_unaligned(const uint8_t* p) {
 }
 
 // bits [bit, bit+width) of an LSB-first little-endian stream, width <= 24.
-// Reads up to 3 bytes past the field's last byte within the same aligned words, so
-// callers keep streams inside 4-byte-padded allocations.
-__device__ __forceinline__ uint32_t load_bits(const uint8_t* base, unsigned bit, unsigned width) {
+// Reads whole aligned 32-bit words, so it never touches a word that holds no byte of
+// the field.  NC = true uses the read-only (ld.global.nc) path and is only for buffers
+// that no thread writes during the kernel; scratch written inside the persistent
+// signing kernel is read with NC = false.
+template <bool NC>
+__device__ __forceinline__ uint32_t load_bits_t(const uint8_t* base, unsigned bit, unsigned width) {
   const uint8_t* p = base + (bit >> 3);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
   const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
   const unsigned sh = (unsigned)(a & 3) * 8 + (bit & 7);
-  const uint32_t lo = __ldg(w);
+  const uint32_t lo = NC ? __ldg(w) : *w;
   uint32_t v = lo >> sh;
-  if (sh + width > 32) v |= __ldg(w + 1) << (32 - sh);
+  if (sh + width > 32) v |= (NC ? __ldg(w + 1) : w[1]) << (32 - sh);
   return v & ((1u << width) - 1);
+}
+
+__device__ __forceinline__ uint32_t load_bits(const uint8_t* base, unsigned bit, unsigned width) {
+  return load_bits_t<true>(base, bit, width);
+}
+
+__device__ __forceinline__ uint32_t load_bits_rw(const uint8_t* base, unsigned bit, unsigned width) {
+  return load_bits_t<false>(base, bit, width);
+}
+
+// L1 prefetch of [p, p+bytes) by one warp (128-byte lines)
+__device__ __forceinline__ void prefetch_l1(const void* p, unsigned bytes, int lane) {
+  const char* c = static_cast<const char*>(p);
+  for (unsigned o = lane * 128u; o < bytes; o += 32u * 128u)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(c + o));
 }
 
 #define DLB_CUDA_CHECK(x)                                   \

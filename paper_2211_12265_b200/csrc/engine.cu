@@ -114,7 +114,7 @@ __global__ void k_dbg_unpack_mask(unsigned n_polys, const uint8_t* ybytes, int32
 }
 
 __global__ void k_dbg_ntt(unsigned n, int32_t* polys, int inverse) {
-  __shared__ int2 zs[256], nzs[256];
+  __shared__ __align__(16) int2 zs[256], nzs[256];
   __shared__ __align__(16) int32_t tiles[4][kTileWords];
   load_twiddles(zs, nzs);
   __syncthreads();
@@ -162,6 +162,11 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev1));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev2));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev3));
+  for (int b = 0; b < 2; ++b) {
+    DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in[b], cudaEventDisableTiming));
+    DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_comp[b], cudaEventDisableTiming));
+    DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out[b], cudaEventDisableTiming));
+  }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   *out = c;
   return 0;
@@ -179,6 +184,11 @@ void dlb_destroy(dlb_ctx* c) {
   cudaEventDestroy(c->ev1);
   cudaEventDestroy(c->ev2);
   cudaEventDestroy(c->ev3);
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(c->ev_in[b]);
+    cudaEventDestroy(c->ev_comp[b]);
+    cudaEventDestroy(c->ev_out[b]);
+  }
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->copy_in);
   cudaStreamDestroy(c->copy_out);
@@ -248,6 +258,47 @@ int dlb_sign_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_sks, si
 }
 
 // ---- host-buffer API -----------------------------------------------------------------
+//
+// Transfers are hidden behind compute (the paper's multi-stream scheme):
+//   keygen / verify  the batch is cut into chunks that flow through three streams --
+//                    H2D of chunk c+1, kernels of chunk c and D2H of chunk c-1 run
+//                    concurrently on double-buffered device arenas;
+//   sign             one persistent kernel covers the whole batch; when the caller's
+//                    signature buffer is pinned (dlb_host_alloc / cudaHostAlloc) the
+//                    commit step stores finished signatures straight into it over PCIe
+//                    while other tasks are still in the rejection loop, so no D2H copy
+//                    remains after the kernel.  Pageable buffers fall back to one
+//                    cudaMemcpy from a device arena.
+
+namespace {
+
+constexpr size_t kPipeChunk = 16384;
+
+struct OwnStream {  // host-buffer calls always run on the engine's own streams
+  dlb_ctx* c;
+  cudaStream_t saved;
+  explicit OwnStream(dlb_ctx* ctx) : c(ctx), saved(ctx->ext) { c->ext = nullptr; }
+  ~OwnStream() { c->ext = saved; }
+};
+
+// device-visible alias of a pinned host pointer, or nullptr for pageable memory
+void* pinned_alias(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type == cudaMemoryTypeHost && at.devicePointer) return at.devicePointer;
+  return nullptr;
+}
+
+#define DLB_CU(x)                                  \
+  do {                                             \
+    const cudaError_t e_ = (x);                    \
+    if (e_ != cudaSuccess) return -1000 - (int)e_; \
+  } while (0)
+
+}  // namespace
 
 int dlb_keygen_batch(dlb_ctx* c, int level, size_t n, const uint8_t* zetas, uint8_t* pks,
                      uint8_t* sks) {
@@ -257,15 +308,37 @@ int dlb_keygen_batch(dlb_ctx* c, int level, size_t n, const uint8_t* zetas, uint
   if (n == 0) return 0;
   if (!zetas || !pks || !sks) return DLB_E_ARG;
   cudaSetDevice(c->device);
-  uint8_t *dz, *dpk, *dsk;
+  OwnStream own(c);
+  cudaStream_t S = c->stream, CO = c->copy_out;
+  const size_t chunk = n < kPipeChunk ? n : kPipeChunk;
+  uint8_t *dz, *dpk[2], *dsk[2];
   DLB_TRY(dalloc(c, "io.zeta", n * 32, &dz));
-  DLB_TRY(dalloc(c, "io.pk", n * ls.pk, &dpk));
-  DLB_TRY(dalloc(c, "io.sk", n * ls.sk, &dsk));
-  DLB_TRY(h2d(c, dz, zetas, n * 32));
-  DLB_TRY(dlb_keygen_batch_dev(c, level, n, dz, dpk, dsk));
-  DLB_TRY(d2h(c, pks, dpk, n * ls.pk));
-  DLB_TRY(d2h(c, sks, dsk, n * ls.sk));
-  return sync(c);
+  DLB_TRY(dalloc(c, "io.pk0", chunk * ls.pk, &dpk[0]));
+  DLB_TRY(dalloc(c, "io.pk1", chunk * ls.pk, &dpk[1]));
+  DLB_TRY(dalloc(c, "io.sk0", chunk * ls.sk, &dsk[0]));
+  DLB_TRY(dalloc(c, "io.sk1", chunk * ls.sk, &dsk[1]));
+  c->launches = 0;
+  DLB_CU(cudaEventRecord(c->ev0, S));
+  DLB_CU(cudaMemcpyAsync(dz, zetas, n * 32, cudaMemcpyHostToDevice, S));
+  size_t ci = 0;
+  for (size_t lo = 0; lo < n; lo += chunk, ++ci) {
+    const size_t cnt = n - lo < chunk ? n - lo : chunk;
+    const int b = (int)(ci & 1);
+    if (ci >= 2) DLB_CU(cudaStreamWaitEvent(S, c->ev_out[b], 0));  // arena b drained
+    DLB_TRY(with_level(level, [&](auto p) {
+      return keygen_dev<decltype(p)>(c, cnt, dz + lo * 32, dpk[b], dsk[b]);
+    }));
+    DLB_CU(cudaEventRecord(c->ev_comp[b], S));
+    DLB_CU(cudaStreamWaitEvent(CO, c->ev_comp[b], 0));
+    DLB_CU(cudaMemcpyAsync(pks + lo * ls.pk, dpk[b], cnt * ls.pk, cudaMemcpyDeviceToHost, CO));
+    DLB_CU(cudaMemcpyAsync(sks + lo * ls.sk, dsk[b], cnt * ls.sk, cudaMemcpyDeviceToHost, CO));
+    DLB_CU(cudaEventRecord(c->ev_out[b], CO));
+  }
+  DLB_CU(cudaEventRecord(c->ev1, S));
+  DLB_CU(cudaStreamSynchronize(CO));
+  DLB_CU(cudaStreamSynchronize(S));
+  cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  return 0;
 }
 
 int dlb_verify_batch(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_stride,
@@ -278,22 +351,46 @@ int dlb_verify_batch(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t
   if (!pks || !msg_off || !sigs || !flags) return DLB_E_ARG;
   if (pk_stride != 0 && pk_stride != ls.pk) return DLB_E_ARG;
   cudaSetDevice(c->device);
+  OwnStream own(c);
+  cudaStream_t S = c->stream, CI = c->copy_in;
   const size_t mbytes = msg_off[n];
-  const size_t nk = pk_stride ? n : 1;
-  uint8_t *dpk, *dm, *dsig, *dfl;
+  const size_t chunk = n < kPipeChunk ? n : kPipeChunk;
+  const size_t pk_cap = pk_stride ? chunk : 1;
+  uint8_t *dpk[2], *dm, *dsig[2], *dfl;
   uint64_t* doff;
-  DLB_TRY(dalloc(c, "io.pk", nk * ls.pk, &dpk));
+  DLB_TRY(dalloc(c, "io.pk0", pk_cap * ls.pk, &dpk[0]));
+  DLB_TRY(dalloc(c, "io.pk1", pk_cap * ls.pk, &dpk[1]));
   DLB_TRY(dalloc(c, "io.msg", mbytes + 8, &dm));
   DLB_TRY(dalloc(c, "io.off", n + 1, &doff));
-  DLB_TRY(dalloc(c, "io.sig", n * ls.sig + 8, &dsig));
+  DLB_TRY(dalloc(c, "io.sig0", chunk * ls.sig + 8, &dsig[0]));
+  DLB_TRY(dalloc(c, "io.sig1", chunk * ls.sig + 8, &dsig[1]));
   DLB_TRY(dalloc(c, "io.flag", n, &dfl));
-  DLB_TRY(h2d(c, dpk, pks, nk * ls.pk));
-  DLB_TRY(h2d(c, dm, msgs, mbytes));
-  DLB_TRY(h2d(c, doff, msg_off, (n + 1) * 8));
-  DLB_TRY(h2d(c, dsig, sigs, n * ls.sig));
-  DLB_TRY(dlb_verify_batch_dev(c, level, n, dpk, pk_stride, dm, doff, dsig, dfl));
-  DLB_TRY(d2h(c, flags, dfl, n));
-  return sync(c);
+  c->launches = 0;
+  DLB_CU(cudaEventRecord(c->ev0, S));
+  if (mbytes) DLB_CU(cudaMemcpyAsync(dm, msgs, mbytes, cudaMemcpyHostToDevice, CI));
+  DLB_CU(cudaMemcpyAsync(doff, msg_off, (n + 1) * 8, cudaMemcpyHostToDevice, CI));
+  if (!pk_stride) DLB_CU(cudaMemcpyAsync(dpk[0], pks, ls.pk, cudaMemcpyHostToDevice, CI));
+  size_t ci = 0;
+  for (size_t lo = 0; lo < n; lo += chunk, ++ci) {
+    const size_t cnt = n - lo < chunk ? n - lo : chunk;
+    const int b = (int)(ci & 1);
+    if (ci >= 2) DLB_CU(cudaStreamWaitEvent(CI, c->ev_comp[b], 0));  // arena b consumed
+    DLB_CU(cudaMemcpyAsync(dsig[b], sigs + lo * ls.sig, cnt * ls.sig, cudaMemcpyHostToDevice, CI));
+    if (pk_stride)
+      DLB_CU(cudaMemcpyAsync(dpk[b], pks + lo * ls.pk, cnt * ls.pk, cudaMemcpyHostToDevice, CI));
+    DLB_CU(cudaEventRecord(c->ev_in[b], CI));
+    DLB_CU(cudaStreamWaitEvent(S, c->ev_in[b], 0));
+    DLB_TRY(with_level(level, [&](auto p) {
+      return verify_dev<decltype(p)>(c, cnt, pk_stride ? dpk[b] : dpk[0], pk_stride, dm, doff + lo,
+                                     dsig[b], dfl + lo);
+    }));
+    DLB_CU(cudaEventRecord(c->ev_comp[b], S));
+  }
+  DLB_CU(cudaMemcpyAsync(flags, dfl, n, cudaMemcpyDeviceToHost, S));
+  DLB_CU(cudaEventRecord(c->ev1, S));
+  DLB_CU(cudaStreamSynchronize(S));
+  cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  return 0;
 }
 
 int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride,
@@ -308,30 +405,45 @@ int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t s
   if (!sks || !msg_off || !sigs) return DLB_E_ARG;
   if (sk_stride != 0 && sk_stride != ls.sk) return DLB_E_ARG;
   cudaSetDevice(c->device);
+  OwnStream own(c);
+  cudaStream_t S = c->stream;
   const size_t mbytes = msg_off[n];
   const size_t nk = sk_stride ? n : 1;
   uint8_t *dsk, *dm, *dsig, *dfail, *drp = nullptr;
   uint64_t* doff;
   uint32_t* datt;
+  uint8_t* zero_copy = static_cast<uint8_t*>(pinned_alias(sigs));  // pinned: write in place
   DLB_TRY(dalloc(c, "io.sk", nk * ls.sk, &dsk));
   DLB_TRY(dalloc(c, "io.msg", mbytes + 8, &dm));
   DLB_TRY(dalloc(c, "io.off", n + 1, &doff));
-  DLB_TRY(dalloc(c, "io.sig", n * ls.sig + 8, &dsig));
+  if (!zero_copy) DLB_TRY(dalloc(c, "io.sig", n * ls.sig + 8, &dsig));
+  else dsig = zero_copy;
   DLB_TRY(dalloc(c, "io.att", n, &datt));
   DLB_TRY(dalloc(c, "io.fail", n, &dfail));
-  DLB_TRY(h2d(c, dsk, sks, nk * ls.sk));
-  DLB_TRY(h2d(c, dm, msgs, mbytes));
-  DLB_TRY(h2d(c, doff, msg_off, (n + 1) * 8));
+  DLB_CU(cudaMemcpyAsync(dsk, sks, nk * ls.sk, cudaMemcpyHostToDevice, S));
+  if (mbytes) DLB_CU(cudaMemcpyAsync(dm, msgs, mbytes, cudaMemcpyHostToDevice, S));
+  DLB_CU(cudaMemcpyAsync(doff, msg_off, (n + 1) * 8, cudaMemcpyHostToDevice, S));
   if (rho_prime) {
     DLB_TRY(dalloc(c, "io.rp", n * 64, &drp));
-    DLB_TRY(h2d(c, drp, rho_prime, n * 64));
+    DLB_CU(cudaMemcpyAsync(drp, rho_prime, n * 64, cudaMemcpyHostToDevice, S));
   }
-  DLB_TRY(dlb_sign_batch_dev(c, level, n, dsk, sk_stride, dm, doff, drp, psi, speculate, dsig, datt,
-                             dfail, stats));
-  DLB_TRY(d2h(c, sigs, dsig, n * ls.sig));
-  if (attempts) DLB_TRY(d2h(c, attempts, datt, n * 4));
-  if (failed) DLB_TRY(d2h(c, failed, dfail, n));
-  return sync(c);
+  c->launches = 0;
+  DLB_CU(cudaEventRecord(c->ev0, S));
+  const int rc = with_level(level, [&](auto p) {
+    return sign_dev<decltype(p)>(c, n, dsk, sk_stride, dm, doff, drp, psi, speculate, dsig, datt,
+                                 dfail, stats);
+  });
+  DLB_CU(cudaEventRecord(c->ev1, S));
+  if (rc != 0) {
+    cudaStreamSynchronize(S);
+    return rc;
+  }
+  if (!zero_copy) DLB_CU(cudaMemcpyAsync(sigs, dsig, n * ls.sig, cudaMemcpyDeviceToHost, S));
+  if (attempts) DLB_CU(cudaMemcpyAsync(attempts, datt, n * 4, cudaMemcpyDeviceToHost, S));
+  if (failed) DLB_CU(cudaMemcpyAsync(failed, dfail, n, cudaMemcpyDeviceToHost, S));
+  DLB_CU(cudaStreamSynchronize(S));
+  cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  return 0;
 }
 
 // ---- stage-level entry points -----------------------------------------------------------

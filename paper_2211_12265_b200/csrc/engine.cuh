@@ -36,6 +36,7 @@ struct dlb_ctx {
   cudaStream_t copy_out = nullptr;    // D2H stream
   cudaStream_t ext = nullptr;         // caller's stream for *_dev calls (optional)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};  // chunk pipeline hand-offs
   float last_ms = 0.f, last_main_ms = 0.f;  // whole call / dominant kernel only
   unsigned launches = 0;
   int sm_count = 148;

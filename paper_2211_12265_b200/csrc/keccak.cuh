@@ -34,8 +34,8 @@ __device__ __forceinline__ uint64_t rotl64(uint64_t x) {
     nlo = __funnelshift_l(hi, lo, R);
     nhi = __funnelshift_l(lo, hi, R);
   } else {
-    nlo = __funnelshift_l(lo, hi, R - 32);
-    nhi = __funnelshift_l(hi, lo, R - 32);
+    nlo = __funnelshift_l(lo, hi, (R - 32) & 31);
+    nhi = __funnelshift_l(hi, lo, (R - 32) & 31);
   }
   return ((uint64_t)nhi << 32) | nlo;
 }

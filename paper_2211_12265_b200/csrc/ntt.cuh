@@ -69,13 +69,19 @@ __device__ __forceinline__ void ntt_fwd(int32_t (&r)[8], int32_t* tile, const in
     const int2 z = zs[8 + b];
 #pragma unroll
     for (int i = 0; i < 4; ++i) ct_bfly(r[i], r[i + 4], z);
-    const int2 z0 = zs[16 + 2 * b], z1 = zs[17 + 2 * b];
+    // twiddle pairs / quads are fetched as 128-bit shared loads (no bank conflicts)
+    const int4 zp = *reinterpret_cast<const int4*>(zs + 16 + 2 * b);
+    const int2 z0 = make_int2(zp.x, zp.y), z1 = make_int2(zp.z, zp.w);
     ct_bfly(r[0], r[2], z0);
     ct_bfly(r[1], r[3], z0);
     ct_bfly(r[4], r[6], z1);
     ct_bfly(r[5], r[7], z1);
-#pragma unroll
-    for (int i = 0; i < 8; i += 2) ct_bfly(r[i], r[i + 1], zs[32 + 4 * b + i / 2]);
+    const int4 qa = *reinterpret_cast<const int4*>(zs + 32 + 4 * b);
+    const int4 qb = *reinterpret_cast<const int4*>(zs + 34 + 4 * b);
+    ct_bfly(r[0], r[1], make_int2(qa.x, qa.y));
+    ct_bfly(r[2], r[3], make_int2(qa.z, qa.w));
+    ct_bfly(r[4], r[5], make_int2(qb.x, qb.y));
+    ct_bfly(r[6], r[7], make_int2(qb.z, qb.w));
   }
   __syncwarp();
 #pragma unroll
@@ -90,13 +96,18 @@ __device__ __forceinline__ void ntt_fwd(int32_t (&r)[8], int32_t* tile, const in
   }
   // pass C: c = 8 lane + m; levels len = 2, 1
   {
-    const int2 z0 = zs[64 + 2 * lane], z1 = zs[65 + 2 * lane];
+    const int4 zp = *reinterpret_cast<const int4*>(zs + 64 + 2 * lane);
+    const int2 z0 = make_int2(zp.x, zp.y), z1 = make_int2(zp.z, zp.w);
     ct_bfly(r[0], r[2], z0);
     ct_bfly(r[1], r[3], z0);
     ct_bfly(r[4], r[6], z1);
     ct_bfly(r[5], r[7], z1);
-#pragma unroll
-    for (int m = 0; m < 8; m += 2) ct_bfly(r[m], r[m + 1], zs[128 + 4 * lane + m / 2]);
+    const int4 qa = *reinterpret_cast<const int4*>(zs + 128 + 4 * lane);
+    const int4 qb = *reinterpret_cast<const int4*>(zs + 130 + 4 * lane);
+    ct_bfly(r[0], r[1], make_int2(qa.x, qa.y));
+    ct_bfly(r[2], r[3], make_int2(qa.z, qa.w));
+    ct_bfly(r[4], r[5], make_int2(qb.x, qb.y));
+    ct_bfly(r[6], r[7], make_int2(qb.z, qb.w));
   }
   __syncwarp();  // tile free for the caller
 }
@@ -104,10 +115,17 @@ __device__ __forceinline__ void ntt_fwd(int32_t (&r)[8], int32_t* tile, const in
 __device__ __forceinline__ void ntt_inv(int32_t (&r)[8], int32_t* tile, const int2* nzs, int lane) {
   // pass C': c = 8 lane + m; levels len = 1, 2, 4.  Level with G = 128/len groups
   // uses twiddle index 2G-1-g for group g (the reference's --k walk).
-#pragma unroll
-  for (int m = 0; m < 8; m += 2) gs_bfly(r[m], r[m + 1], nzs[255 - 4 * lane - m / 2]);
   {
-    const int2 z0 = nzs[127 - 2 * lane], z1 = nzs[126 - 2 * lane];
+    const int4 qa = *reinterpret_cast<const int4*>(nzs + 252 - 4 * lane);  // [252-4l, 253-4l]
+    const int4 qb = *reinterpret_cast<const int4*>(nzs + 254 - 4 * lane);  // [254-4l, 255-4l]
+    gs_bfly(r[0], r[1], make_int2(qb.z, qb.w));
+    gs_bfly(r[2], r[3], make_int2(qb.x, qb.y));
+    gs_bfly(r[4], r[5], make_int2(qa.z, qa.w));
+    gs_bfly(r[6], r[7], make_int2(qa.x, qa.y));
+  }
+  {
+    const int4 zp = *reinterpret_cast<const int4*>(nzs + 126 - 2 * lane);
+    const int2 z0 = make_int2(zp.z, zp.w), z1 = make_int2(zp.x, zp.y);
     gs_bfly(r[0], r[2], z0);
     gs_bfly(r[1], r[3], z0);
     gs_bfly(r[4], r[6], z1);
@@ -127,10 +145,17 @@ __device__ __forceinline__ void ntt_inv(int32_t (&r)[8], int32_t* tile, const in
 #pragma unroll
   for (int i = 0; i < 8; ++i) r[i] = tile[v + 8 * i + 72 * h + 4 * (i >> 2)];
   // pass B': levels len = 8, 16, 32
-#pragma unroll
-  for (int i = 0; i < 8; i += 2) gs_bfly(r[i], r[i + 1], nzs[31 - 4 * h - i / 2]);
   {
-    const int2 z0 = nzs[15 - 2 * h], z1 = nzs[14 - 2 * h];
+    const int4 qa = *reinterpret_cast<const int4*>(nzs + 28 - 4 * h);
+    const int4 qb = *reinterpret_cast<const int4*>(nzs + 30 - 4 * h);
+    gs_bfly(r[0], r[1], make_int2(qb.z, qb.w));
+    gs_bfly(r[2], r[3], make_int2(qb.x, qb.y));
+    gs_bfly(r[4], r[5], make_int2(qa.z, qa.w));
+    gs_bfly(r[6], r[7], make_int2(qa.x, qa.y));
+  }
+  {
+    const int4 zp = *reinterpret_cast<const int4*>(nzs + 14 - 2 * h);
+    const int2 z0 = make_int2(zp.z, zp.w), z1 = make_int2(zp.x, zp.y);
     gs_bfly(r[0], r[2], z0);
     gs_bfly(r[1], r[3], z0);
     gs_bfly(r[4], r[6], z1);

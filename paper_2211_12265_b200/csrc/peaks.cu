@@ -24,9 +24,13 @@ __global__ void __launch_bounds__(256) k_peak_int32(uint32_t* out, int iters, ui
           asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(a), "r"(b));
         } else if (MODE == 2) {
           asm volatile("shf.l.wrap.b32 %0, %0, %1, 7;" : "+r"(x[i]) : "r"(x[(i + 1) & 7]));
-        } else {
+        } else if (MODE == 3) {
           if (i & 1) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[i]) : "r"(a), "r"(b));
           else asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(a), "r"(b));
+        } else if (MODE == 4) {
+          asm volatile("mul.hi.s32 %0, %0, %1;" : "+r"(x[i]) : "r"(a));
+        } else {
+          asm volatile("{ .reg .b64 t; mul.wide.s32 t, %0, %1; mov.b64 {%0, _}, t; }" : "+r"(x[i]) : "r"(a));
         }
       }
     }
@@ -70,5 +74,17 @@ extern "C" int dlb_measure_int32_peak(dlb_ctx* c, double* out) {
   DLB_TRY(dlb::run_peak<1>(c, scratch, &out[1]));
   DLB_TRY(dlb::run_peak<2>(c, scratch, &out[2]));
   DLB_TRY(dlb::run_peak<3>(c, scratch, &out[3]));
+  return 0;
+}
+
+// out[0] mul.hi.s32 (IMAD.HI), out[1] mul.wide.s32 (IMAD.WIDE): the Montgomery-product
+// building blocks, same unit as above
+extern "C" int dlb_measure_imad_hi_peak(dlb_ctx* c, double* out) {
+  if (!c || !out) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  uint32_t* scratch;
+  DLB_TRY(dlb::dalloc(c, "peak", 64, &scratch));
+  DLB_TRY(dlb::run_peak<4>(c, scratch, &out[0]));
+  DLB_TRY(dlb::run_peak<5>(c, scratch, &out[1]));
   return 0;
 }

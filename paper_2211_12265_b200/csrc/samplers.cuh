@@ -168,14 +168,16 @@ __device__ __forceinline__ void expand_mask_stream(const uint64_t* __restrict__ 
   s[16] = 0x8000000000000000ull;
   uint64_t* out = reinterpret_cast<uint64_t*>(dst);
 #pragma unroll 1
-  for (int blk = 0; blk < FULL; ++blk) {
+  for (int blk = 0; blk <= FULL; ++blk) {  // one permutation call site
     keccak_f1600(s);
+    if (blk < FULL) {
 #pragma unroll
-    for (int w = 0; w < kWords256; ++w) out[blk * kWords256 + w] = s[w];
+      for (int w = 0; w < kWords256; ++w) out[blk * kWords256 + w] = s[w];
+    } else {
+#pragma unroll
+      for (int w = 0; w < TAILW; ++w) out[FULL * kWords256 + w] = s[w];
+    }
   }
-  keccak_f1600(s);
-#pragma unroll
-  for (int w = 0; w < TAILW; ++w) out[FULL * kWords256 + w] = s[w];
 }
 
 // ---------------------------------------------------------------- SampleInBall
@@ -195,15 +197,20 @@ __device__ __forceinline__ void sample_in_ball_words(const uint64_t (&ct)[4],
   uint32_t* row32 = reinterpret_cast<uint32_t*>(row);
 #pragma unroll
   for (int w = 0; w < 64; ++w) row32[w] = 0;
-  keccak_f1600(s);
-  uint64_t signs = s[0];
+  // One permutation call site and a rolled walk over the squeezed words keep this
+  // (once-per-attempt, inherently sequential) routine small in the instruction cache;
+  // lanes leave the walk as soon as their tau positions are placed.
+  uint64_t signs = 0;
   unsigned i = kN - TAU;
-  bool first = true;
+  int wstart = 1;  // bytes 0..7 of the first block are the sign bits
   while (true) {
+    keccak_f1600(s);
+    if (wstart) signs = s[0];
+#pragma unroll 1
+    for (int w = wstart; w < kWords256 && i < (unsigned)kN; ++w) {
+      uint64_t v = s[0];
 #pragma unroll
-    for (int w = 0; w < kWords256; ++w) {
-      if (w == 0 && first) continue;  // bytes 0..7 of the first block are the sign bits
-      const uint64_t v = s[w];
+      for (int k = 1; k < kWords256; ++k) v = (w == k) ? s[k] : v;  // register select, no local mem
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const unsigned b = (unsigned)(v >> (8 * e)) & 0xFF;
@@ -216,8 +223,7 @@ __device__ __forceinline__ void sample_in_ball_words(const uint64_t (&ct)[4],
       }
     }
     if (i >= (unsigned)kN) break;
-    first = false;
-    keccak_f1600(s);
+    wstart = 0;
   }
 }
 
@@ -334,10 +340,9 @@ static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_
 
 // c~ = SHAKE256(mu || w1_packed, 32)  (scheme.hpp:158-163,311-317) for one stream:
 // mu 8 words (global, aligned), w1 W1_ALL bytes (global, 8-byte aligned).
-template <int W1_ALL>
+template <int W1_ALL, bool NC = true>
 __device__ __forceinline__ void hash_ctilde_stream(const uint64_t* __restrict__ mu,
-                                                   const uint64_t* __restrict__ w1,
-                                                   uint64_t (&out)[4]) {
+                                                   const uint64_t* w1, uint64_t (&out)[4]) {
   static_assert(W1_ALL % 8 == 0, "w1 block is word aligned");
   constexpr int TOTALW = 8 + W1_ALL / 8;          // message words
   constexpr int NBLK = TOTALW / kWords256 + 1;    // incl. the padding block
@@ -350,7 +355,7 @@ __device__ __forceinline__ void hash_ctilde_stream(const uint64_t* __restrict__ 
       const int idx = blk * kWords256 + w;  // message word index
       uint64_t v = 0;
       if (idx < 8) v = __ldg(mu + idx);
-      else if (idx < TOTALW) v = __ldg(w1 + (idx - 8));
+      else if (idx < TOTALW) v = NC ? __ldg(w1 + (idx - 8)) : w1[idx - 8];
       else if (idx == TOTALW) v = 0x1F;
       s[w] ^= v;
     }

@@ -27,6 +27,9 @@
 
 namespace dlb {
 
+#ifndef DLB_SIGN_MINB
+#define DLB_SIGN_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr int kSignThreads = 128;          // threads = attempt slots per CTA
 constexpr int kSignWarps = kSignThreads / 32;
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
@@ -40,7 +43,7 @@ __global__ void __launch_bounds__(WARPS * 32)
                   int32_t* __restrict__ shat, unsigned* __restrict__ key_bad) {
   using S = Sizes<P>;
   constexpr int PV = P::L + 2 * P::K;
-  __shared__ int2 zs[256], nzs[256];
+  __shared__ __align__(16) int2 zs[256], nzs[256];
   __shared__ __align__(16) int32_t tiles[WARPS][kTileWords];
   load_twiddles(zs, nzs);
   __syncthreads();
@@ -145,7 +148,7 @@ __device__ __forceinline__ void stage_w(WarpScratch<P>& ws, const int2* zs, cons
     const uint8_t* yb = ybytes + j * S::Z_POLY;
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      r[e] = P::GAMMA1 - (int32_t)load_bits(yb, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
+      r[e] = P::GAMMA1 - (int32_t)load_bits_rw(yb, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
     ntt_fwd(r, ws.tile, zs, lane);
 #pragma unroll
     for (int m = 0; m < 8; ++m) ws.vhat[j][m][lane] = r[m];
@@ -203,45 +206,47 @@ __device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, const int2* zs,
   for (int e = 0; e < 8; ++e) ch[e] = c8[lane + 32 * e];
   ntt_fwd(ch, ws.tile, zs, lane);
 
-  // z = y + c s1, ||z|| < gamma1 - beta  (scheme.hpp:167-174)
-#pragma unroll 1
-  for (int j = 0; j < P::L; ++j) {
-    mul_challenge(t, ch, shat + (size_t)j * kN, ws.tile, nzs, lane);
-    const uint8_t* yb = ybytes + j * S::Z_POLY;
-    bool bad = false;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int32_t y = P::GAMMA1 - (int32_t)load_bits(yb, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
-      const int32_t z = center(freeze(y + t[e]));
-      bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
-      ws.vhat[j][e][lane] = z;
-    }
-    if (__any_sync(FULL, bad)) return false;
-  }
-  // r0 = LowBits(w - c s2), c t0, hints  (scheme.hpp:177-215), row by row
+  // One loop over the L + 2K products c*s (one inverse-NTT instance in the instruction
+  // stream): s1_0..s1_{L-1}, then (s2_i, t0_i) row by row.  Every exit is warp-uniform.
+  //   z = y + c s1, ||z|| < gamma1 - beta                      (scheme.hpp:167-174)
+  //   r0 = LowBits(w - c s2), ||r0|| < gamma2 - beta            (scheme.hpp:177-190)
+  //   ||c t0|| < gamma2, h = [HB(w - c s2 + c t0) != HB(w - c s2)]   (scheme.hpp:192-215)
   unsigned weight = 0;
+  int32_t wcs2[8], hb0[8];
 #pragma unroll 1
-  for (int i = 0; i < P::K; ++i) {
-    mul_challenge(t, ch, shat + (size_t)(P::L + i) * kN, ws.tile, nzs, lane);
-    int32_t wcs2[8], hb0[8];
+  for (int p = 0; p < P::L + 2 * P::K; ++p) {
+    const int q = p - P::L, i = q >> 1;
+    const bool is_t0 = (q & 1) != 0;
+    const int poly = p < P::L ? p : (is_t0 ? P::L + P::K + i : P::L + i);
+    mul_challenge(t, ch, shat + (size_t)poly * kN, ws.tile, nzs, lane);
     bool bad = false;
+    if (p < P::L) {
+      const uint8_t* yb = ybytes + p * S::Z_POLY;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      wcs2[e] = freeze(win[i * kN + lane + 32 * e] - t[e]);
-      int32_t r0;
-      hb0[e] = decompose<P::GAMMA2>(wcs2[e], r0);
-      bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
-    }
-    if (__any_sync(FULL, bad)) return false;
-    mul_challenge(t, ch, shat + (size_t)(P::L + P::K + i) * kN, ws.tile, nzs, lane);
+      for (int e = 0; e < 8; ++e) {
+        const int32_t y = P::GAMMA1 - (int32_t)load_bits_rw(yb, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
+        const int32_t z = center(freeze(y + t[e]));
+        bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
+        ws.vhat[p][e][lane] = z;
+      }
+    } else if (!is_t0) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int32_t vt = center(caddq(t[e]));
-      bad = bad || abs(vt) >= P::GAMMA2;
-      const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != hb0[e];
-      const unsigned mask = __ballot_sync(FULL, h);
-      if (lane == 0) ws.hbits[i][e] = mask;
-      weight += __popc(mask);
+      for (int e = 0; e < 8; ++e) {
+        wcs2[e] = freeze(win[i * kN + lane + 32 * e] - t[e]);
+        int32_t r0;
+        hb0[e] = decompose<P::GAMMA2>(wcs2[e], r0);
+        bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int32_t vt = center(caddq(t[e]));
+        bad = bad || abs(vt) >= P::GAMMA2;
+        const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != hb0[e];
+        const unsigned mask = __ballot_sync(FULL, h);
+        if (lane == 0) ws.hbits[i][e] = mask;
+        weight += __popc(mask);
+      }
     }
     if (__any_sync(FULL, bad)) return false;
   }
@@ -275,7 +280,7 @@ __device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, const int2* zs,
 }
 
 template <class P>
-__global__ void __launch_bounds__(kSignThreads, 4) k_sign_persistent(SignArgs a) {
+__global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent(SignArgs a) {
   using S = Sizes<P>;
   using Z = SignSizes<P>;
   __shared__ __align__(16) SignSmem<P> sm;
@@ -358,6 +363,8 @@ __global__ void __launch_bounds__(kSignThreads, 4) k_sign_persistent(SignArgs a)
       const unsigned task = sm.slot_task[s];
       if (task == kNoSlot) continue;
       const size_t key = (size_t)task * a.key_stride;
+      if (s + kSignWarps < kSignThreads)  // next slot of this warp: pull its masks into L1
+        prefetch_l1(ybytes + (size_t)(s + kSignWarps) * Z::Y_SLOT, Z::Y_SLOT, lane);
       stage_w<P>(sm.u.ws[warp], sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
                  a.A + key * (P::K * P::L * kN), wbuf + (size_t)s * Z::W_SLOT,
                  w1buf + (size_t)s * S::W1_ALL);
@@ -368,7 +375,7 @@ __global__ void __launch_bounds__(kSignThreads, 4) k_sign_persistent(SignArgs a)
     {
       if (my_task != kNoSlot) {
         uint64_t ct[4];
-        hash_ctilde_stream<S::W1_ALL>(a.mu + (size_t)my_task * 8,
+        hash_ctilde_stream<S::W1_ALL, false>(a.mu + (size_t)my_task * 8,
                                       reinterpret_cast<const uint64_t*>(w1buf + (size_t)tid * S::W1_ALL),
                                       ct);
 #pragma unroll
@@ -394,6 +401,12 @@ __global__ void __launch_bounds__(kSignThreads, 4) k_sign_persistent(SignArgs a)
       const unsigned task = sm.slot_task[s];
       if (task == kNoSlot) continue;
       const size_t key = (size_t)task * a.key_stride;
+      if (s + kSignWarps < kSignThreads) {
+        const int nx = s + kSignWarps;
+        prefetch_l1(c8buf + (size_t)nx * kN, kN, lane);
+        prefetch_l1(ybytes + (size_t)nx * Z::Y_SLOT, S::Z_POLY, lane);
+        prefetch_l1(wbuf + (size_t)nx * Z::W_SLOT, 1024, lane);
+      }
       const bool ok = stage_finish<P>(sm.u.ws[warp], sm.zs, sm.nzs, lane,
                                       ybytes + (size_t)s * Z::Y_SLOT, wbuf + (size_t)s * Z::W_SLOT,
                                       c8buf + (size_t)s * kN, ctbuf + s * 4,
@@ -462,12 +475,18 @@ __global__ void __launch_bounds__(kSignThreads, 4) k_sign_persistent(SignArgs a)
         if (win < 0) continue;
         const uint8_t* src = staging + (size_t)win * Z::SIG_PAD;
         uint8_t* dst = a.sigs + (size_t)sm.utask[u] * S::SIG;
-        if ((S::SIG & 3) == 0) {
-          for (int w = lane; w < S::SIG / 4; w += 32)
-            reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(src)[w];
-        } else {
-          for (int b = lane; b < S::SIG; b += 32) dst[b] = src[b];
-        }
+        // word-granular, coalesced copy to a destination of any alignment (sig_bytes is
+        // odd at levels 3/5): the destination may be pinned host memory, where 128-byte
+        // write bursts matter
+        const unsigned head = (4u - (unsigned)(reinterpret_cast<uintptr_t>(dst) & 3)) & 3u;
+        if (lane < (int)head) dst[lane] = src[lane];
+        const unsigned nwords = (S::SIG - head) / 4;
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
+        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);  // staging is 16-byte aligned
+        for (unsigned w = lane; w < nwords; w += 32)
+          d32[w] = head ? __funnelshift_r(s32[w], s32[w + 1], 8 * head) : s32[w];
+        const unsigned done = head + 4 * nwords;
+        if (lane < (int)(S::SIG - done)) dst[done + lane] = src[done + lane];
       }
       __syncthreads();
       if (keep) {

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(WARPS * 32)
                    const int8_t* __restrict__ c8, uint8_t* __restrict__ w1buf,
                    uint8_t* __restrict__ pre_ok) {
   using S = Sizes<P>;
-  __shared__ int2 zs[256], nzs[256];
+  __shared__ __align__(16) int2 zs[256], nzs[256];
   __shared__ __align__(16) WarpScratch<P> scratch[WARPS];
   load_twiddles(zs, nzs);
   __syncthreads();
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(WARPS * 32)
                    const int32_t* __restrict__ A, uint8_t* __restrict__ pk,
                    uint8_t* __restrict__ sk) {
   using S = Sizes<P>;
-  __shared__ int2 zs[256], nzs[256];
+  __shared__ __align__(16) int2 zs[256], nzs[256];
   __shared__ __align__(16) WarpScratch<P> scratch[WARPS];
   load_twiddles(zs, nzs);
   __syncthreads();

@@ -28,7 +28,8 @@ class SignStats(C.Structure):
 
 
 def lib_path():
-    return os.path.join(_HERE, "libdilithium_b200.so")
+    # DLB_LIB selects an alternative build of the same library (A/B kernel experiments)
+    return os.environ.get("DLB_LIB") or os.path.join(_HERE, "libdilithium_b200.so")
 
 
 _lib = None
@@ -55,6 +56,7 @@ def load_library():
         "dlb_last_launches": (C.c_uint, [vp]),
         "dlb_set_stream": (C.c_int, [vp, vp]),
         "dlb_measure_int32_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "dlb_measure_imad_hi_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "dlb_host_alloc": (vp, [sz]),
         "dlb_host_free": (None, [vp]),
         "dlb_keygen_batch": (C.c_int, [vp, C.c_int, sz, _u8p, _u8p, _u8p]),
@@ -84,7 +86,7 @@ def load_library():
 
 EXPORTED_SYMBOLS = [
     "dlb_create", "dlb_destroy", "dlb_version", "dlb_last_kernel_ms", "dlb_last_main_kernel_ms", "dlb_last_launches",
-    "dlb_set_stream", "dlb_measure_int32_peak", "dlb_host_alloc", "dlb_host_free", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
+    "dlb_set_stream", "dlb_measure_int32_peak", "dlb_measure_imad_hi_peak", "dlb_host_alloc", "dlb_host_free", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
     "dlb_keygen_batch_dev", "dlb_sign_batch_dev", "dlb_verify_batch_dev", "dlb_dbg_keccak_f1600",
     "dlb_dbg_shake256", "dlb_dbg_expand_a", "dlb_dbg_expand_s", "dlb_dbg_expand_mask",
     "dlb_dbg_sample_in_ball", "dlb_dbg_ntt", "dlb_dbg_sign_attempt",
@@ -153,7 +155,10 @@ class Engine:
     def measure_int32_peak(self):
         out = (C.c_double * 4)()
         self._chk(self.lib.dlb_measure_int32_peak(self.ctx, out), "dlb_measure_int32_peak")
-        return {"lop3": out[0], "imad": out[1], "shf": out[2], "lop3_imad_mix": out[3]}
+        hi = (C.c_double * 2)()
+        self._chk(self.lib.dlb_measure_imad_hi_peak(self.ctx, hi), "dlb_measure_imad_hi_peak")
+        return {"lop3": out[0], "imad": out[1], "shf": out[2], "lop3_imad_mix": out[3],
+                "imad_hi": hi[0], "imad_wide": hi[1]}
 
     # ---- batch.hpp:159-166
     def batch_keygen(self, level, zetas):
