@@ -33,6 +33,7 @@ namespace dlb {
 constexpr int kSignThreads = 128;          // threads = attempt slots per CTA
 constexpr int kSignWarps = kSignThreads / 32;
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+constexpr int kChunkBytes = 1024;  // cp.async landing buffer: one packed polynomial
 
 // ---- per-key precomputation -----------------------------------------------------------
 // One warp per (key, polynomial): s1 (L), s2 (K), t0 (K) unpacked from the secret key,
@@ -122,7 +123,10 @@ template <class P>
 struct SignSmem {
   int2 zs[256], nzs[256];
   union {
-    WarpScratch<P> ws[kSignWarps];
+    struct {
+      WarpScratch<P> ws[kSignWarps];
+      uint8_t pre[kSignWarps][4][kChunkBytes];  // cp.async landing buffers: head x2, ring x2
+    } a;
     int8_t rows[kSignThreads][kByteRowStride];
   } u;
   uint32_t utask[kSignThreads];    // open tasks of this CTA (compact)
@@ -136,19 +140,66 @@ struct SignSmem {
   unsigned U, newU, got, base;
 };
 
-// S2: w = INTT(A * NTT(y)), w1 = HighBits(w) packed (scheme.hpp:141-156)
+// ---- asynchronous scratch prefetch ----------------------------------------------------
+// The per-slot scratch (masks y, w) of all resident CTAs is far larger than L2, so the
+// warp-per-slot stages would eat one DRAM latency per polynomial.  Each warp therefore
+// streams its inputs through small shared-memory buffers with cp.async, one chunk
+// (= one packed polynomial, <= 1 KiB) ahead of the arithmetic: `head` holds c | y_0 of
+// a slot (fetched while the previous slot is processed), `ring` the remaining chunks.
+
+struct SlotPipe {
+  uint8_t* base;  // 4 * kChunkBytes of shared memory: head 0, head 1, ring 0, ring 1
+  unsigned k;     // ring chunks issued so far (buffer = k & 1), warp-uniform
+  __device__ __forceinline__ uint8_t* head(int par) const { return base + (par & 1) * kChunkBytes; }
+  __device__ __forceinline__ uint8_t* ring(unsigned i) const {
+    return base + (2 + (i & 1)) * kChunkBytes;
+  }
+};
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// one warp copies `bytes` (multiple of 16, 16-byte aligned) global -> shared, no commit
+__device__ __forceinline__ void warp_fetch(uint8_t* sdst, const void* gsrc, unsigned bytes, int lane) {
+  const uint8_t* g = static_cast<const uint8_t*>(gsrc);
+  for (unsigned o = lane * 16u; o < bytes; o += 512u) cp_async16(sdst + o, g + o);
+}
+
+// bits [bit, bit+width) of a 4-byte aligned shared-memory stream (reads one word past
+// the field: buffers are kChunkBytes long, fields end well before)
+__device__ __forceinline__ uint32_t load_bits_s(const uint8_t* sbase, unsigned bit, unsigned width) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(sbase) + (bit >> 5);
+  return __funnelshift_r(w[0], w[1], bit & 31) & ((1u << width) - 1);
+}
+
+// S2: w = INTT(A * NTT(y)), w1 = HighBits(w) packed (scheme.hpp:141-156).
+// Precondition: ring chunk y_0 of this slot already issued; `next_y` = y bytes of the
+// warp's next active slot (nullptr if none): its y_0 is issued during the last polynomial.
 template <class P>
-__device__ __forceinline__ void stage_w(WarpScratch<P>& ws, const int2* zs, const int2* nzs,
-                                        int lane, const uint8_t* ybytes, const int32_t* A,
-                                        int32_t* wout, uint8_t* w1out) {
+__device__ __forceinline__ void stage_w(WarpScratch<P>& ws, SlotPipe& pp, const int2* zs,
+                                        const int2* nzs, int lane, const uint8_t* ybytes,
+                                        const uint8_t* next_y, const int32_t* A, int32_t* wout,
+                                        uint8_t* w1out) {
   using S = Sizes<P>;
   int32_t r[8];
 #pragma unroll 1
   for (int j = 0; j < P::L; ++j) {
-    const uint8_t* yb = ybytes + j * S::Z_POLY;
+    const uint8_t* cur = pp.ring(pp.k - 1);  // chunk y_j
+    if (j + 1 < P::L) warp_fetch(pp.ring(pp.k), ybytes + (j + 1) * S::Z_POLY, S::Z_POLY, lane);
+    else if (next_y) warp_fetch(pp.ring(pp.k), next_y, S::Z_POLY, lane);
+    cp_async_commit();
+    ++pp.k;
+    cp_async_wait<1>();
+    __syncwarp();
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      r[e] = P::GAMMA1 - (int32_t)load_bits_rw(yb, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
+      r[e] = P::GAMMA1 - (int32_t)load_bits_s(cur, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
     ntt_fwd(r, ws.tile, zs, lane);
 #pragma unroll
     for (int m = 0; m < 8; ++m) ws.vhat[j][m][lane] = r[m];
@@ -158,10 +209,16 @@ __device__ __forceinline__ void stage_w(WarpScratch<P>& ws, const int2* zs, cons
     int32_t acc[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) acc[m] = 0;
+    // the cached matrix row streams through registers one polynomial ahead of its use
+    const int4* ap = reinterpret_cast<const int4*>(A + (size_t)(i * P::L) * kN) + 2 * lane;
+    int4 n0 = __ldg(ap), n1 = __ldg(ap + 1);
 #pragma unroll 1
     for (int j = 0; j < P::L; ++j) {
-      const int4* ap = reinterpret_cast<const int4*>(A + (size_t)(i * P::L + j) * kN) + 2 * lane;
-      const int4 a0 = __ldg(ap), a1 = __ldg(ap + 1);
+      const int4 a0 = n0, a1 = n1;
+      if (j + 1 < P::L) {
+        n0 = __ldg(ap + (j + 1) * (kN / 4));
+        n1 = __ldg(ap + (j + 1) * (kN / 4) + 1);
+      }
       const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
       for (int m = 0; m < 8; ++m) acc[m] += mont_mul(a[m], ws.vhat[j][m][lane]);
@@ -192,18 +249,47 @@ __device__ __forceinline__ void mul_challenge(int32_t (&out)[8], const int32_t (
   ntt_inv(out, tile, nzs, lane);
 }
 
+// issue the head chunk (c | y_0) of a slot into pp.head(par); caller commits
+template <class P>
+__device__ __forceinline__ void fetch_head(SlotPipe& pp, int par, const int8_t* c8,
+                                           const uint8_t* ybytes, int lane) {
+  warp_fetch(pp.head(par), c8, kN, lane);
+  warp_fetch(pp.head(par) + kN, ybytes, Sizes<P>::Z_POLY, lane);
+}
+
 // S4: everything after the challenge (scheme.hpp:165-215) + signature packing into the
 // slot's staging buffer (packing.hpp:236-254).  Warp-uniform return: accepted?
+// Precondition: head[par] of this slot issued (possibly still in flight).  next_* describe
+// the warp's next active slot (nullptr if none); its head goes to head[par ^ 1].
 template <class P>
-__device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, const int2* zs, const int2* nzs,
-                                             int lane, const uint8_t* ybytes, const int32_t* win,
-                                             const int8_t* c8, const uint64_t* ct,
-                                             const int32_t* shat, uint8_t* stage_sig) {
+__device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, SlotPipe& pp, int par,
+                                             const int2* zs, const int2* nzs, int lane,
+                                             const uint8_t* ybytes, const int32_t* win,
+                                             const int8_t* next_c8, const uint8_t* next_y,
+                                             const uint64_t* ct, const int32_t* shat,
+                                             uint8_t* stage_sig) {
   using S = Sizes<P>;
   constexpr unsigned FULL = 0xffffffffu;
+  constexpr int R = P::L - 1 + P::K;  // ring chunks of a slot: y_1..y_{L-1}, w_0..w_{K-1}
+  auto ring_src = [&](int r) -> const void* {
+    return r < P::L - 1 ? static_cast<const void*>(ybytes + (r + 1) * S::Z_POLY)
+                        : static_cast<const void*>(win + (size_t)(r - (P::L - 1)) * kN);
+  };
+  auto ring_bytes = [&](int r) -> unsigned { return r < P::L - 1 ? S::Z_POLY : kN * 4; };
+
+  // ring chunk 0, then the next slot's head; then wait for everything older (our head)
+  warp_fetch(pp.ring(pp.k), ring_src(0), ring_bytes(0), lane);
+  cp_async_commit();
+  ++pp.k;
+  if (next_c8) fetch_head<P>(pp, par ^ 1, next_c8, next_y, lane);
+  cp_async_commit();
+  cp_async_wait<2>();
+  __syncwarp();
+  const uint8_t* hd = pp.head(par);
+
   int32_t ch[8], t[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) ch[e] = c8[lane + 32 * e];
+  for (int e = 0; e < 8; ++e) ch[e] = reinterpret_cast<const int8_t*>(hd)[lane + 32 * e];
   ntt_fwd(ch, ws.tile, zs, lane);
 
   // One loop over the L + 2K products c*s (one inverse-NTT instance in the instruction
@@ -212,27 +298,39 @@ __device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, const int2* zs,
   //   r0 = LowBits(w - c s2), ||r0|| < gamma2 - beta            (scheme.hpp:177-190)
   //   ||c t0|| < gamma2, h = [HB(w - c s2 + c t0) != HB(w - c s2)]   (scheme.hpp:192-215)
   unsigned weight = 0;
+  int rnext = 1;  // next ring chunk of this slot to issue
   int32_t wcs2[8], hb0[8];
 #pragma unroll 1
   for (int p = 0; p < P::L + 2 * P::K; ++p) {
     const int q = p - P::L, i = q >> 1;
-    const bool is_t0 = (q & 1) != 0;
+    const bool is_t0 = p >= P::L && (q & 1) != 0;
     const int poly = p < P::L ? p : (is_t0 ? P::L + P::K + i : P::L + i);
     mul_challenge(t, ch, shat + (size_t)poly * kN, ws.tile, nzs, lane);
     bool bad = false;
+    const uint8_t* cur = hd + kN;  // y_0 rides in the head chunk
+    if (p >= 1 && !is_t0) {
+      // consume the oldest ring chunk; keep one more in flight behind it
+      cur = pp.ring(pp.k - 1);
+      if (rnext < R) warp_fetch(pp.ring(pp.k), ring_src(rnext), ring_bytes(rnext), lane);
+      cp_async_commit();
+      ++pp.k;
+      ++rnext;
+      cp_async_wait<1>();
+      __syncwarp();
+    }
     if (p < P::L) {
-      const uint8_t* yb = ybytes + p * S::Z_POLY;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int32_t y = P::GAMMA1 - (int32_t)load_bits_rw(yb, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
+        const int32_t y = P::GAMMA1 - (int32_t)load_bits_s(cur, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
         const int32_t z = center(freeze(y + t[e]));
         bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
         ws.vhat[p][e][lane] = z;
       }
     } else if (!is_t0) {
+      const int32_t* wrow = reinterpret_cast<const int32_t*>(cur);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        wcs2[e] = freeze(win[i * kN + lane + 32 * e] - t[e]);
+        wcs2[e] = freeze(wrow[lane + 32 * e] - t[e]);
         int32_t r0;
         hb0[e] = decompose<P::GAMMA2>(wcs2[e], r0);
         bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
@@ -283,7 +381,8 @@ template <class P>
 __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent(SignArgs a) {
   using S = Sizes<P>;
   using Z = SignSizes<P>;
-  __shared__ __align__(16) SignSmem<P> sm;
+  extern __shared__ __align__(16) unsigned char sign_smem_raw[];  // dynamic: > 48 KB at levels 3/5
+  SignSmem<P>& sm = *reinterpret_cast<SignSmem<P>*>(sign_smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t cta = blockIdx.x;
   uint8_t* ybytes = a.ybytes + cta * kSignThreads * Z::Y_SLOT;
@@ -358,16 +457,32 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
     __syncthreads();
 
     // ---- S2: w, w1 ---------------------------------------------------------------
+    SlotPipe pp;
+    pp.base = &sm.u.a.pre[warp][0][0];
+    pp.k = 0;
+    auto next_active = [&](int s) {
+      s += kSignWarps;
+      while (s < kSignThreads && sm.slot_task[s] == kNoSlot) s += kSignWarps;
+      return s;
+    };
+    {
+      int s = sm.slot_task[warp] == kNoSlot ? next_active(warp) : warp;
+      if (s < kSignThreads) {  // prologue: first mask polynomial of the first slot
+        warp_fetch(pp.ring(pp.k), ybytes + (size_t)s * Z::Y_SLOT, S::Z_POLY, lane);
+        cp_async_commit();
+        ++pp.k;
+      }
 #pragma unroll 1
-    for (int s = warp; s < kSignThreads; s += kSignWarps) {
-      const unsigned task = sm.slot_task[s];
-      if (task == kNoSlot) continue;
-      const size_t key = (size_t)task * a.key_stride;
-      if (s + kSignWarps < kSignThreads)  // next slot of this warp: pull its masks into L1
-        prefetch_l1(ybytes + (size_t)(s + kSignWarps) * Z::Y_SLOT, Z::Y_SLOT, lane);
-      stage_w<P>(sm.u.ws[warp], sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
-                 a.A + key * (P::K * P::L * kN), wbuf + (size_t)s * Z::W_SLOT,
-                 w1buf + (size_t)s * S::W1_ALL);
+      while (s < kSignThreads) {
+        const int nx = next_active(s);
+        const size_t key = (size_t)sm.slot_task[s] * a.key_stride;
+        stage_w<P>(sm.u.a.ws[warp], pp, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
+                   nx < kSignThreads ? ybytes + (size_t)nx * Z::Y_SLOT : nullptr,
+                   a.A + key * (P::K * P::L * kN), wbuf + (size_t)s * Z::W_SLOT,
+                   w1buf + (size_t)s * S::W1_ALL);
+        s = nx;
+      }
+      cp_async_wait<0>();
     }
     __syncthreads();
 
@@ -396,23 +511,27 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
     __syncthreads();
 
     // ---- S4: finish --------------------------------------------------------------
-#pragma unroll 1
-    for (int s = warp; s < kSignThreads; s += kSignWarps) {
-      const unsigned task = sm.slot_task[s];
-      if (task == kNoSlot) continue;
-      const size_t key = (size_t)task * a.key_stride;
-      if (s + kSignWarps < kSignThreads) {
-        const int nx = s + kSignWarps;
-        prefetch_l1(c8buf + (size_t)nx * kN, kN, lane);
-        prefetch_l1(ybytes + (size_t)nx * Z::Y_SLOT, S::Z_POLY, lane);
-        prefetch_l1(wbuf + (size_t)nx * Z::W_SLOT, 1024, lane);
+    {
+      int s = sm.slot_task[warp] == kNoSlot ? next_active(warp) : warp;
+      int par = 0;
+      if (s < kSignThreads) {  // prologue: head chunk (c | y_0) of the first slot
+        fetch_head<P>(pp, par, c8buf + (size_t)s * kN, ybytes + (size_t)s * Z::Y_SLOT, lane);
+        cp_async_commit();
       }
-      const bool ok = stage_finish<P>(sm.u.ws[warp], sm.zs, sm.nzs, lane,
-                                      ybytes + (size_t)s * Z::Y_SLOT, wbuf + (size_t)s * Z::W_SLOT,
-                                      c8buf + (size_t)s * kN, ctbuf + s * 4,
-                                      a.shat + key * ((P::L + 2 * P::K) * kN),
-                                      staging + (size_t)s * Z::SIG_PAD);
-      if (lane == 0) sm.slot_valid[s] = ok ? 1 : 0;
+#pragma unroll 1
+      while (s < kSignThreads) {
+        const int nx = next_active(s);
+        const size_t key = (size_t)sm.slot_task[s] * a.key_stride;
+        const bool ok = stage_finish<P>(
+            sm.u.a.ws[warp], pp, par, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
+            wbuf + (size_t)s * Z::W_SLOT, nx < kSignThreads ? c8buf + (size_t)nx * kN : nullptr,
+            nx < kSignThreads ? ybytes + (size_t)nx * Z::Y_SLOT : nullptr, ctbuf + s * 4,
+            a.shat + key * ((P::L + 2 * P::K) * kN), staging + (size_t)s * Z::SIG_PAD);
+        if (lane == 0) sm.slot_valid[s] = ok ? 1 : 0;
+        s = nx;
+        par ^= 1;
+      }
+      cp_async_wait<0>();
     }
     __syncthreads();
 
@@ -551,8 +670,11 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
 
   // grid: resident CTAs of the persistent kernel
   int occ = 0;
+  const size_t smem_bytes = sizeof(SignSmem<P>);
+  DLB_CUDA_CHECK(cudaFuncSetAttribute(k_sign_persistent<P>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
   DLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sign_persistent<P>,
-                                                               kSignThreads, 0));
+                                                               kSignThreads, smem_bytes));
   if (occ < 1) occ = 1;
   const size_t grid_max = (size_t)c->sm_count * occ;
   size_t grid;
@@ -599,7 +721,7 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   a.dbg_ctilde = d_dbg_ct;
   a.q = q;
   cudaEventRecord(c->ev2, st);
-  k_sign_persistent<P><<<(unsigned)grid, kSignThreads, 0, st>>>(a);
+  k_sign_persistent<P><<<(unsigned)grid, kSignThreads, smem_bytes, st>>>(a);
   cudaEventRecord(c->ev3, st);
   c->launches += 1;
   DLB_LAUNCH_CHECK();
