@@ -91,6 +91,20 @@ __device__ __forceinline__ int32_t mont_mul(int32_t a, int32_t b) {
   return mont_fold(p, t);
 }
 
+// 64-bit multiply-accumulate and a single Montgomery fold at the end: a row of the
+// matrix-vector product costs L IMAD.WIDE + 2 instead of L full Montgomery products.
+// |acc| must stay below 2^31 q: L <= 7 terms of |a| < 2^23 times |b| < 2^27.
+__device__ __forceinline__ int64_t mac_wide(int64_t acc, int32_t a, int32_t b) {
+  int64_t r;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(acc));
+  return r;
+}
+
+__device__ __forceinline__ int32_t mont_reduce64(int64_t p) {
+  const int32_t t = (int32_t)p * (int32_t)kQInv;
+  return mont_fold(p, t);
+}
+
 // same with the constant operand's b*qinv supplied (twiddles): IMAD + 2 IMAD.WIDE
 __device__ __forceinline__ int32_t mont_mul_pre(int32_t a, int32_t b, int32_t bq) {
   const int32_t t = a * bq;

@@ -158,6 +158,11 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) {
+    DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->lane_s[b], cudaStreamNonBlocking));
+    DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join[b], cudaEventDisableTiming));
+  }
+  DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev0));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev1));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev2));
@@ -189,6 +194,11 @@ void dlb_destroy(dlb_ctx* c) {
     cudaEventDestroy(c->ev_comp[b]);
     cudaEventDestroy(c->ev_out[b]);
   }
+  for (int b = 0; b < 2; ++b) {
+    cudaStreamDestroy(c->lane_s[b]);
+    cudaEventDestroy(c->ev_join[b]);
+  }
+  cudaEventDestroy(c->ev_fork);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->copy_in);
   cudaStreamDestroy(c->copy_out);

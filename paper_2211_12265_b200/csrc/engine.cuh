@@ -35,6 +35,8 @@ struct dlb_ctx {
   cudaStream_t copy_in = nullptr;     // H2D stream
   cudaStream_t copy_out = nullptr;    // D2H stream
   cudaStream_t ext = nullptr;         // caller's stream for *_dev calls (optional)
+  cudaStream_t lane_s[2] = {};        // two compute lanes: consecutive chunks overlap
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};  // chunk pipeline hand-offs
   float last_ms = 0.f, last_main_ms = 0.f;  // whole call / dominant kernel only

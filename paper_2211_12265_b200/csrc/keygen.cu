@@ -13,33 +13,52 @@ namespace dlb {
 
 constexpr size_t kKeygenChunk = 16384;
 
+// Chunks alternate between two compute lanes so the one-thread-per-task hashes of one
+// chunk overlap the wide sampler / arithmetic kernels of the next (see verify.cu).
 template <class P>
 int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uint8_t* d_sks) {
   using S = Sizes<P>;
   constexpr int KL = P::K * P::L, PV = P::K + P::L;
   constexpr int HW = 4;
   if (n == 0) return 0;
-  cudaStream_t st = c->s();
-  const size_t chunk = n < kKeygenChunk ? n : kKeygenChunk;
-  uint64_t* seeds;
-  int8_t* s8;
-  int32_t* A;
-  DLB_TRY(dalloc(c, "g.seeds", chunk * 16, &seeds));
-  DLB_TRY(dalloc(c, "g.s8", chunk * PV * kN, &s8));
-  DLB_TRY(dalloc(c, "g.A", chunk * KL * kN, &A));
-  const uint8_t* seedb = reinterpret_cast<const uint8_t*>(seeds);
-  for (size_t lo = 0; lo < n; lo += chunk) {
+  cudaStream_t main = c->s();
+  size_t chunk = (n + 1) / 2;
+  if (chunk < 2048) chunk = 2048;
+  if (chunk > kKeygenChunk) chunk = kKeygenChunk;
+  if (chunk > n) chunk = n;
+  uint64_t* seeds[2];
+  int8_t* s8[2];
+  int32_t* A[2];
+  const char* nm[2][3] = {{"g.seeds0", "g.s80", "g.A0"}, {"g.seeds1", "g.s81", "g.A1"}};
+  for (int b = 0; b < 2; ++b) {
+    DLB_TRY(dalloc(c, nm[b][0], chunk * 16, &seeds[b]));
+    DLB_TRY(dalloc(c, nm[b][1], chunk * PV * kN, &s8[b]));
+    DLB_TRY(dalloc(c, nm[b][2], chunk * KL * kN, &A[b]));
+  }
+  DLB_CUDA_CHECK(cudaEventRecord(c->ev_fork, main));
+  DLB_CUDA_CHECK(cudaStreamWaitEvent(c->lane_s[0], c->ev_fork, 0));
+  DLB_CUDA_CHECK(cudaStreamWaitEvent(c->lane_s[1], c->ev_fork, 0));
+  size_t ci = 0;
+  for (size_t lo = 0; lo < n; lo += chunk, ++ci) {
     const size_t cnt = n - lo < chunk ? n - lo : chunk;
+    const int b = (int)(ci & 1);
+    cudaStream_t st = c->lane_s[b];
+    const uint8_t* seedb = reinterpret_cast<const uint8_t*>(seeds[b]);
     uint8_t* pks = d_pks + lo * S::PK;
     uint8_t* sks = d_sks + lo * S::SK;
-    k_keygen_seed<<<cdiv(cnt, 128), 128, 0, st>>>(d_zetas + lo * 32, (unsigned)cnt, seeds);
+    k_keygen_seed<<<cdiv(cnt, 128), 128, 0, st>>>(d_zetas + lo * 32, (unsigned)cnt, seeds[b]);
     k_expand_s<P, HW><<<cdiv(cnt * PV, HW * 32), HW * 32, 0, st>>>(seedb + 32, 128,
-                                                                    (unsigned)(cnt * PV), s8);
-    k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(seedb, 128, (unsigned)(cnt * KL), A);
-    k_keygen_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>((unsigned)cnt, seedb, s8, A, pks, sks);
+                                                                    (unsigned)(cnt * PV), s8[b]);
+    k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(seedb, 128, (unsigned)(cnt * KL),
+                                                                    A[b]);
+    k_keygen_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>((unsigned)cnt, seedb, s8[b], A[b], pks, sks);
     k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, S::PK, S::PK, (unsigned)cnt, sks + 64, S::SK);
     c->launches += 5;
     DLB_LAUNCH_CHECK();
+  }
+  for (int b = 0; b < 2; ++b) {
+    DLB_CUDA_CHECK(cudaEventRecord(c->ev_join[b], c->lane_s[b]));
+    DLB_CUDA_CHECK(cudaStreamWaitEvent(main, c->ev_join[b], 0));
   }
   return 0;
 }

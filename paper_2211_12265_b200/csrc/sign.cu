@@ -138,6 +138,7 @@ struct SignSmem {
   uint32_t keep_pos[kSignThreads];
   uint32_t warp_sums[kSignWarps];
   unsigned U, newU, got, base;
+  unsigned cursor2, cursor4;  // next unclaimed slot of stages S2 / S4 (warps pull slots)
 };
 
 // ---- asynchronous scratch prefetch ----------------------------------------------------
@@ -206,9 +207,9 @@ __device__ __forceinline__ void stage_w(WarpScratch<P>& ws, SlotPipe& pp, const 
   }
 #pragma unroll 1
   for (int i = 0; i < P::K; ++i) {
-    int32_t acc[8];
+    int64_t acc64[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) acc[m] = 0;
+    for (int m = 0; m < 8; ++m) acc64[m] = 0;
     // the cached matrix row streams through registers one polynomial ahead of its use
     const int4* ap = reinterpret_cast<const int4*>(A + (size_t)(i * P::L) * kN) + 2 * lane;
     int4 n0 = __ldg(ap), n1 = __ldg(ap + 1);
@@ -221,10 +222,11 @@ __device__ __forceinline__ void stage_w(WarpScratch<P>& ws, SlotPipe& pp, const 
       }
       const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-      for (int m = 0; m < 8; ++m) acc[m] += mont_mul(a[m], ws.vhat[j][m][lane]);
+      for (int m = 0; m < 8; ++m) acc64[m] = mac_wide(acc64[m], a[m], ws.vhat[j][m][lane]);
     }
+    int32_t acc[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) acc[m] = reduce32(acc[m]);
+    for (int m = 0; m < 8; ++m) acc[m] = mont_reduce64(acc64[m]);  // |.| < q: ready for the INTT
     ntt_inv(acc, ws.tile, nzs, lane);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -434,6 +436,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
       sm.slot_task[tid] = on ? sm.utask[u] : kNoSlot;
       sm.slot_attempt[tid] = att;
       sm.slot_valid[tid] = 0;
+      if (tid == 0) sm.cursor2 = sm.cursor4 = 0;
       const unsigned n_on = __syncthreads_count(on);
       const unsigned n_spec = __syncthreads_count(on && depth > 0);
       if (tid == 0) {
@@ -460,13 +463,20 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
     SlotPipe pp;
     pp.base = &sm.u.a.pre[warp][0][0];
     pp.k = 0;
-    auto next_active = [&](int s) {
-      s += kSignWarps;
-      while (s < kSignThreads && sm.slot_task[s] == kNoSlot) s += kSignWarps;
-      return s;
+    // Warps pull slots from a CTA-wide cursor instead of owning a fixed stripe: S4's work
+    // per slot varies with the early aborts, and a static split leaves warps waiting at
+    // the stage barrier.  Returns kSignThreads when the stage has no slot left.
+    auto grab = [&](unsigned* cursor) {
+      unsigned s = kSignThreads;
+      if (lane == 0) {
+        do s = atomicAdd(cursor, 1u);
+        while (s < (unsigned)kSignThreads && sm.slot_task[s] == kNoSlot);
+        if (s > (unsigned)kSignThreads) s = kSignThreads;
+      }
+      return (int)__shfl_sync(0xffffffffu, s, 0);
     };
     {
-      int s = sm.slot_task[warp] == kNoSlot ? next_active(warp) : warp;
+      int s = grab(&sm.cursor2);
       if (s < kSignThreads) {  // prologue: first mask polynomial of the first slot
         warp_fetch(pp.ring(pp.k), ybytes + (size_t)s * Z::Y_SLOT, S::Z_POLY, lane);
         cp_async_commit();
@@ -474,7 +484,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
       }
 #pragma unroll 1
       while (s < kSignThreads) {
-        const int nx = next_active(s);
+        const int nx = grab(&sm.cursor2);
         const size_t key = (size_t)sm.slot_task[s] * a.key_stride;
         stage_w<P>(sm.u.a.ws[warp], pp, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
                    nx < kSignThreads ? ybytes + (size_t)nx * Z::Y_SLOT : nullptr,
@@ -512,7 +522,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
 
     // ---- S4: finish --------------------------------------------------------------
     {
-      int s = sm.slot_task[warp] == kNoSlot ? next_active(warp) : warp;
+      int s = grab(&sm.cursor4);
       int par = 0;
       if (s < kSignThreads) {  // prologue: head chunk (c | y_0) of the first slot
         fetch_head<P>(pp, par, c8buf + (size_t)s * kN, ybytes + (size_t)s * Z::Y_SLOT, lane);
@@ -520,7 +530,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
       }
 #pragma unroll 1
       while (s < kSignThreads) {
-        const int nx = next_active(s);
+        const int nx = grab(&sm.cursor4);
         const size_t key = (size_t)sm.slot_task[s] * a.key_stride;
         const bool ok = stage_finish<P>(
             sm.u.a.ws[warp], pp, par, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
@@ -681,9 +691,10 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   if (psi) {
     grid = (psi + kSignThreads - 1) / kSignThreads;
   } else {
-    // default Psi: about two slots per open task while the batch is smaller than the
-    // machine, all resident slots otherwise
-    const size_t want_slots = speculate ? 2 * n : n;
+    // default Psi: about three slots per open task while the batch is smaller than the
+    // machine (measured optimum of the Psi sweep, profiles/r01_summary.md), all resident
+    // slots otherwise
+    const size_t want_slots = speculate ? 3 * n : n;
     grid = (want_slots + kSignThreads - 1) / kSignThreads;
   }
   if (grid > grid_max) grid = grid_max;

@@ -33,6 +33,10 @@ __global__ void k_verify_final(unsigned n, const uint64_t* __restrict__ mu,
 
 constexpr size_t kVerifyChunk = 16384;
 
+// Chunks alternate between two compute lanes (streams forked from / joined to the
+// caller's stream): the sponge-per-task kernels of one chunk (tr, mu, challenge, final
+// hash -- one thread per task, too few warps to fill 148 SMs on their own) overlap the
+// wide ExpandA / arithmetic kernels of the neighbouring chunk.
 template <class P>
 int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, const uint8_t* d_msgs,
                const uint64_t* d_msg_off, const uint8_t* d_sigs, uint8_t* d_flags) {
@@ -40,42 +44,68 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, con
   constexpr int KL = P::K * P::L;
   constexpr int HW = 4;  // warps per CTA for the sponge kernels
   if (n == 0) return 0;
-  cudaStream_t st = c->s();
+  cudaStream_t main = c->s();
   const bool shared_key = pk_stride == 0;
-  const size_t chunk = n < kVerifyChunk ? n : kVerifyChunk;
+  size_t chunk = (n + 1) / 2;
+  if (chunk < 2048) chunk = 2048;
+  if (chunk > kVerifyChunk) chunk = kVerifyChunk;
+  if (chunk > n) chunk = n;
   const size_t keys_cap = shared_key ? 1 : chunk;
 
-  int32_t* A;
-  uint8_t *tr, *w1buf, *pre_ok;
-  uint64_t* mu;
-  int8_t* c8;
-  DLB_TRY(dalloc(c, "v.A", keys_cap * KL * kN, &A));
-  DLB_TRY(dalloc(c, "v.tr", keys_cap * 32, &tr));
-  DLB_TRY(dalloc(c, "v.mu", chunk * 8, &mu));
-  DLB_TRY(dalloc(c, "v.c8", chunk * kN, &c8));
-  DLB_TRY(dalloc(c, "v.w1", chunk * S::W1_ALL, &w1buf));
-  DLB_TRY(dalloc(c, "v.ok", chunk, &pre_ok));
-
-  for (size_t lo = 0; lo < n; lo += chunk) {
+  int32_t* A[2];
+  uint8_t *tr[2], *w1buf[2], *pre_ok[2];
+  uint64_t* mu[2];
+  int8_t* c8[2];
+  const char* nm[2][6] = {{"v.A0", "v.tr0", "v.mu0", "v.c80", "v.w10", "v.ok0"},
+                          {"v.A1", "v.tr1", "v.mu1", "v.c81", "v.w11", "v.ok1"}};
+  for (int b = 0; b < 2; ++b) {
+    if (b == 1 && shared_key) {  // one expanded key serves both lanes
+      A[1] = A[0];
+      tr[1] = tr[0];
+    } else {
+      DLB_TRY(dalloc(c, nm[b][0], keys_cap * KL * kN, &A[b]));
+      DLB_TRY(dalloc(c, nm[b][1], keys_cap * 32, &tr[b]));
+    }
+    DLB_TRY(dalloc(c, nm[b][2], chunk * 8, &mu[b]));
+    DLB_TRY(dalloc(c, nm[b][3], chunk * kN, &c8[b]));
+    DLB_TRY(dalloc(c, nm[b][4], chunk * S::W1_ALL, &w1buf[b]));
+    DLB_TRY(dalloc(c, nm[b][5], chunk, &pre_ok[b]));
+  }
+  if (shared_key) {  // expand once on the caller's stream, before the fork
+    k_expand_a<P, HW><<<cdiv(KL, HW * 32), HW * 32, 0, main>>>(d_pks, 0, (unsigned)KL, A[0]);
+    k_hash_tr<<<1, 128, 0, main>>>(d_pks, 0, S::PK, 1u, tr[0], 32);
+    c->launches += 2;
+  }
+  DLB_CUDA_CHECK(cudaEventRecord(c->ev_fork, main));
+  DLB_CUDA_CHECK(cudaStreamWaitEvent(c->lane_s[0], c->ev_fork, 0));
+  DLB_CUDA_CHECK(cudaStreamWaitEvent(c->lane_s[1], c->ev_fork, 0));
+  size_t ci = 0;
+  for (size_t lo = 0; lo < n; lo += chunk, ++ci) {
     const size_t cnt = n - lo < chunk ? n - lo : chunk;
+    const int b = (int)(ci & 1);
+    cudaStream_t st = c->lane_s[b];
     const uint8_t* pks = d_pks + lo * pk_stride;
     const uint8_t* sigs = d_sigs + lo * S::SIG;
-    if (!shared_key || lo == 0) {
-      const size_t nk = shared_key ? 1 : cnt;
-      k_expand_a<P, HW><<<cdiv(nk * KL, HW * 32), HW * 32, 0, st>>>(pks, pk_stride, (unsigned)(nk * KL), A);
-      k_hash_tr<<<cdiv(nk, 128), 128, 0, st>>>(pks, pk_stride, S::PK, (unsigned)nk, tr, 32);
+    if (!shared_key) {
+      k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(pks, pk_stride,
+                                                                     (unsigned)(cnt * KL), A[b]);
+      k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, pk_stride, S::PK, (unsigned)cnt, tr[b], 32);
       c->launches += 2;
     }
-    k_hash_mu<<<cdiv(cnt, 128), 128, 0, st>>>(tr, shared_key ? 0 : 32, nullptr, 0, d_msgs,
-                                              d_msg_off + lo, (unsigned)cnt, mu, nullptr);
-    k_sample_in_ball<P, HW><<<cdiv(cnt, HW * 32), HW * 32, 0, st>>>(sigs, S::SIG, (unsigned)cnt, c8);
+    k_hash_mu<<<cdiv(cnt, 128), 128, 0, st>>>(tr[b], shared_key ? 0 : 32, nullptr, 0, d_msgs,
+                                              d_msg_off + lo, (unsigned)cnt, mu[b], nullptr);
+    k_sample_in_ball<P, HW><<<cdiv(cnt, HW * 32), HW * 32, 0, st>>>(sigs, S::SIG, (unsigned)cnt, c8[b]);
     k_verify_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>(
-        (unsigned)cnt, pks, pk_stride, sigs, S::SIG, A, shared_key ? 0 : (size_t)KL * kN, c8, w1buf,
-        pre_ok);
-    k_verify_final<P><<<cdiv(cnt, 128), 128, 0, st>>>((unsigned)cnt, mu, w1buf, sigs, S::SIG, pre_ok,
-                                                      d_flags + lo);
+        (unsigned)cnt, pks, pk_stride, sigs, S::SIG, A[b], shared_key ? 0 : (size_t)KL * kN, c8[b],
+        w1buf[b], pre_ok[b]);
+    k_verify_final<P><<<cdiv(cnt, 128), 128, 0, st>>>((unsigned)cnt, mu[b], w1buf[b], sigs, S::SIG,
+                                                      pre_ok[b], d_flags + lo);
     c->launches += 4;
     DLB_LAUNCH_CHECK();
+  }
+  for (int b = 0; b < 2; ++b) {
+    DLB_CUDA_CHECK(cudaEventRecord(c->ev_join[b], c->lane_s[b]));
+    DLB_CUDA_CHECK(cudaStreamWaitEvent(main, c->ev_join[b], 0));
   }
   return 0;
 }

@@ -106,19 +106,22 @@ __global__ void __launch_bounds__(WARPS * 32)
 #pragma unroll
     for (int e = 0; e < 8; ++e) r[e] = (int32_t)(load_bits(t1b, (lane + 32 * e) * 10, 10) << 13);
     ntt_fwd(r, ws.tile, zs, lane);
-    int32_t acc[8];
+    // 64-bit accumulation of A z - c t1, one Montgomery fold per coefficient.  t1hat is
+    // reduced first so |c t1| < 2^27 * 2^23 like every other term (8 terms max).
+    int64_t acc64[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) acc[m] = -mont_mul(ch[m], r[m]);
+    for (int m = 0; m < 8; ++m) acc64[m] = mac_wide(0, -ch[m], reduce32(r[m]));
 #pragma unroll 1
     for (int j = 0; j < P::L; ++j) {
       const int4* ap = reinterpret_cast<const int4*>(tA + (size_t)(i * P::L + j) * kN) + 2 * lane;
       const int4 a0 = __ldg(ap), a1 = __ldg(ap + 1);
       const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-      for (int m = 0; m < 8; ++m) acc[m] += mont_mul(a[m], ws.vhat[j][m][lane]);
+      for (int m = 0; m < 8; ++m) acc64[m] = mac_wide(acc64[m], a[m], ws.vhat[j][m][lane]);
     }
+    int32_t acc[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) acc[m] = reduce32(acc[m]);
+    for (int m = 0; m < 8; ++m) acc[m] = mont_reduce64(acc64[m]);
     ntt_inv(acc, ws.tile, nzs, lane);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -182,19 +185,20 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
 #pragma unroll 1
   for (int i = 0; i < P::K; ++i) {
-    int32_t acc[8];
+    int64_t acc64[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) acc[m] = 0;
+    for (int m = 0; m < 8; ++m) acc64[m] = 0;
 #pragma unroll 1
     for (int j = 0; j < P::L; ++j) {
       const int4* ap = reinterpret_cast<const int4*>(tA + (size_t)(i * P::L + j) * kN) + 2 * lane;
       const int4 a0 = __ldg(ap), a1 = __ldg(ap + 1);
       const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-      for (int m = 0; m < 8; ++m) acc[m] += mont_mul(a[m], ws.vhat[j][m][lane]);
+      for (int m = 0; m < 8; ++m) acc64[m] = mac_wide(acc64[m], a[m], ws.vhat[j][m][lane]);
     }
+    int32_t acc[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) acc[m] = reduce32(acc[m]);
+    for (int m = 0; m < 8; ++m) acc[m] = mont_reduce64(acc64[m]);
     ntt_inv(acc, ws.tile, nzs, lane);
     // t = A s1 + s2 canonical; Power2Round; s2, t1, t0 codecs (scheme.hpp:91-99)
     int32_t s2v[8], t0v[8];
