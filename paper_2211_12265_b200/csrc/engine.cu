@@ -282,7 +282,16 @@ int dlb_sign_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_sks, si
 
 namespace {
 
-constexpr size_t kPipeChunk = 16384;
+constexpr size_t kPipeChunkMax = 16384;
+
+// transfer/compute pipeline granularity: at least four chunks per batch so small batches
+// (the batch-10k latency case) overlap their copies too
+inline size_t pipe_chunk(size_t n) {
+  size_t c = (n + 3) / 4;
+  if (c < 2048) c = 2048;
+  if (c > kPipeChunkMax) c = kPipeChunkMax;
+  return c < n ? c : n;
+}
 
 struct OwnStream {  // host-buffer calls always run on the engine's own streams
   dlb_ctx* c;
@@ -320,7 +329,7 @@ int dlb_keygen_batch(dlb_ctx* c, int level, size_t n, const uint8_t* zetas, uint
   cudaSetDevice(c->device);
   OwnStream own(c);
   cudaStream_t S = c->stream, CO = c->copy_out;
-  const size_t chunk = n < kPipeChunk ? n : kPipeChunk;
+  const size_t chunk = pipe_chunk(n);
   uint8_t *dz, *dpk[2], *dsk[2];
   DLB_TRY(dalloc(c, "io.zeta", n * 32, &dz));
   DLB_TRY(dalloc(c, "io.pk0", chunk * ls.pk, &dpk[0]));
@@ -364,7 +373,7 @@ int dlb_verify_batch(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t
   OwnStream own(c);
   cudaStream_t S = c->stream, CI = c->copy_in;
   const size_t mbytes = msg_off[n];
-  const size_t chunk = n < kPipeChunk ? n : kPipeChunk;
+  const size_t chunk = pipe_chunk(n);
   const size_t pk_cap = pk_stride ? chunk : 1;
   uint8_t *dpk[2], *dm, *dsig[2], *dfl;
   uint64_t* doff;
