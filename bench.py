@@ -234,6 +234,87 @@ def workload_config(args):
                   "scheduler scratch through the 126 MB L2" % (args.tasks * 2420 / 1e6)}
 
 
+
+def other_level_numbers(eng, torch, dev, level, n, steps, rank):
+    """configs[2] / configs[3]: Dilithium3 / Dilithium5 keygen, sign, verify throughput with
+    inputs resident in HBM (same step shape as the headline), plus host->host batch-10k
+    latency.  Single GPU numbers (per rank); reported under ops.levels."""
+    from paper_2211_12265_b200 import LEVELS
+    from paper_2211_12265_b200.engine import SignStats
+    lib, ctx = eng.lib, eng.ctx
+    k, l, pkb, skb, sgb = LEVELS[level]
+    pk1, sk1 = eng.batch_keygen(level, np.arange(32, dtype=np.uint8))
+    msgs, off = make_inputs(n, 31337 + level + rank)
+    p = lambda t: C.c_void_p(t.data_ptr())
+    d_msgs = torch.from_numpy(msgs).to(dev)
+    d_off = torch.from_numpy(off.astype(np.int64)).to(dev)
+    d_sk = torch.from_numpy(sk1[0].copy()).to(dev)
+    d_pk_rep = torch.from_numpy(pk1[0].copy()).to(dev).unsqueeze(0).repeat(n, 1).contiguous()
+    d_sigs = torch.zeros((n, sgb), dtype=torch.uint8, device=dev)
+    d_att = torch.zeros(n, dtype=torch.int32, device=dev)
+    d_fail = torch.zeros(n, dtype=torch.uint8, device=dev)
+    d_flags = torch.zeros(n, dtype=torch.uint8, device=dev)
+    d_pks = torch.zeros((n, pkb), dtype=torch.uint8, device=dev)
+    d_sks = torch.zeros((n, skb), dtype=torch.uint8, device=dev)
+    st = SignStats()
+    fns = {
+        "sign": lambda: lib.dlb_sign_batch_dev(ctx, level, n, p(d_sk), 0, p(d_msgs), p(d_off), None, 0, 1,
+                                               p(d_sigs), p(d_att), p(d_fail), C.byref(st)),
+        "verify": lambda: lib.dlb_verify_batch_dev(ctx, level, n, p(d_pk_rep), pkb, p(d_msgs), p(d_off),
+                                                   p(d_sigs), p(d_flags)),
+        "keygen": lambda: lib.dlb_keygen_batch_dev(ctx, level, n, p(d_msgs), p(d_pks), p(d_sks)),
+    }
+    out = {}
+    for name in ("sign", "verify", "keygen"):
+        for _ in range(2):
+            assert fns[name]() == 0
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            assert fns[name]() == 0
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        wk = WORK[level]
+        if name == "sign":
+            work = st.accepted_attempt_sum / n * int_ops(wk["attempt"])
+        else:
+            work = int_ops(wk[name])
+        out[name] = {"value": n / (ms * 1e-3), "unit": "ops/s", "ms_per_step": ms, "int32_ops_per_unit": work}
+    assert bool(d_flags.all().item()) and bool((d_fail == 0).all().item())
+    out["sign"]["attempts_per_sig"] = st.accepted_attempt_sum / n
+    # host -> host batch-10k latency
+    m = 10000
+    h_m = torch.from_numpy(msgs[:m].copy()).pin_memory()
+    h_off = torch.from_numpy(off[:m + 1].astype(np.int64)).pin_memory()
+    h_sk = torch.from_numpy(sk1[0].copy()).pin_memory()
+    h_pk = torch.from_numpy(pk1[0].copy()).pin_memory()
+    h_sig = torch.zeros((m, sgb), dtype=torch.uint8).pin_memory()
+    h_fl = torch.zeros(m, dtype=torch.uint8).pin_memory()
+    u8 = lambda t: C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_uint8))
+    u64 = lambda t: C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_uint64))
+    eng.set_stream(0)
+
+    def med(fn):
+        for _ in range(2):
+            assert fn() == 0
+        xs = []
+        for _ in range(7):
+            t0 = time.perf_counter()
+            assert fn() == 0
+            xs.append((time.perf_counter() - t0) * 1e3)
+        return float(np.median(xs))
+
+    out["batch10k_latency_ms"] = {
+        "sign": med(lambda: lib.dlb_sign_batch(ctx, level, m, u8(h_sk), 0, u8(h_m), u64(h_off), None, 0, 1,
+                                               u8(h_sig), None, None, None)),
+        "verify": med(lambda: lib.dlb_verify_batch(ctx, level, m, u8(h_pk), 0, u8(h_m), u64(h_off), u8(h_sig),
+                                                   u8(h_fl))),
+    }
+    assert bool(h_fl.all().item())
+    return out
+
 # ----------------------------------------------------------------------------------------
 def run_ours(args, dist):
     import torch
@@ -401,6 +482,17 @@ def run_ours(args, dist):
 
     lat_sign, lat_ver, lat_kg = lat(sign_host), lat(verify_host), lat(keygen_host)
 
+    levels = None
+    if not args.no_levels and world == 1:
+        eng.set_stream(side.cuda_stream)
+        levels = {}
+        for lv in (3, 5):
+            r = other_level_numbers(eng, torch, dev, lv, n, max(2, K // 2), dist.rank)
+            for op in ("sign", "verify", "keygen"):
+                r[op]["roofline_frac"] = r[op]["value"] * r[op]["int32_ops_per_unit"] / 1e12 / peaks["lop3"]
+            levels[str(lv)] = r
+        eng.set_stream(0)
+
     # ---- roofline of the dominant kernel -------------------------------------------------
     wk = WORK[LEVEL]
     w_attempt = int_ops(wk["attempt"])
@@ -467,6 +559,7 @@ def run_ours(args, dist):
                            "gpu_launches": int(l_kg)},
                 "batch10k_latency_ms": {"sign": lat_sign, "verify": lat_ver, "keygen": lat_kg,
                                         "note": "host buffers in -> host buffers out, median of 11"},
+                "levels": levels,
             },
             "context": {"paper_a100_ops_per_s": PAPER_A100},
         }
@@ -516,6 +609,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tasks", type=int, default=100000, help="tasks per GPU per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-levels", action="store_true", help="skip the Dilithium3/5 extras")
     args = ap.parse_args()
     dist = Dist()
     if args.impl == "reference":

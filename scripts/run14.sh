@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+for tool in memcheck racecheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 5 python scripts/sanitize_probe.py > gpurun_out/sanitizer_$tool.log 2>&1
+  echo "== $tool rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|level . ok" gpurun_out/sanitizer_$tool.log | head -8
+done

@@ -1,0 +1,16 @@
+"""Small end-to-end pass used under compute-sanitizer (memcheck / racecheck / initcheck)."""
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+from paper_2211_12265_b200 import Engine
+eng = Engine(0)
+rng = np.random.default_rng(5)
+for level, n in ((2, 300), (3, 150), (5, 130)):
+    zetas = rng.integers(0, 256, (n, 32), dtype=np.uint8)
+    msgs = [bytes(rng.integers(0, 256, int(rng.integers(0, 300)), dtype=np.uint8)) for _ in range(n)]
+    pks, sks = eng.batch_keygen(level, zetas)
+    sigs, att, failed, st = eng.batch_sign(level, sks, msgs, return_info=True)
+    sigs2 = eng.batch_sign(level, sks[0], msgs, psi=256)
+    assert eng.batch_verify(level, pks, msgs, sigs).all()
+    assert eng.batch_verify(level, pks[0], msgs, sigs2).all()
+    print("level", level, "ok, mean attempts %.2f" % att.mean())
