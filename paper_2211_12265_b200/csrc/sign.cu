@@ -87,6 +87,8 @@ struct SignQueue {
 struct SignArgs {
   unsigned n;                 // tasks
   unsigned tcap;              // max open tasks per CTA (<= slots)
+  unsigned slots;             // attempt slots a CTA uses (<= 128): small batches are spread
+                              // over more CTAs with fewer slots each to cut round latency
   unsigned max_attempt;       // (65535 - (L-1)) / L   (scheduler.hpp:52)
   int speculate;
   int single_round;           // stage-test mode: exactly one round, then fail open tasks
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
     {
       const unsigned u = tid % U, depth = tid / U;
       const unsigned att = sm.unext[u] + depth;
-      const bool on = (depth == 0 || a.speculate) && att <= a.max_attempt;
+      const bool on = (unsigned)tid < a.slots && (depth == 0 || a.speculate) && att <= a.max_attempt;
       sm.slot_task[tid] = on ? sm.utask[u] : kNoSlot;
       sm.slot_attempt[tid] = att;
       sm.slot_valid[tid] = 0;
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
         st_rounds += 1;
         st_attempts += n_on;
         st_spec += n_spec;
-        st_idle += kSignThreads - n_on;
+        st_idle += a.slots - n_on;
       }
     }
     const unsigned my_task = sm.slot_task[tid];
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
       unsigned next = sm.unext[tid];
       int win = -1;
       unsigned ran = 0;
-      for (unsigned s = tid; s < (unsigned)kSignThreads; s += U) {
+      for (unsigned s = tid; s < a.slots; s += U) {
         if (sm.slot_task[s] == kNoSlot) break;
         ++ran;
         if (sm.slot_valid[s]) {
@@ -687,21 +689,25 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
                                                                kSignThreads, smem_bytes));
   if (occ < 1) occ = 1;
   const size_t grid_max = (size_t)c->sm_count * occ;
-  size_t grid;
-  if (psi) {
-    grid = (psi + kSignThreads - 1) / kSignThreads;
-  } else {
-    // default Psi: about three slots per open task while the batch is smaller than the
-    // machine (measured optimum of the Psi sweep, profiles/r01_summary.md), all resident
-    // slots otherwise
-    const size_t want_slots = speculate ? 3 * n : n;
-    grid = (want_slots + kSignThreads - 1) / kSignThreads;
+  // Psi = resident attempt slots (BatchConfig::psi).  Default: about three slots per open
+  // task while the batch is smaller than the machine (measured optimum of the Psi sweep,
+  // profiles/r01_summary.md), every resident slot otherwise.  A Psi below the machine's
+  // capacity is spread over as many CTAs as possible, each using fewer of its 128 slots:
+  // the warp-per-slot stages of a round then take proportionally less time.
+  size_t want_slots = psi ? psi : (speculate ? 3 * n : n);
+  if (want_slots < 1) want_slots = 1;
+  size_t slots_per = kSignThreads, grid = grid_max;
+  if (want_slots < grid_max * kSignThreads) {
+    slots_per = (want_slots + grid_max - 1) / grid_max;
+    slots_per = (slots_per + 31) / 32 * 32;
+    if (slots_per > (size_t)kSignThreads) slots_per = kSignThreads;
+    grid = (want_slots + slots_per - 1) / slots_per;
+    if (grid > grid_max) grid = grid_max;
   }
-  if (grid > grid_max) grid = grid_max;
-  if (grid < 1) grid = 1;
   size_t tcap = (n + grid - 1) / grid;
-  if (tcap > (size_t)kSignThreads) tcap = kSignThreads;
+  if (tcap > slots_per) tcap = slots_per;
   if (single_round) {
+    slots_per = kSignThreads;
     tcap = kSignThreads;
     grid = (n + kSignThreads - 1) / kSignThreads;
   }
@@ -710,6 +716,7 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   memset(&a, 0, sizeof a);
   a.n = (unsigned)n;
   a.tcap = (unsigned)tcap;
+  a.slots = (unsigned)slots_per;
   a.max_attempt = (65535u - (P::L - 1)) / P::L;
   a.speculate = single_round ? 0 : speculate;
   a.single_round = single_round;
