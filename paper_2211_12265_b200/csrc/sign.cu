@@ -28,7 +28,7 @@
 namespace dlb {
 
 #ifndef DLB_SIGN_MINB
-#define DLB_SIGN_MINB 4  // resident CTAs per SM the register budget is sized for
+#define DLB_SIGN_MINB 4  // resident CTAs per SM: 5 (96 regs) was measured slower -- it squeezes L1 to ~10 KB
 #endif
 constexpr int kSignThreads = 128;          // threads = attempt slots per CTA
 constexpr int kSignWarps = kSignThreads / 32;
@@ -121,13 +121,24 @@ struct SignSizes {
   static constexpr int SIG_PAD = (S::SIG + 15) / 16 * 16;   // staging stride
 };
 
+// per-warp scratch of the signing stages; bit-packing borrows a free cp.async ring buffer
+template <class P>
+struct SignWarpScratch {
+  int32_t tile[kTileWords];
+  int32_t vhat[P::L][8][32];
+  uint32_t hbits[P::K][8];
+};
+
+constexpr int kHeadBytes = 896;  // c (256) | y_0 (<= 640)
+constexpr int kPreBytes = 2 * kHeadBytes + 2 * kChunkBytes;
+
 template <class P>
 struct SignSmem {
   int2 zs[256], nzs[256];
   union {
     struct {
-      WarpScratch<P> ws[kSignWarps];
-      uint8_t pre[kSignWarps][4][kChunkBytes];  // cp.async landing buffers: head x2, ring x2
+      SignWarpScratch<P> ws[kSignWarps];
+      uint8_t pre[kSignWarps][kPreBytes];  // cp.async landing buffers: head x2, ring x2
     } a;
     int8_t rows[kSignThreads][kByteRowStride];
   } u;
@@ -137,10 +148,10 @@ struct SignSmem {
   uint32_t slot_attempt[kSignThreads];
   uint8_t slot_valid[kSignThreads];
   int32_t winner[kSignThreads];    // per open task: winning slot, -1 none, -2 failed
-  uint32_t keep_pos[kSignThreads];
   uint32_t warp_sums[kSignWarps];
   unsigned U, newU, got, base;
   unsigned cursor2, cursor4;  // next unclaimed slot of stages S2 / S4 (warps pull slots)
+  unsigned long long st_rounds, st_attempts, st_spec, st_idle;  // per-CTA counters
 };
 
 // ---- asynchronous scratch prefetch ----------------------------------------------------
@@ -151,11 +162,11 @@ struct SignSmem {
 // a slot (fetched while the previous slot is processed), `ring` the remaining chunks.
 
 struct SlotPipe {
-  uint8_t* base;  // 4 * kChunkBytes of shared memory: head 0, head 1, ring 0, ring 1
+  uint8_t* base;  // kPreBytes of shared memory: head 0, head 1, ring 0, ring 1
   unsigned k;     // ring chunks issued so far (buffer = k & 1), warp-uniform
-  __device__ __forceinline__ uint8_t* head(int par) const { return base + (par & 1) * kChunkBytes; }
+  __device__ __forceinline__ uint8_t* head(int par) const { return base + (par & 1) * kHeadBytes; }
   __device__ __forceinline__ uint8_t* ring(unsigned i) const {
-    return base + (2 + (i & 1)) * kChunkBytes;
+    return base + 2 * kHeadBytes + (i & 1) * kChunkBytes;
   }
 };
 
@@ -185,7 +196,7 @@ __device__ __forceinline__ uint32_t load_bits_s(const uint8_t* sbase, unsigned b
 // Precondition: ring chunk y_0 of this slot already issued; `next_y` = y bytes of the
 // warp's next active slot (nullptr if none): its y_0 is issued during the last polynomial.
 template <class P>
-__device__ __forceinline__ void stage_w(WarpScratch<P>& ws, SlotPipe& pp, const int2* zs,
+__device__ __forceinline__ void stage_w(SignWarpScratch<P>& ws, SlotPipe& pp, const int2* zs,
                                         const int2* nzs, int lane, const uint8_t* ybytes,
                                         const uint8_t* next_y, const int32_t* A, int32_t* wout,
                                         uint8_t* w1out) {
@@ -237,7 +248,8 @@ __device__ __forceinline__ void stage_w(WarpScratch<P>& ws, SlotPipe& pp, const 
       ws.tile[lane + 36 * e] = highbits<P::GAMMA2>(w);
     }
     __syncwarp();
-    pack_tile<P::W1_BITS>(ws.tile, ws.bytes, w1out + i * S::W1_POLY, lane);
+    // packing scratch = the ring buffer whose chunk was consumed last (nothing in flight there)
+    pack_tile<P::W1_BITS>(ws.tile, pp.ring(pp.k), w1out + i * S::W1_POLY, lane);
   }
 }
 
@@ -266,7 +278,7 @@ __device__ __forceinline__ void fetch_head(SlotPipe& pp, int par, const int8_t* 
 // Precondition: head[par] of this slot issued (possibly still in flight).  next_* describe
 // the warp's next active slot (nullptr if none); its head goes to head[par ^ 1].
 template <class P>
-__device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, SlotPipe& pp, int par,
+__device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp, int par,
                                              const int2* zs, const int2* nzs, int lane,
                                              const uint8_t* ybytes, const int32_t* win,
                                              const int8_t* next_c8, const uint8_t* next_y,
@@ -362,7 +374,7 @@ __device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, SlotPipe& pp, i
 #pragma unroll
     for (int e = 0; e < 8; ++e) ws.tile[lane + 36 * e] = P::GAMMA1 - ws.vhat[j][e][lane];
     __syncwarp();
-    pack_tile<P::Z_BITS>(ws.tile, ws.bytes, stage_sig + 32 + j * S::Z_POLY, lane);
+    pack_tile<P::Z_BITS>(ws.tile, pp.ring(pp.k), stage_sig + 32 + j * S::Z_POLY, lane);
   }
   uint8_t* hint = stage_sig + 32 + P::L * S::Z_POLY;
   for (int b = lane; b < S::HINT; b += 32) hint[b] = 0;
@@ -382,7 +394,8 @@ __device__ __forceinline__ bool stage_finish(WarpScratch<P>& ws, SlotPipe& pp, i
 }
 
 template <class P>
-__global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent(SignArgs a) {
+__global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 4)
+    k_sign_persistent(SignArgs a) {
   using S = Sizes<P>;
   using Z = SignSizes<P>;
   extern __shared__ __align__(16) unsigned char sign_smem_raw[];  // dynamic: > 48 KB at levels 3/5
@@ -397,8 +410,10 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
   uint8_t* staging = a.staging + cta * kSignThreads * Z::SIG_PAD;
 
   load_twiddles(sm.zs, sm.nzs);
-  if (tid == 0) sm.U = 0;
-  unsigned long long st_rounds = 0, st_attempts = 0, st_spec = 0, st_idle = 0;  // thread 0 only
+  if (tid == 0) {
+    sm.U = 0;
+    sm.st_rounds = sm.st_attempts = sm.st_spec = sm.st_idle = 0;
+  }
   __syncthreads();
 
   while (true) {
@@ -406,7 +421,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
     if (tid == 0) {
       const unsigned U = sm.U;
       unsigned got = 0, base = 0;
-      if (U < a.tcap && !(a.single_round && st_rounds > 0)) {
+      if (U < a.tcap && !(a.single_round && sm.st_rounds > 0)) {
         const unsigned want = a.tcap - U;
         if (*(volatile unsigned*)&a.q->head < a.n) {
           base = atomicAdd(&a.q->head, want);
@@ -442,10 +457,10 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
       const unsigned n_on = __syncthreads_count(on);
       const unsigned n_spec = __syncthreads_count(on && depth > 0);
       if (tid == 0) {
-        st_rounds += 1;
-        st_attempts += n_on;
-        st_spec += n_spec;
-        st_idle += a.slots - n_on;
+        sm.st_rounds += 1;
+        sm.st_attempts += n_on;
+        sm.st_spec += n_spec;
+        sm.st_idle += a.slots - n_on;
       }
     }
     const unsigned my_task = sm.slot_task[tid];
@@ -463,7 +478,7 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
 
     // ---- S2: w, w1 ---------------------------------------------------------------
     SlotPipe pp;
-    pp.base = &sm.u.a.pre[warp][0][0];
+    pp.base = &sm.u.a.pre[warp][0];
     pp.k = 0;
     // Warps pull slots from a CTA-wide cursor instead of owning a fixed stripe: S4's work
     // per slot varies with the early aborts, and a static split leaves warps waiting at
@@ -629,10 +644,10 @@ __global__ void __launch_bounds__(kSignThreads, DLB_SIGN_MINB) k_sign_persistent
     }
   }
   if (tid == 0) {
-    atomicAdd(&a.q->rounds, st_rounds);
-    atomicAdd(&a.q->attempts, st_attempts);
-    atomicAdd(&a.q->speculative, st_spec);
-    atomicAdd(&a.q->idle_slots, st_idle);
+    atomicAdd(&a.q->rounds, sm.st_rounds);
+    atomicAdd(&a.q->attempts, sm.st_attempts);
+    atomicAdd(&a.q->speculative, sm.st_spec);
+    atomicAdd(&a.q->idle_slots, sm.st_idle);
   }
 }
 
