@@ -87,7 +87,9 @@ int dlb_keygen_batch(dlb_ctx* ctx, int level, size_t n, const uint8_t* zetas, ui
  *   msgs, msg_off:  messages concatenated; task i signs msgs[msg_off[i] .. msg_off[i+1]).
  *   rho_prime_override: NULL (deterministic signing) or n*64 bytes (scheme.hpp:253-258).
  *   psi:       resident attempt slots, BatchConfig::psi (0 = engine default).
- *   speculate: BatchConfig::speculate.
+ *   speculate: BatchConfig::speculate.  0 = one attempt per open task and round; 1 = idle
+ *              slots run future nonces breadth first, at most 8 deep per round (measured
+ *              optimum); N > 1 = the same with depth cap N.  Output never depends on it.
  *   sigs:      n*sig_bytes out.  attempts (nullable): winning attempt ordinal per task
  *              (SignOutput::attempts).  failed (nullable): 1 if the nonce space was
  *              exhausted (BatchStats::failed_tasks).  stats nullable.

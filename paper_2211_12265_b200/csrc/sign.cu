@@ -21,6 +21,8 @@
 // when the queue runs dry run speculative future nonces of the CTA's open tasks,
 // breadth first, exactly the reference's pass 2.  CTAs never wait on each other, so
 // variable repetition counts cannot idle an SM while work remains.
+#include <cstdlib>
+
 #include "engine.cuh"
 #include "samplers.cuh"
 #include "verify_keygen.cuh"
@@ -91,6 +93,7 @@ struct SignArgs {
                               // over more CTAs with fewer slots each to cut round latency
   unsigned max_attempt;       // (65535 - (L-1)) / L   (scheduler.hpp:52)
   int speculate;
+  unsigned spec_depth;        // deepest speculative attempt per task and round (pass-2 cap)
   int single_round;           // stage-test mode: exactly one round, then fail open tasks
   const uint64_t* mu;         // n * 8
   const uint64_t* rho_prime;  // n * 8
@@ -129,7 +132,7 @@ struct SignWarpScratch {
   uint32_t hbits[P::K][8];
 };
 
-constexpr int kHeadBytes = 896;  // c (256) | y_0 (<= 640)
+constexpr int kHeadBytes = 256;  // the challenge c as int8
 constexpr int kPreBytes = 2 * kHeadBytes + 2 * kChunkBytes;
 
 template <class P>
@@ -185,11 +188,18 @@ __device__ __forceinline__ void warp_fetch(uint8_t* sdst, const void* gsrc, unsi
   for (unsigned o = lane * 16u; o < bytes; o += 512u) cp_async16(sdst + o, g + o);
 }
 
-// bits [bit, bit+width) of a 4-byte aligned shared-memory stream (reads one word past
-// the field: buffers are kChunkBytes long, fields end well before)
-__device__ __forceinline__ uint32_t load_bits_s(const uint8_t* sbase, unsigned bit, unsigned width) {
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(sbase) + (bit >> 5);
-  return __funnelshift_r(w[0], w[1], bit & 31) & ((1u << width) - 1);
+// Raw BITS-wide fields of coefficients lane, lane + 32, ..., lane + 224 of a packed
+// polynomial in a 4-byte aligned shared-memory buffer.  32 * BITS is a multiple of 32, so
+// the eight fields of a lane share one shift and sit BITS words apart: two loads, one
+// funnel shift and one mask per coefficient, all offsets immediate.  (Reads one word past
+// the last field: buffers are kChunkBytes long, fields end well before.)
+template <int BITS>
+__device__ __forceinline__ void unpack_strided(const uint8_t* sbase, int lane, uint32_t (&raw)[8]) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(sbase) + ((lane * BITS) >> 5);
+  const unsigned sh = (unsigned)(lane * BITS) & 31u;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    raw[e] = __funnelshift_r(w[BITS * e], w[BITS * e + 1], sh) & ((1u << BITS) - 1);
 }
 
 // S2: w = INTT(A * NTT(y)), w1 = HighBits(w) packed (scheme.hpp:141-156).
@@ -211,9 +221,12 @@ __device__ __forceinline__ void stage_w(SignWarpScratch<P>& ws, SlotPipe& pp, co
     ++pp.k;
     cp_async_wait<1>();
     __syncwarp();
+    {
+      uint32_t raw[8];
+      unpack_strided<P::Z_BITS>(cur, lane, raw);
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-      r[e] = P::GAMMA1 - (int32_t)load_bits_s(cur, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
+      for (int e = 0; e < 8; ++e) r[e] = P::GAMMA1 - (int32_t)raw[e];
+    }
     ntt_fwd(r, ws.tile, zs, lane);
 #pragma unroll
     for (int m = 0; m < 8; ++m) ws.vhat[j][m][lane] = r[m];
@@ -265,102 +278,110 @@ __device__ __forceinline__ void mul_challenge(int32_t (&out)[8], const int32_t (
   ntt_inv(out, tile, nzs, lane);
 }
 
-// issue the head chunk (c | y_0) of a slot into pp.head(par); caller commits
-template <class P>
-__device__ __forceinline__ void fetch_head(SlotPipe& pp, int par, const int8_t* c8,
-                                           const uint8_t* ybytes, int lane) {
+// issue the head chunk (the challenge c, 256 bytes) of a slot into pp.head(par); caller commits
+__device__ __forceinline__ void fetch_head(SlotPipe& pp, int par, const int8_t* c8, int lane) {
   warp_fetch(pp.head(par), c8, kN, lane);
-  warp_fetch(pp.head(par) + kN, ybytes, Sizes<P>::Z_POLY, lane);
 }
 
 // S4: everything after the challenge (scheme.hpp:165-215) + signature packing into the
 // slot's staging buffer (packing.hpp:236-254).  Warp-uniform return: accepted?
-// Precondition: head[par] of this slot issued (possibly still in flight).  next_* describe
-// the warp's next active slot (nullptr if none); its head goes to head[par ^ 1].
+//
+// The reference checks z, then r0, then ct0 / hints (scheme.hpp:167-215); accept/reject
+// does not depend on the order, so the checks run in the order that
+// rejects soonest per transform spent: the K rows of r0 = LowBits(w - c s2) first (each
+// fails with the highest probability), then the L rows of z, and only survivors of both
+// pay for c t0 and the hints.  w - c s2 overwrites w in the slot's scratch row so the hint
+// phase can pick it up again.
+//
+// Precondition: head[par] (c) of this slot issued (possibly still in flight).  next_c8 is
+// the challenge of the warp's next active slot (nullptr if none); it goes to head[par ^ 1].
 template <class P>
 __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp, int par,
                                              const int2* zs, const int2* nzs, int lane,
-                                             const uint8_t* ybytes, const int32_t* win,
-                                             const int8_t* next_c8, const uint8_t* next_y,
-                                             const uint64_t* ct, const int32_t* shat,
-                                             uint8_t* stage_sig) {
+                                             const uint8_t* ybytes, int32_t* wrows,
+                                             const int8_t* next_c8, const uint64_t* ct,
+                                             const int32_t* shat, uint8_t* stage_sig) {
   using S = Sizes<P>;
   constexpr unsigned FULL = 0xffffffffu;
-  constexpr int R = P::L - 1 + P::K;  // ring chunks of a slot: y_1..y_{L-1}, w_0..w_{K-1}
+  constexpr int R = P::K + P::L;  // ring chunks of a slot: w_0..w_{K-1}, y_0..y_{L-1}
   auto ring_src = [&](int r) -> const void* {
-    return r < P::L - 1 ? static_cast<const void*>(ybytes + (r + 1) * S::Z_POLY)
-                        : static_cast<const void*>(win + (size_t)(r - (P::L - 1)) * kN);
+    return r < P::K ? static_cast<const void*>(wrows + (size_t)r * kN)
+                    : static_cast<const void*>(ybytes + (r - P::K) * S::Z_POLY);
   };
-  auto ring_bytes = [&](int r) -> unsigned { return r < P::L - 1 ? S::Z_POLY : kN * 4; };
+  auto ring_bytes = [&](int r) -> unsigned { return r < P::K ? kN * 4 : S::Z_POLY; };
 
   // ring chunk 0, then the next slot's head; then wait for everything older (our head)
   warp_fetch(pp.ring(pp.k), ring_src(0), ring_bytes(0), lane);
   cp_async_commit();
   ++pp.k;
-  if (next_c8) fetch_head<P>(pp, par ^ 1, next_c8, next_y, lane);
+  if (next_c8) fetch_head(pp, par ^ 1, next_c8, lane);
   cp_async_commit();
   cp_async_wait<2>();
   __syncwarp();
-  const uint8_t* hd = pp.head(par);
 
   int32_t ch[8], t[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) ch[e] = reinterpret_cast<const int8_t*>(hd)[lane + 32 * e];
+  for (int e = 0; e < 8; ++e) ch[e] = reinterpret_cast<const int8_t*>(pp.head(par))[lane + 32 * e];
   ntt_fwd(ch, ws.tile, zs, lane);
 
-  // One loop over the L + 2K products c*s (one inverse-NTT instance in the instruction
-  // stream): s1_0..s1_{L-1}, then (s2_i, t0_i) row by row.  Every exit is warp-uniform.
-  //   z = y + c s1, ||z|| < gamma1 - beta                      (scheme.hpp:167-174)
+  // One loop over the K + L products c*s2_i, c*s1_j (one inverse-NTT instance in the
+  // instruction stream); iteration p consumes ring chunk p.  Every exit is warp-uniform.
   //   r0 = LowBits(w - c s2), ||r0|| < gamma2 - beta            (scheme.hpp:177-190)
-  //   ||c t0|| < gamma2, h = [HB(w - c s2 + c t0) != HB(w - c s2)]   (scheme.hpp:192-215)
-  unsigned weight = 0;
-  int rnext = 1;  // next ring chunk of this slot to issue
-  int32_t wcs2[8], hb0[8];
+  //   z = y + c s1, ||z|| < gamma1 - beta                      (scheme.hpp:167-174)
 #pragma unroll 1
-  for (int p = 0; p < P::L + 2 * P::K; ++p) {
-    const int q = p - P::L, i = q >> 1;
-    const bool is_t0 = p >= P::L && (q & 1) != 0;
-    const int poly = p < P::L ? p : (is_t0 ? P::L + P::K + i : P::L + i);
+  for (int p = 0; p < R; ++p) {
+    const int poly = p < P::K ? P::L + p : p - P::K;  // shat order: s1 (L), s2 (K), t0 (K)
     mul_challenge(t, ch, shat + (size_t)poly * kN, ws.tile, nzs, lane);
+    // consume the oldest ring chunk; keep one more in flight behind it
+    const uint8_t* cur = pp.ring(pp.k - 1);
+    if (p + 1 < R) warp_fetch(pp.ring(pp.k), ring_src(p + 1), ring_bytes(p + 1), lane);
+    cp_async_commit();
+    ++pp.k;
+    cp_async_wait<1>();
+    __syncwarp();
     bool bad = false;
-    const uint8_t* cur = hd + kN;  // y_0 rides in the head chunk
-    if (p >= 1 && !is_t0) {
-      // consume the oldest ring chunk; keep one more in flight behind it
-      cur = pp.ring(pp.k - 1);
-      if (rnext < R) warp_fetch(pp.ring(pp.k), ring_src(rnext), ring_bytes(rnext), lane);
-      cp_async_commit();
-      ++pp.k;
-      ++rnext;
-      cp_async_wait<1>();
-      __syncwarp();
-    }
-    if (p < P::L) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int32_t y = P::GAMMA1 - (int32_t)load_bits_s(cur, (lane + 32 * e) * P::Z_BITS, P::Z_BITS);
-        const int32_t z = center(freeze(y + t[e]));
-        bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
-        ws.vhat[p][e][lane] = z;
-      }
-    } else if (!is_t0) {
+    if (p < P::K) {
       const int32_t* wrow = reinterpret_cast<const int32_t*>(cur);
+      int32_t* wdst = wrows + (size_t)p * kN;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        wcs2[e] = freeze(wrow[lane + 32 * e] - t[e]);
+        const int32_t wcs2 = freeze(wrow[lane + 32 * e] - t[e]);
         int32_t r0;
-        hb0[e] = decompose<P::GAMMA2>(wcs2[e], r0);
+        decompose<P::GAMMA2>(wcs2, r0);
         bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
+        wdst[lane + 32 * e] = wcs2;  // read back by this same lane in the hint phase
       }
     } else {
+      uint32_t raw[8];
+      unpack_strided<P::Z_BITS>(cur, lane, raw);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int32_t vt = center(caddq(t[e]));
-        bad = bad || abs(vt) >= P::GAMMA2;
-        const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != hb0[e];
-        const unsigned mask = __ballot_sync(FULL, h);
-        if (lane == 0) ws.hbits[i][e] = mask;
-        weight += __popc(mask);
+        const int32_t y = P::GAMMA1 - (int32_t)raw[e];
+        const int32_t z = center(freeze(y + t[e]));
+        bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
+        ws.vhat[p - P::K][e][lane] = z;
       }
+    }
+    if (__any_sync(FULL, bad)) return false;
+  }
+
+  //   ||c t0|| < gamma2, h = [HB(w - c s2 + c t0) != HB(w - c s2)]   (scheme.hpp:192-215)
+  unsigned weight = 0;
+#pragma unroll 1
+  for (int i = 0; i < P::K; ++i) {
+    int32_t wcs2[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) wcs2[e] = wrows[(size_t)i * kN + lane + 32 * e];
+    mul_challenge(t, ch, shat + (size_t)(P::L + P::K + i) * kN, ws.tile, nzs, lane);
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int32_t vt = center(caddq(t[e]));
+      bad = bad || abs(vt) >= P::GAMMA2;
+      const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != highbits<P::GAMMA2>(wcs2[e]);
+      const unsigned mask = __ballot_sync(FULL, h);
+      if (lane == 0) ws.hbits[i][e] = mask;
+      weight += __popc(mask);
     }
     if (__any_sync(FULL, bad)) return false;
   }
@@ -449,7 +470,8 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
     {
       const unsigned u = tid % U, depth = tid / U;
       const unsigned att = sm.unext[u] + depth;
-      const bool on = (unsigned)tid < a.slots && (depth == 0 || a.speculate) && att <= a.max_attempt;
+      const bool on = (unsigned)tid < a.slots && (depth == 0 || (a.speculate && depth <= a.spec_depth)) &&
+                      att <= a.max_attempt;
       sm.slot_task[tid] = on ? sm.utask[u] : kNoSlot;
       sm.slot_attempt[tid] = att;
       sm.slot_valid[tid] = 0;
@@ -541,8 +563,8 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
     {
       int s = grab(&sm.cursor4);
       int par = 0;
-      if (s < kSignThreads) {  // prologue: head chunk (c | y_0) of the first slot
-        fetch_head<P>(pp, par, c8buf + (size_t)s * kN, ybytes + (size_t)s * Z::Y_SLOT, lane);
+      if (s < kSignThreads) {  // prologue: head chunk (c) of the first slot
+        fetch_head(pp, par, c8buf + (size_t)s * kN, lane);
         cp_async_commit();
       }
 #pragma unroll 1
@@ -552,8 +574,8 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
         const bool ok = stage_finish<P>(
             sm.u.a.ws[warp], pp, par, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
             wbuf + (size_t)s * Z::W_SLOT, nx < kSignThreads ? c8buf + (size_t)nx * kN : nullptr,
-            nx < kSignThreads ? ybytes + (size_t)nx * Z::Y_SLOT : nullptr, ctbuf + s * 4,
-            a.shat + key * ((P::L + 2 * P::K) * kN), staging + (size_t)s * Z::SIG_PAD);
+            ctbuf + s * 4, a.shat + key * ((P::L + 2 * P::K) * kN),
+            staging + (size_t)s * Z::SIG_PAD);
         if (lane == 0) sm.slot_valid[s] = ok ? 1 : 0;
         s = nx;
         par ^= 1;
@@ -697,7 +719,8 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
 
   // grid: resident CTAs of the persistent kernel
   int occ = 0;
-  const size_t smem_bytes = sizeof(SignSmem<P>);
+  size_t smem_bytes = sizeof(SignSmem<P>);
+  if (const char* e = getenv("DLB_SIGN_PAD_SMEM")) smem_bytes += (size_t)atoi(e);  // occupancy experiments
   DLB_CUDA_CHECK(cudaFuncSetAttribute(k_sign_persistent<P>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
   DLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sign_persistent<P>,
@@ -734,6 +757,12 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   a.slots = (unsigned)slots_per;
   a.max_attempt = (65535u - (P::L - 1)) / P::L;
   a.speculate = single_round ? 0 : speculate;
+  // Deepest speculative attempt a task may run in one round.  Filling every idle slot
+  // (the reference's pass 2) wastes work once few tasks remain: attempt d is only needed
+  // with probability (1-p)^d.  Measured on B200 (profiles/r02_summary.md): cap 8 gives the
+  // best batch-10k latency and batch-100k throughput; speculate > 1 sets the cap explicitly.
+  a.spec_depth = speculate > 1 ? (unsigned)speculate : 8u;
+  if (const char* e = getenv("DLB_SPEC_DEPTH")) a.spec_depth = (unsigned)atoi(e);  // experiments
   a.single_round = single_round;
   a.mu = mu_use;
   a.rho_prime = rp_use;
