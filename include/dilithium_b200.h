@@ -41,6 +41,8 @@ typedef struct dlb_sign_stats {
   uint64_t idle_slot_rounds;     /* slot-rounds that ran no attempt */
   uint64_t accepted_attempt_sum; /* sum over tasks of the winning attempt ordinal */
   uint64_t failed_tasks;         /* nonce space exhausted (scheduler.hpp:52,122-128) */
+  /* device clock (%globaltimer, ns) of the scheduler kernel: first / last CTA start and exit */
+  uint64_t t_first_start_ns, t_last_start_ns, t_first_exit_ns, t_last_exit_ns;
 } dlb_sign_stats;
 
 /* Library / device ------------------------------------------------------------------ */

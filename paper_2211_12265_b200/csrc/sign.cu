@@ -84,6 +84,7 @@ struct SignQueue {
   unsigned head;          // next unclaimed task of the batch (the device work queue)
   unsigned key_bad;       // some secret key failed the eta range check
   unsigned long long rounds, attempts, speculative, idle_slots, accepted_sum, failed;
+  unsigned long long t_first_start, t_last_start, t_first_exit, t_last_exit;  // %globaltimer, ns
 };
 
 struct SignArgs {
@@ -434,6 +435,10 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
   if (tid == 0) {
     sm.U = 0;
     sm.st_rounds = sm.st_attempts = sm.st_spec = sm.st_idle = 0;
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicMin(&a.q->t_first_start, now);
+    atomicMax(&a.q->t_last_start, now);
   }
   __syncthreads();
 
@@ -666,6 +671,10 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
     }
   }
   if (tid == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicMin(&a.q->t_first_exit, now);
+    atomicMax(&a.q->t_last_exit, now);
     atomicAdd(&a.q->rounds, sm.st_rounds);
     atomicAdd(&a.q->attempts, sm.st_attempts);
     atomicAdd(&a.q->speculative, sm.st_spec);
@@ -698,6 +707,8 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   DLB_TRY(dalloc(c, "s.rp", n * 8, &rp));
   DLB_TRY(dalloc(c, "s.q", 1, &q));
   DLB_CUDA_CHECK(cudaMemsetAsync(q, 0, sizeof(SignQueue), st));
+  DLB_CUDA_CHECK(cudaMemsetAsync(&q->t_first_start, 0xFF, 8, st));
+  DLB_CUDA_CHECK(cudaMemsetAsync(&q->t_first_exit, 0xFF, 8, st));
 
   // per-key precomputation (scheme.hpp:106-125)
   k_expand_a<P, 4><<<cdiv(nk * KL, 128), 128, 0, st>>>(d_sks, sk_stride, (unsigned)(nk * KL), A);
@@ -799,6 +810,10 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
     stats->idle_slot_rounds = hq.idle_slots;
     stats->accepted_attempt_sum = hq.accepted_sum;
     stats->failed_tasks = hq.failed;
+    stats->t_first_start_ns = hq.t_first_start;
+    stats->t_last_start_ns = hq.t_last_start;
+    stats->t_first_exit_ns = hq.t_first_exit;
+    stats->t_last_exit_ns = hq.t_last_exit;
   }
   if (hq.key_bad) return DLB_E_KEY;
   return 0;

@@ -24,7 +24,8 @@ class EngineError(RuntimeError):
 
 class SignStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("rounds", "attempts", "speculative", "idle_slot_rounds",
-                                          "accepted_attempt_sum", "failed_tasks")]
+                                          "accepted_attempt_sum", "failed_tasks", "t_first_start_ns",
+                                          "t_last_start_ns", "t_first_exit_ns", "t_last_exit_ns")]
 
 
 def lib_path():
