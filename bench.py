@@ -592,7 +592,7 @@ def run_ours(args, dist):
             traffic = t["dram_bytes_read_plus_write"]
             traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, " + t["source"] +
                             "; = scheduler scratch of ~75k in-flight attempts (>> L2), streamed with "
-                            "cp.async one polynomial ahead; 0.68 TB/s = 10% of HBM peak")
+                            "cp.async one polynomial ahead; about 0.85 TB/s = 13% of HBM peak")
     roofline = {
         "bound": "int32-alu", "kernel": "k_sign_persistent", "achieved": achieved, "peak": peak_single,
         "unit": "Tint32-op/s", "frac": achieved / peak_single,

@@ -111,6 +111,21 @@ int dlb_verify_batch(dlb_ctx* ctx, int level, size_t n, const uint8_t* pks, size
                      const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* sigs,
                      uint8_t* flags);
 
+/* Mixed-key batches --------------------------------------------------------------------
+ * batch.hpp:41-44: every SignJob carries a pointer to a caller-owned SignPrecomp and jobs
+ * may share keys arbitrarily (a signing service multiplexing tenants).  The keyed forms
+ * take the DISTINCT keys once (n_keys * sk_bytes / pk_bytes, contiguous) plus one 32-bit
+ * key index per task, so make_precomp's work (ExpandA: 80/150/280 permutations, the NTTs
+ * of s1, s2, t0; scheme.hpp:106-125) is done once per key on the device instead of once
+ * per task.  key_idx[i] >= n_keys is DLB_E_ARG.  Everything else as the plain forms. */
+int dlb_sign_batch_keyed(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t* sks, size_t n,
+                         const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+                         const uint8_t* rho_prime_override, size_t psi, int speculate,
+                         uint8_t* sigs, uint32_t* attempts, uint8_t* failed, dlb_sign_stats* stats);
+int dlb_verify_batch_keyed(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t* pks, size_t n,
+                           const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+                           const uint8_t* sigs, uint8_t* flags);
+
 /* Device-resident variants -------------------------------------------------------------
  * Same contracts with every buffer already in device memory (HBM); no copies are made.
  * Used for kernel-only timing and by callers that keep keys/messages on the GPU. */
@@ -124,6 +139,15 @@ int dlb_sign_batch_dev(dlb_ctx* ctx, int level, size_t n, const uint8_t* d_sks, 
 int dlb_verify_batch_dev(dlb_ctx* ctx, int level, size_t n, const uint8_t* d_pks,
                          size_t pk_stride, const uint8_t* d_msgs, const uint64_t* d_msg_off,
                          const uint8_t* d_sigs, uint8_t* d_flags);
+
+int dlb_sign_batch_keyed_dev(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t* d_sks, size_t n,
+                             const uint32_t* d_key_idx, const uint8_t* d_msgs,
+                             const uint64_t* d_msg_off, const uint8_t* d_rho_prime_override,
+                             size_t psi, int speculate, uint8_t* d_sigs, uint32_t* d_attempts,
+                             uint8_t* d_failed, dlb_sign_stats* stats /* host */);
+int dlb_verify_batch_keyed_dev(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t* d_pks,
+                               size_t n, const uint32_t* d_key_idx, const uint8_t* d_msgs,
+                               const uint64_t* d_msg_off, const uint8_t* d_sigs, uint8_t* d_flags);
 
 /* Stage-level entry points (device parity tests; host buffers) --------------------------
  * They run the same device functions the batch kernels use. */

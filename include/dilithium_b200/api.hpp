@@ -25,6 +25,7 @@
 #include <span>
 #include <stdexcept>
 #include <utility>
+#include <unordered_map>
 #include <vector>
 
 #include "../dilithium_b200.h"
@@ -183,13 +184,23 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
   const size_t n = jobs.size();
   std::vector<SigBytes<P>> out(n);
   if (n == 0) return out;
-  bool shared = true;
-  for (const auto& j : jobs) shared = shared && j.key == jobs[0].key;
+  // SignJob.key is a non-owning pointer and jobs may share keys (batch.hpp:41-44): collect the
+  // distinct keys once so the device precomputes each of them once, not once per task
+  std::unordered_map<const SignPrecomp<P>*, uint32_t> key_of;
+  std::vector<const SignPrecomp<P>*> keys;
+  std::vector<uint32_t> key_idx(n);
+  for (size_t i = 0; i < n; ++i) {
+    auto [it, fresh] = key_of.try_emplace(jobs[i].key, static_cast<uint32_t>(keys.size()));
+    if (fresh) keys.push_back(jobs[i].key);
+    key_idx[i] = it->second;
+  }
+  const bool shared = keys.size() == 1;
   std::vector<uint8_t> sks;
   const uint8_t* skp = jobs[0].key->sk.data();
   if (!shared) {
-    sks.resize(n * P.sk_bytes());
-    for (size_t i = 0; i < n; ++i) std::memcpy(sks.data() + i * P.sk_bytes(), jobs[i].key->sk.data(), P.sk_bytes());
+    sks.resize(keys.size() * P.sk_bytes());
+    for (size_t k = 0; k < keys.size(); ++k)
+      std::memcpy(sks.data() + k * P.sk_bytes(), keys[k]->sk.data(), P.sk_bytes());
     skp = sks.data();
   }
   std::vector<uint8_t> flat;
@@ -199,10 +210,13 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
   std::vector<uint8_t> failed(n);
   dlb_sign_stats st{};
   static_assert(sizeof(SigBytes<P>) == P.sig_bytes());
-  const int rc = dlb_sign_batch(eng.ctx(), P.level, n, skp, shared ? 0 : P.sk_bytes(), flat.data(),
-                                off.data(), rho_prime_override ? rho_prime_override->data() : nullptr,
-                                cfg.psi, cfg.speculate ? 1 : 0, out[0].data(), att.data(),
-                                failed.data(), &st);
+  const uint8_t* rp = rho_prime_override ? rho_prime_override->data() : nullptr;
+  const int rc =
+      shared ? dlb_sign_batch(eng.ctx(), P.level, n, skp, 0, flat.data(), off.data(), rp, cfg.psi,
+                              cfg.speculate ? 1 : 0, out[0].data(), att.data(), failed.data(), &st)
+             : dlb_sign_batch_keyed(eng.ctx(), P.level, keys.size(), skp, n, key_idx.data(), flat.data(),
+                                    off.data(), rp, cfg.psi, cfg.speculate ? 1 : 0, out[0].data(),
+                                    att.data(), failed.data(), &st);
   if (rc == DLB_E_KEY) throw std::invalid_argument("batch_sign: malformed secret key");
   check(rc, "dlb_sign_batch");
   if (stats) {

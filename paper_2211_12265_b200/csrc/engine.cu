@@ -241,6 +241,21 @@ int dlb_keygen_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_zetas
   return tm.finish();
 }
 
+int dlb_verify_batch_keyed_dev(dlb_ctx* c, int level, size_t n_keys, const uint8_t* d_pks, size_t n,
+                               const uint32_t* d_key_idx, const uint8_t* d_msgs,
+                               const uint64_t* d_msg_off, const uint8_t* d_sigs, uint8_t* d_flags) {
+  LevelSizes ls;
+  if (!c || (n && (!d_pks || !d_msg_off || !d_sigs || !d_flags || !d_key_idx || !n_keys))) return DLB_E_ARG;
+  if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
+  cudaSetDevice(c->device);
+  Timed tm(c);
+  DLB_TRY(with_level(level, [&](auto p) {
+    return verify_dev<decltype(p)>(c, n, d_pks, ls.pk, n_keys, d_key_idx, d_msgs, d_msg_off, d_sigs,
+                                   d_flags);
+  }));
+  return tm.finish();
+}
+
 int dlb_verify_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_pks, size_t pk_stride,
                          const uint8_t* d_msgs, const uint64_t* d_msg_off, const uint8_t* d_sigs,
                          uint8_t* d_flags) {
@@ -248,7 +263,25 @@ int dlb_verify_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_pks, 
   cudaSetDevice(c->device);
   Timed tm(c);
   DLB_TRY(with_level(level, [&](auto p) {
-    return verify_dev<decltype(p)>(c, n, d_pks, pk_stride, d_msgs, d_msg_off, d_sigs, d_flags);
+    return verify_dev<decltype(p)>(c, n, d_pks, pk_stride, 0, nullptr, d_msgs, d_msg_off, d_sigs,
+                                   d_flags);
+  }));
+  return tm.finish();
+}
+
+int dlb_sign_batch_keyed_dev(dlb_ctx* c, int level, size_t n_keys, const uint8_t* d_sks, size_t n,
+                             const uint32_t* d_key_idx, const uint8_t* d_msgs,
+                             const uint64_t* d_msg_off, const uint8_t* d_rho_prime, size_t psi,
+                             int speculate, uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed,
+                             dlb_sign_stats* stats) {
+  LevelSizes ls;
+  if (!c || (n && (!d_sks || !d_msg_off || !d_sigs || !d_key_idx || !n_keys))) return DLB_E_ARG;
+  if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
+  cudaSetDevice(c->device);
+  Timed tm(c);
+  DLB_TRY(with_level(level, [&](auto p) {
+    return sign_dev<decltype(p)>(c, n, d_sks, ls.sk, n_keys, d_key_idx, d_msgs, d_msg_off, d_rho_prime,
+                                 psi, speculate, d_sigs, d_attempts, d_failed, stats);
   }));
   return tm.finish();
 }
@@ -261,8 +294,8 @@ int dlb_sign_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_sks, si
   cudaSetDevice(c->device);
   Timed tm(c);
   DLB_TRY(with_level(level, [&](auto p) {
-    return sign_dev<decltype(p)>(c, n, d_sks, sk_stride, d_msgs, d_msg_off, d_rho_prime, psi,
-                                 speculate, d_sigs, d_attempts, d_failed, stats);
+    return sign_dev<decltype(p)>(c, n, d_sks, sk_stride, 0, nullptr, d_msgs, d_msg_off, d_rho_prime,
+                                 psi, speculate, d_sigs, d_attempts, d_failed, stats);
   }));
   return tm.finish();
 }
@@ -360,23 +393,36 @@ int dlb_keygen_batch(dlb_ctx* c, int level, size_t n, const uint8_t* zetas, uint
   return 0;
 }
 
-int dlb_verify_batch(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_stride,
-                     const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* sigs,
-                     uint8_t* flags) {
+namespace {
+
+// range check of a key-index array (host side: an out-of-range index would read past the table)
+bool key_idx_ok(const uint32_t* key_idx, size_t n, size_t n_keys) {
+  for (size_t i = 0; i < n; ++i)
+    if (key_idx[i] >= n_keys) return false;
+  return true;
+}
+
+int verify_host(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_stride, size_t n_keys,
+                const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+                const uint8_t* sigs, uint8_t* flags) {
   LevelSizes ls;
   if (!c) return DLB_E_ARG;
   if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
   if (n == 0) return 0;
   if (!pks || !msg_off || !sigs || !flags) return DLB_E_ARG;
   if (pk_stride != 0 && pk_stride != ls.pk) return DLB_E_ARG;
+  if (key_idx && (n_keys == 0 || pk_stride == 0 || !key_idx_ok(key_idx, n, n_keys))) return DLB_E_ARG;
   cudaSetDevice(c->device);
   OwnStream own(c);
   cudaStream_t S = c->stream, CI = c->copy_in;
   const size_t mbytes = msg_off[n];
   const size_t chunk = pipe_chunk(n);
-  const size_t pk_cap = pk_stride ? chunk : 1;
+  const bool keyed = key_idx != nullptr;
+  const size_t pk_cap = keyed ? n_keys : (pk_stride ? chunk : 1);
   uint8_t *dpk[2], *dm, *dsig[2], *dfl;
   uint64_t* doff;
+  uint32_t* dkidx = nullptr;
+  if (keyed) DLB_TRY(dalloc(c, "io.kidx", n, &dkidx));
   DLB_TRY(dalloc(c, "io.pk0", pk_cap * ls.pk, &dpk[0]));
   DLB_TRY(dalloc(c, "io.pk1", pk_cap * ls.pk, &dpk[1]));
   DLB_TRY(dalloc(c, "io.msg", mbytes + 8, &dm));
@@ -388,20 +434,25 @@ int dlb_verify_batch(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t
   DLB_CU(cudaEventRecord(c->ev0, S));
   if (mbytes) DLB_CU(cudaMemcpyAsync(dm, msgs, mbytes, cudaMemcpyHostToDevice, CI));
   DLB_CU(cudaMemcpyAsync(doff, msg_off, (n + 1) * 8, cudaMemcpyHostToDevice, CI));
-  if (!pk_stride) DLB_CU(cudaMemcpyAsync(dpk[0], pks, ls.pk, cudaMemcpyHostToDevice, CI));
+  if (keyed) {
+    DLB_CU(cudaMemcpyAsync(dpk[0], pks, n_keys * ls.pk, cudaMemcpyHostToDevice, CI));
+    DLB_CU(cudaMemcpyAsync(dkidx, key_idx, n * 4, cudaMemcpyHostToDevice, CI));
+  } else if (!pk_stride) {
+    DLB_CU(cudaMemcpyAsync(dpk[0], pks, ls.pk, cudaMemcpyHostToDevice, CI));
+  }
   size_t ci = 0;
   for (size_t lo = 0; lo < n; lo += chunk, ++ci) {
     const size_t cnt = n - lo < chunk ? n - lo : chunk;
     const int b = (int)(ci & 1);
     if (ci >= 2) DLB_CU(cudaStreamWaitEvent(CI, c->ev_comp[b], 0));  // arena b consumed
     DLB_CU(cudaMemcpyAsync(dsig[b], sigs + lo * ls.sig, cnt * ls.sig, cudaMemcpyHostToDevice, CI));
-    if (pk_stride)
+    if (pk_stride && !keyed)
       DLB_CU(cudaMemcpyAsync(dpk[b], pks + lo * ls.pk, cnt * ls.pk, cudaMemcpyHostToDevice, CI));
     DLB_CU(cudaEventRecord(c->ev_in[b], CI));
     DLB_CU(cudaStreamWaitEvent(S, c->ev_in[b], 0));
     DLB_TRY(with_level(level, [&](auto p) {
-      return verify_dev<decltype(p)>(c, cnt, pk_stride ? dpk[b] : dpk[0], pk_stride, dm, doff + lo,
-                                     dsig[b], dfl + lo);
+      return verify_dev<decltype(p)>(c, cnt, (pk_stride && !keyed) ? dpk[b] : dpk[0], pk_stride, n_keys,
+                                     keyed ? dkidx + lo : nullptr, dm, doff + lo, dsig[b], dfl + lo);
     }));
     DLB_CU(cudaEventRecord(c->ev_comp[b], S));
   }
@@ -412,10 +463,29 @@ int dlb_verify_batch(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t
   return 0;
 }
 
-int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride,
-                   const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* rho_prime,
-                   size_t psi, int speculate, uint8_t* sigs, uint32_t* attempts, uint8_t* failed,
-                   dlb_sign_stats* stats) {
+}  // namespace
+
+int dlb_verify_batch(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_stride,
+                     const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* sigs,
+                     uint8_t* flags) {
+  return verify_host(c, level, n, pks, pk_stride, 0, nullptr, msgs, msg_off, sigs, flags);
+}
+
+int dlb_verify_batch_keyed(dlb_ctx* c, int level, size_t n_keys, const uint8_t* pks, size_t n,
+                           const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+                           const uint8_t* sigs, uint8_t* flags) {
+  LevelSizes ls;
+  if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
+  if (n && !key_idx) return DLB_E_ARG;
+  return verify_host(c, level, n, pks, ls.pk, n_keys, key_idx, msgs, msg_off, sigs, flags);
+}
+
+namespace {
+
+int sign_host(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride, size_t n_keys,
+              const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+              const uint8_t* rho_prime, size_t psi, int speculate, uint8_t* sigs, uint32_t* attempts,
+              uint8_t* failed, dlb_sign_stats* stats) {
   LevelSizes ls;
   if (!c) return DLB_E_ARG;
   if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
@@ -423,14 +493,16 @@ int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t s
   if (n == 0) return 0;
   if (!sks || !msg_off || !sigs) return DLB_E_ARG;
   if (sk_stride != 0 && sk_stride != ls.sk) return DLB_E_ARG;
+  if (key_idx && (n_keys == 0 || sk_stride == 0 || !key_idx_ok(key_idx, n, n_keys))) return DLB_E_ARG;
   cudaSetDevice(c->device);
   OwnStream own(c);
   cudaStream_t S = c->stream;
   const size_t mbytes = msg_off[n];
-  const size_t nk = sk_stride ? n : 1;
+  const size_t nk = key_idx ? n_keys : (sk_stride ? n : 1);
   uint8_t *dsk, *dm, *dsig, *dfail, *drp = nullptr;
   uint64_t* doff;
-  uint32_t* datt;
+  uint32_t *datt, *dkidx = nullptr;
+  if (key_idx) DLB_TRY(dalloc(c, "io.kidx", n, &dkidx));
   uint8_t* zero_copy = static_cast<uint8_t*>(pinned_alias(sigs));  // pinned: write in place
   DLB_TRY(dalloc(c, "io.sk", nk * ls.sk, &dsk));
   DLB_TRY(dalloc(c, "io.msg", mbytes + 8, &dm));
@@ -442,6 +514,7 @@ int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t s
   DLB_CU(cudaMemcpyAsync(dsk, sks, nk * ls.sk, cudaMemcpyHostToDevice, S));
   if (mbytes) DLB_CU(cudaMemcpyAsync(dm, msgs, mbytes, cudaMemcpyHostToDevice, S));
   DLB_CU(cudaMemcpyAsync(doff, msg_off, (n + 1) * 8, cudaMemcpyHostToDevice, S));
+  if (key_idx) DLB_CU(cudaMemcpyAsync(dkidx, key_idx, n * 4, cudaMemcpyHostToDevice, S));
   if (rho_prime) {
     DLB_TRY(dalloc(c, "io.rp", n * 64, &drp));
     DLB_CU(cudaMemcpyAsync(drp, rho_prime, n * 64, cudaMemcpyHostToDevice, S));
@@ -449,8 +522,8 @@ int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t s
   c->launches = 0;
   DLB_CU(cudaEventRecord(c->ev0, S));
   const int rc = with_level(level, [&](auto p) {
-    return sign_dev<decltype(p)>(c, n, dsk, sk_stride, dm, doff, drp, psi, speculate, dsig, datt,
-                                 dfail, stats);
+    return sign_dev<decltype(p)>(c, n, dsk, sk_stride, n_keys, dkidx, dm, doff, drp, psi, speculate,
+                                 dsig, datt, dfail, stats);
   });
   DLB_CU(cudaEventRecord(c->ev1, S));
   if (rc != 0) {
@@ -463,6 +536,27 @@ int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t s
   DLB_CU(cudaStreamSynchronize(S));
   cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
   return 0;
+}
+
+}  // namespace
+
+int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride,
+                   const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* rho_prime,
+                   size_t psi, int speculate, uint8_t* sigs, uint32_t* attempts, uint8_t* failed,
+                   dlb_sign_stats* stats) {
+  return sign_host(c, level, n, sks, sk_stride, 0, nullptr, msgs, msg_off, rho_prime, psi, speculate,
+                   sigs, attempts, failed, stats);
+}
+
+int dlb_sign_batch_keyed(dlb_ctx* c, int level, size_t n_keys, const uint8_t* sks, size_t n,
+                         const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+                         const uint8_t* rho_prime, size_t psi, int speculate, uint8_t* sigs,
+                         uint32_t* attempts, uint8_t* failed, dlb_sign_stats* stats) {
+  LevelSizes ls;
+  if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
+  if (n && !key_idx) return DLB_E_ARG;
+  return sign_host(c, level, n, sks, ls.sk, n_keys, key_idx, msgs, msg_off, rho_prime, psi, speculate,
+                   sigs, attempts, failed, stats);
 }
 
 // ---- stage-level entry points -----------------------------------------------------------

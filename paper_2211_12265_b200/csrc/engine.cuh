@@ -119,12 +119,16 @@ inline unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 // per-level device-resident implementations (keygen.cu / verify.cu / sign.cu)
 template <class P>
 int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uint8_t* d_sks);
+// d_key_idx == nullptr: stride 0 = one shared key, else task t uses key t; d_key_idx != nullptr:
+// a table of n_keys keys (stride apart), task t uses key d_key_idx[t].
 template <class P>
-int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, const uint8_t* d_msgs,
-               const uint64_t* d_msg_off, const uint8_t* d_sigs, uint8_t* d_flags);
+int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, size_t n_keys,
+               const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
+               const uint8_t* d_sigs, uint8_t* d_flags);
 template <class P>
-int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, const uint8_t* d_msgs,
-             const uint64_t* d_msg_off, const uint8_t* d_rho_prime, size_t psi, int speculate,
-             uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats);
+int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, size_t n_keys,
+             const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
+             const uint8_t* d_rho_prime, size_t psi, int speculate, uint8_t* d_sigs,
+             uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats);
 
 }  // namespace dlb

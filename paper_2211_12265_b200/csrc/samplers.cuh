@@ -301,10 +301,11 @@ static __global__ void k_hash_tr(const uint8_t* __restrict__ pk, size_t pk_strid
 }
 
 // mu = SHAKE256(tr || M, 64) and optionally rho' = SHAKE256(K || mu, 64)
-// (scheme.hpp:240-248).  tr (32 B) and K (32 B) per key, 8-byte aligned;
-// key index of task t = key_stride_sel ? t : 0.
+// (scheme.hpp:240-248).  tr (32 B) and K (32 B) per key, 8-byte aligned; task t uses key
+// key_idx[t] (key_idx == nullptr: key t), strides 0 = one shared key.
 static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_stride,
                           const uint8_t* __restrict__ key_base, size_t key_stride,
+                          const uint32_t* __restrict__ key_idx,
                           const uint8_t* __restrict__ msgs, const uint64_t* __restrict__ msg_off,
                           unsigned n, uint64_t* __restrict__ mu_out,
                           uint64_t* __restrict__ rho_prime_out) {
@@ -312,7 +313,8 @@ static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_
   if (t >= n) return;
   uint64_t s[25];
   uint64_t pre[4];
-  const uint64_t* tr = reinterpret_cast<const uint64_t*>(tr_base + (size_t)t * tr_stride);
+  const size_t kt = key_idx ? (size_t)__ldg(key_idx + t) : (size_t)t;
+  const uint64_t* tr = reinterpret_cast<const uint64_t*>(tr_base + kt * tr_stride);
 #pragma unroll
   for (int w = 0; w < 4; ++w) pre[w] = __ldg(tr + w);
   const uint64_t m0 = msg_off[t], m1 = msg_off[t + 1];
@@ -324,7 +326,7 @@ static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_
     mu_out[(size_t)t * 8 + w] = s[w];
   }
   if (rho_prime_out != nullptr) {
-    const uint64_t* key = reinterpret_cast<const uint64_t*>(key_base + (size_t)t * key_stride);
+    const uint64_t* key = reinterpret_cast<const uint64_t*>(key_base + kt * key_stride);
     keccak_clear(s);
 #pragma unroll
     for (int w = 0; w < 4; ++w) s[w] = __ldg(key + w);

@@ -101,7 +101,8 @@ struct SignArgs {
   const uint32_t* kappa0;     // nullable: first nonce per task (stage tests)
   const int32_t* A;           // keys * K*L*256
   const int32_t* shat;        // keys * (L+2K)*256
-  unsigned key_stride;        // 0 shared key, 1 per-task keys
+  unsigned key_stride;        // 0 shared key, 1 per-task keys (when key_idx == nullptr)
+  const uint32_t* key_idx;    // nullable: key table index of each task
   // per-CTA scratch in HBM/L2, indexed [cta][slot]
   uint8_t* ybytes;
   int32_t* wbuf;
@@ -529,7 +530,8 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
 #pragma unroll 1
       while (s < kSignThreads) {
         const int nx = grab(&sm.cursor2);
-        const size_t key = (size_t)sm.slot_task[s] * a.key_stride;
+        const size_t key = a.key_idx ? (size_t)__ldg(a.key_idx + sm.slot_task[s])
+                                     : (size_t)sm.slot_task[s] * a.key_stride;
         stage_w<P>(sm.u.a.ws[warp], pp, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
                    nx < kSignThreads ? ybytes + (size_t)nx * Z::Y_SLOT : nullptr,
                    a.A + key * (P::K * P::L * kN), wbuf + (size_t)s * Z::W_SLOT,
@@ -575,7 +577,8 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
 #pragma unroll 1
       while (s < kSignThreads) {
         const int nx = grab(&sm.cursor4);
-        const size_t key = (size_t)sm.slot_task[s] * a.key_stride;
+        const size_t key = a.key_idx ? (size_t)__ldg(a.key_idx + sm.slot_task[s])
+                                     : (size_t)sm.slot_task[s] * a.key_stride;
         const bool ok = stage_finish<P>(
             sm.u.a.ws[warp], pp, par, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
             wbuf + (size_t)s * Z::W_SLOT, nx < kSignThreads ? c8buf + (size_t)nx * kN : nullptr,
@@ -685,8 +688,8 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
 // ---- host side ---------------------------------------------------------------------
 
 template <class P>
-static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride,
-                     const uint8_t* d_msgs, const uint64_t* d_msg_off, const uint64_t* d_mu_in,
+static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, size_t n_keys,
+                     const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off, const uint64_t* d_mu_in,
                      const uint8_t* d_rho_prime, const uint32_t* d_kappa0, size_t psi,
                      int speculate, int single_round, uint8_t* d_sigs, uint32_t* d_attempts,
                      uint8_t* d_failed, uint8_t* d_dbg_ct, dlb_sign_stats* stats) {
@@ -696,7 +699,9 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   if (n == 0) return 0;
   if (n > 0x7fffffffu) return DLB_E_ARG;
   cudaStream_t st = c->s();
-  const size_t nk = sk_stride ? n : 1;
+  if (d_key_idx && (n_keys == 0 || sk_stride == 0)) return DLB_E_ARG;
+  // distinct keys to precompute: the key table, one key per task, or one shared key
+  const size_t nk = d_key_idx ? n_keys : (sk_stride ? n : 1);
 
   int32_t *A, *shat;
   uint64_t *mu, *rp;
@@ -722,8 +727,9 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
     mu_use = d_mu_in;  // stage tests supply mu and rho' directly
     rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
   } else {
-    k_hash_mu<<<cdiv(n, 128), 128, 0, st>>>(d_sks + 64, sk_stride, d_sks + 32, sk_stride, d_msgs,
-                                            d_msg_off, (unsigned)n, mu, d_rho_prime ? nullptr : rp);
+    k_hash_mu<<<cdiv(n, 128), 128, 0, st>>>(d_sks + 64, sk_stride, d_sks + 32, sk_stride, d_key_idx,
+                                            d_msgs, d_msg_off, (unsigned)n, mu,
+                                            d_rho_prime ? nullptr : rp);
     c->launches += 1;
     if (d_rho_prime) rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
   }
@@ -781,6 +787,7 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   a.A = A;
   a.shat = shat;
   a.key_stride = sk_stride ? 1u : 0u;
+  a.key_idx = d_key_idx;
   const size_t slots = grid * kSignThreads;
   DLB_TRY(dalloc(c, "s.y", slots * Z::Y_SLOT + 16, &a.ybytes));
   DLB_TRY(dalloc(c, "s.w", slots * Z::W_SLOT, &a.wbuf));
@@ -820,17 +827,20 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
 }
 
 template <class P>
-int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, const uint8_t* d_msgs,
-             const uint64_t* d_msg_off, const uint8_t* d_rho_prime, size_t psi, int speculate,
-             uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats) {
-  return sign_core<P>(c, n, d_sks, sk_stride, d_msgs, d_msg_off, nullptr, d_rho_prime, nullptr, psi,
-                      speculate, 0, d_sigs, d_attempts, d_failed, nullptr, stats);
+int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, size_t n_keys,
+             const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
+             const uint8_t* d_rho_prime, size_t psi, int speculate, uint8_t* d_sigs,
+             uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats) {
+  return sign_core<P>(c, n, d_sks, sk_stride, n_keys, d_key_idx, d_msgs, d_msg_off, nullptr,
+                      d_rho_prime, nullptr, psi, speculate, 0, d_sigs, d_attempts, d_failed, nullptr,
+                      stats);
 }
 
 #define DLB_INST(LV)                                                                            \
-  template int sign_dev<Params<LV>>(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*,   \
-                                    const uint64_t*, const uint8_t*, size_t, int, uint8_t*,     \
-                                    uint32_t*, uint8_t*, dlb_sign_stats*);
+  template int sign_dev<Params<LV>>(dlb_ctx*, size_t, const uint8_t*, size_t, size_t,           \
+                                    const uint32_t*, const uint8_t*, const uint64_t*,           \
+                                    const uint8_t*, size_t, int, uint8_t*, uint32_t*, uint8_t*, \
+                                    dlb_sign_stats*);
 DLB_INST(2)
 DLB_INST(3)
 DLB_INST(5)
@@ -869,8 +879,8 @@ extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8
     DLB_CUDA_CHECK(cudaMemcpyAsync(drp, rho_primes, n * 64, cudaMemcpyHostToDevice, st));
     DLB_CUDA_CHECK(cudaMemcpyAsync(dk, kappas, n * 4, cudaMemcpyHostToDevice, st));
     DLB_CUDA_CHECK(cudaMemsetAsync(dsig, 0, n * S::SIG, st));
-    DLB_TRY(sign_core<P>(c, n, dsk, sk_stride, nullptr, nullptr, dmu, drp, dk, 0, 0, 1, dsig, datt,
-                         dfail, dct, nullptr));
+    DLB_TRY(sign_core<P>(c, n, dsk, sk_stride, 0, nullptr, nullptr, nullptr, dmu, drp, dk, 0, 0, 1,
+                         dsig, datt, dfail, dct, nullptr));
     uint8_t* hsig = new uint8_t[n * S::SIG];
     uint8_t* hfail = new uint8_t[n];
     cudaMemcpyAsync(hsig, dsig, n * S::SIG, cudaMemcpyDeviceToHost, st);

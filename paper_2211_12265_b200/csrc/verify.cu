@@ -37,20 +37,29 @@ constexpr size_t kVerifyChunk = 16384;
 // caller's stream): the sponge-per-task kernels of one chunk (tr, mu, challenge, final
 // hash -- one thread per task, too few warps to fill 148 SMs on their own) overlap the
 // wide ExpandA / arithmetic kernels of the neighbouring chunk.
+//
+// Keys: pk_stride == 0 -> one public key for the whole batch; d_key_idx != nullptr -> a
+// table of n_keys public keys (pk_stride apart) and task t verifies under key
+// d_key_idx[t] (every distinct key is expanded once, before the chunks); otherwise task
+// t uses the key at d_pks + t * pk_stride and keys are expanded chunk by chunk.
 template <class P>
-int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, const uint8_t* d_msgs,
-               const uint64_t* d_msg_off, const uint8_t* d_sigs, uint8_t* d_flags) {
+int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, size_t n_keys,
+               const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
+               const uint8_t* d_sigs, uint8_t* d_flags) {
   using S = Sizes<P>;
   constexpr int KL = P::K * P::L;
   constexpr int HW = 4;  // warps per CTA for the sponge kernels
   if (n == 0) return 0;
   cudaStream_t main = c->s();
-  const bool shared_key = pk_stride == 0;
+  const bool keyed = d_key_idx != nullptr;
+  if (keyed && (n_keys == 0 || pk_stride == 0)) return DLB_E_ARG;
+  const bool shared_key = pk_stride == 0 || keyed;  // keys expanded once, before the fork
+  if (!keyed) n_keys = 1;
   size_t chunk = (n + 1) / 2;
   if (chunk < 2048) chunk = 2048;
   if (chunk > kVerifyChunk) chunk = kVerifyChunk;
   if (chunk > n) chunk = n;
-  const size_t keys_cap = shared_key ? 1 : chunk;
+  const size_t keys_cap = shared_key ? n_keys : chunk;
 
   int32_t* A[2];
   uint8_t *tr[2], *w1buf[2], *pre_ok[2];
@@ -72,8 +81,9 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, con
     DLB_TRY(dalloc(c, nm[b][5], chunk, &pre_ok[b]));
   }
   if (shared_key) {  // expand once on the caller's stream, before the fork
-    k_expand_a<P, HW><<<cdiv(KL, HW * 32), HW * 32, 0, main>>>(d_pks, 0, (unsigned)KL, A[0]);
-    k_hash_tr<<<1, 128, 0, main>>>(d_pks, 0, S::PK, 1u, tr[0], 32);
+    k_expand_a<P, HW><<<cdiv(n_keys * KL, HW * 32), HW * 32, 0, main>>>(d_pks, pk_stride,
+                                                                        (unsigned)(n_keys * KL), A[0]);
+    k_hash_tr<<<cdiv(n_keys, 128), 128, 0, main>>>(d_pks, pk_stride, S::PK, (unsigned)n_keys, tr[0], 32);
     c->launches += 2;
   }
   DLB_CUDA_CHECK(cudaEventRecord(c->ev_fork, main));
@@ -84,7 +94,9 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, con
     const size_t cnt = n - lo < chunk ? n - lo : chunk;
     const int b = (int)(ci & 1);
     cudaStream_t st = c->lane_s[b];
-    const uint8_t* pks = d_pks + lo * pk_stride;
+    const uint8_t* pks = keyed ? d_pks : d_pks + lo * pk_stride;
+    const uint32_t* kidx = keyed ? d_key_idx + lo : nullptr;
+    const size_t key_step = keyed ? 1 : (shared_key ? 0 : 1);  // 0: every task uses key 0
     const uint8_t* sigs = d_sigs + lo * S::SIG;
     if (!shared_key) {
       k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(pks, pk_stride,
@@ -92,11 +104,11 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, con
       k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, pk_stride, S::PK, (unsigned)cnt, tr[b], 32);
       c->launches += 2;
     }
-    k_hash_mu<<<cdiv(cnt, 128), 128, 0, st>>>(tr[b], shared_key ? 0 : 32, nullptr, 0, d_msgs,
+    k_hash_mu<<<cdiv(cnt, 128), 128, 0, st>>>(tr[b], key_step * 32, nullptr, 0, kidx, d_msgs,
                                               d_msg_off + lo, (unsigned)cnt, mu[b], nullptr);
     k_sample_in_ball<P, HW><<<cdiv(cnt, HW * 32), HW * 32, 0, st>>>(sigs, S::SIG, (unsigned)cnt, c8[b]);
     k_verify_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>(
-        (unsigned)cnt, pks, pk_stride, sigs, S::SIG, A[b], shared_key ? 0 : (size_t)KL * kN, c8[b],
+        (unsigned)cnt, pks, pk_stride, sigs, S::SIG, A[b], key_step * (size_t)KL * kN, kidx, c8[b],
         w1buf[b], pre_ok[b]);
     k_verify_final<P><<<cdiv(cnt, 128), 128, 0, st>>>((unsigned)cnt, mu[b], w1buf[b], sigs, S::SIG,
                                                       pre_ok[b], d_flags + lo);
@@ -110,11 +122,13 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, con
   return 0;
 }
 
-template int verify_dev<Params<2>>(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*,
-                                   const uint64_t*, const uint8_t*, uint8_t*);
-template int verify_dev<Params<3>>(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*,
-                                   const uint64_t*, const uint8_t*, uint8_t*);
-template int verify_dev<Params<5>>(dlb_ctx*, size_t, const uint8_t*, size_t, const uint8_t*,
-                                   const uint64_t*, const uint8_t*, uint8_t*);
+#define DLB_INST(LV)                                                                          \
+  template int verify_dev<Params<LV>>(dlb_ctx*, size_t, const uint8_t*, size_t, size_t,       \
+                                      const uint32_t*, const uint8_t*, const uint64_t*,       \
+                                      const uint8_t*, uint8_t*);
+DLB_INST(2)
+DLB_INST(3)
+DLB_INST(5)
+#undef DLB_INST
 
 }  // namespace dlb

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     k_verify_arith(unsigned n, const uint8_t* __restrict__ pk, size_t pk_stride,
                    const uint8_t* __restrict__ sig, size_t sig_stride,
                    const int32_t* __restrict__ A, size_t a_stride /* int32 per key, 0 shared */,
+                   const uint32_t* __restrict__ key_idx /* nullable: key of task t, else t */,
                    const int8_t* __restrict__ c8, uint8_t* __restrict__ w1buf,
                    uint8_t* __restrict__ pre_ok) {
   using S = Sizes<P>;
@@ -38,9 +39,10 @@ __global__ void __launch_bounds__(WARPS * 32)
   const unsigned t = blockIdx.x * WARPS + warp;
   if (t >= n) return;
   WarpScratch<P>& ws = scratch[warp];
-  const uint8_t* tpk = pk + (size_t)t * pk_stride;
+  const size_t kt = key_idx ? (size_t)__ldg(key_idx + t) : (size_t)t;
+  const uint8_t* tpk = pk + kt * pk_stride;
   const uint8_t* tsig = sig + (size_t)t * sig_stride;
-  const int32_t* tA = A + (size_t)t * a_stride;
+  const int32_t* tA = A + kt * a_stride;
   bool ok = true;
 
   // -- strict hint decode into a bitmap (packing.hpp:122-140)

@@ -64,6 +64,12 @@ def load_library():
         "dlb_sign_batch": (C.c_int, [vp, C.c_int, sz, _u8p, sz, _u8p, _u64p, _u8p, sz, C.c_int,
                                      _u8p, _u32p, _u8p, C.POINTER(SignStats)]),
         "dlb_verify_batch": (C.c_int, [vp, C.c_int, sz, _u8p, sz, _u8p, _u64p, _u8p, _u8p]),
+        "dlb_sign_batch_keyed": (C.c_int, [vp, C.c_int, sz, _u8p, sz, _u32p, _u8p, _u64p, _u8p, sz, C.c_int,
+                                           _u8p, _u32p, _u8p, C.POINTER(SignStats)]),
+        "dlb_verify_batch_keyed": (C.c_int, [vp, C.c_int, sz, _u8p, sz, _u32p, _u8p, _u64p, _u8p, _u8p]),
+        "dlb_sign_batch_keyed_dev": (C.c_int, [vp, C.c_int, sz, vp, sz, vp, vp, vp, vp, sz, C.c_int, vp,
+                                               vp, vp, C.POINTER(SignStats)]),
+        "dlb_verify_batch_keyed_dev": (C.c_int, [vp, C.c_int, sz, vp, sz, vp, vp, vp, vp, vp]),
         "dlb_keygen_batch_dev": (C.c_int, [vp, C.c_int, sz, vp, vp, vp]),
         "dlb_sign_batch_dev": (C.c_int, [vp, C.c_int, sz, vp, sz, vp, vp, vp, sz, C.c_int, vp, vp,
                                          vp, C.POINTER(SignStats)]),
@@ -88,6 +94,7 @@ def load_library():
 EXPORTED_SYMBOLS = [
     "dlb_create", "dlb_destroy", "dlb_version", "dlb_last_kernel_ms", "dlb_last_main_kernel_ms", "dlb_last_launches",
     "dlb_set_stream", "dlb_measure_int32_peak", "dlb_measure_imad_hi_peak", "dlb_host_alloc", "dlb_host_free", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
+    "dlb_sign_batch_keyed", "dlb_verify_batch_keyed", "dlb_sign_batch_keyed_dev", "dlb_verify_batch_keyed_dev",
     "dlb_keygen_batch_dev", "dlb_sign_batch_dev", "dlb_verify_batch_dev", "dlb_dbg_keccak_f1600",
     "dlb_dbg_shake256", "dlb_dbg_expand_a", "dlb_dbg_expand_s", "dlb_dbg_expand_mask",
     "dlb_dbg_sample_in_ball", "dlb_dbg_ntt", "dlb_dbg_sign_attempt",
@@ -173,13 +180,21 @@ class Engine:
 
     # ---- batch.hpp:53-137
     def batch_sign(self, level, sks, messages, rho_prime=None, psi=0, speculate=True,
-                   return_info=False):
+                   return_info=False, key_idx=None):
+        """sks: one key (1-D), one key per task (n x sk_bytes), or -- with key_idx -- a table
+        of distinct keys (n_keys x sk_bytes) indexed per task (SignJob.key sharing,
+        batch.hpp:41-44)."""
         k, l, pkb, skb, sgb = LEVELS[level]
         sk, skp = _u8(sks)
         flat, off = _msgs(messages)
         n = len(off) - 1
         stride = 0 if sk.ndim == 1 else skb
-        if sk.size != (skb if stride == 0 else n * skb):
+        kidx = None
+        if key_idx is not None:
+            kidx = np.ascontiguousarray(key_idx, np.uint32)
+            if kidx.size != n or sk.size % skb:
+                raise ValueError("key_idx / key table have the wrong size")
+        elif sk.size != (skb if stride == 0 else n * skb):
             raise ValueError("secret key array has the wrong size")
         sigs = np.zeros((n, sgb), np.uint8)
         att = np.zeros(n, np.uint32)
@@ -189,10 +204,17 @@ class Engine:
         if rho_prime is not None:
             rpa, rp = _u8(rho_prime)
             assert rpa.size == n * 64
-        rc = self.lib.dlb_sign_batch(self.ctx, level, n, skp, stride, flat.ctypes.data_as(_u8p),
-                                     off.ctypes.data_as(_u64p), rp, psi, 1 if speculate else 0,
-                                     sigs.ctypes.data_as(_u8p), att.ctypes.data_as(_u32p),
-                                     failed.ctypes.data_as(_u8p), C.byref(st))
+        if kidx is not None:
+            rc = self.lib.dlb_sign_batch_keyed(self.ctx, level, sk.size // skb, skp, n,
+                                               kidx.ctypes.data_as(_u32p), flat.ctypes.data_as(_u8p),
+                                               off.ctypes.data_as(_u64p), rp, psi, 1 if speculate else 0,
+                                               sigs.ctypes.data_as(_u8p), att.ctypes.data_as(_u32p),
+                                               failed.ctypes.data_as(_u8p), C.byref(st))
+        else:
+            rc = self.lib.dlb_sign_batch(self.ctx, level, n, skp, stride, flat.ctypes.data_as(_u8p),
+                                         off.ctypes.data_as(_u64p), rp, psi, 1 if speculate else 0,
+                                         sigs.ctypes.data_as(_u8p), att.ctypes.data_as(_u32p),
+                                         failed.ctypes.data_as(_u8p), C.byref(st))
         if rc == -3:
             raise ValueError("sign: malformed secret key")  # scheme.hpp:271
         self._chk(rc, "dlb_sign_batch")
@@ -201,16 +223,25 @@ class Engine:
         return sigs
 
     # ---- batch.hpp:148-156
-    def batch_verify(self, level, pks, messages, sigs):
+    def batch_verify(self, level, pks, messages, sigs, key_idx=None):
         k, l, pkb, skb, sgb = LEVELS[level]
         pk, pkp = _u8(pks)
         sg, sgp = _u8(sigs)
         flat, off = _msgs(messages)
         n = len(off) - 1
         stride = 0 if pk.ndim == 1 else pkb
+        flags = np.zeros(n, np.uint8)
+        if key_idx is not None:
+            kidx = np.ascontiguousarray(key_idx, np.uint32)
+            if kidx.size != n or pk.size % pkb or sg.size != n * sgb:
+                raise ValueError("key_idx / key table / sig arrays have the wrong size")
+            self._chk(self.lib.dlb_verify_batch_keyed(self.ctx, level, pk.size // pkb, pkp, n,
+                                                      kidx.ctypes.data_as(_u32p), flat.ctypes.data_as(_u8p),
+                                                      off.ctypes.data_as(_u64p), sgp,
+                                                      flags.ctypes.data_as(_u8p)), "dlb_verify_batch_keyed")
+            return flags
         if sg.size != n * sgb or pk.size != (pkb if stride == 0 else n * pkb):
             raise ValueError("pk/sig arrays have the wrong size")
-        flags = np.zeros(n, np.uint8)
         self._chk(self.lib.dlb_verify_batch(self.ctx, level, n, pkp, stride,
                                             flat.ctypes.data_as(_u8p), off.ctypes.data_as(_u64p),
                                             sgp, flags.ctypes.data_as(_u8p)), "dlb_verify_batch")

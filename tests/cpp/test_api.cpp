@@ -60,6 +60,24 @@ void level_test(std::mt19937_64& rng) {
   vj[6].sig = std::span<const uint8_t>(sigs[6].data(), 10);  // wrong length
   auto flags = batch_verify<P>(std::span<const VerifyJob<P>>(vj));
   for (size_t i = 0; i < n; ++i) CHECK(flags[i] == ((i == 5 || i == 6) ? 0 : 1));
+  // mixed-key batch: three keys interleaved over the jobs (SignJob.key sharing, batch.hpp:41-44)
+  {
+    std::vector<SeedArray> kz(3);
+    for (auto& z : kz) for (auto& b : z) b = static_cast<uint8_t>(rng());
+    auto kp = batch_keygen<P>(std::span<const SeedArray>(kz));
+    std::vector<SignPrecomp<P>> pres;
+    for (auto& k : kp) pres.push_back(*make_precomp<P>(k.second));
+    std::vector<SignJob<P>> mj(n);
+    for (size_t i = 0; i < n; ++i) mj[i] = {&pres[(i * 7) % 3], msgs[i]};
+    auto ms = batch_sign<P>(std::span<const SignJob<P>>(mj));
+    std::vector<VerifyJob<P>> mv(n);
+    for (size_t i = 0; i < n; ++i) mv[i] = {kp[(i * 7) % 3].first, msgs[i], ms[i]};
+    auto mf = batch_verify<P>(std::span<const VerifyJob<P>>(mv));
+    for (size_t i = 0; i < n; ++i) CHECK(mf[i] == 1);
+    for (size_t i = 0; i < n; i += 11) CHECK(ms[i] == sign<P>(kp[(i * 7) % 3].second, msgs[i]));
+    mv[1].pk = kp[((1 * 7) % 3 + 1) % 3].first;  // wrong key
+    CHECK(batch_verify<P>(std::span<const VerifyJob<P>>(mv))[1] == 0);
+  }
   std::vector<SeedArray> zs(9);
   for (auto& z : zs) for (auto& b : z) b = static_cast<uint8_t>(rng());
   auto keys = batch_keygen<P>(std::span<const SeedArray>(zs));

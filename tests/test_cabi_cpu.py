@@ -101,3 +101,19 @@ def test_bench_work_model():
     assert 0.55e6 < bench.int_ops(bench.WORK[2]["verify"]) < 0.70e6
     assert 0.25e6 < bench.int_ops(bench.WORK[2]["attempt"]) < 0.30e6
     assert bench.WORK[2]["bytes"]["sign"] == 32 + 2420
+
+
+def test_cli_argument_errors_need_no_gpu():
+    """tools/dilithium_b200 rejects bad command lines with exit code 2 before it ever creates an
+    engine (proj/tests/test_cli.cpp:172-175: `keygen --pk a --sk b` without --level fails)."""
+    import subprocess
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools")], check=True)
+    cli = os.path.join(ROOT, "tools", "dilithium_b200")
+    for argv in (["keygen", "--pk", "a", "--sk", "b"], ["frobnicate"], [],
+                 ["verify", "--level", "4", "--pk", "a", "--in", "b", "--sig", "c"],
+                 ["sign", "--level", "2", "--sk", "a", "--in", "b"],
+                 ["batch-sign", "--level", "2", "--sk", "a", "--out-dir", "d"],
+                 ["keygen", "--level", "2", "--pk", "a", "--sk", "b", "--out-format", "base64"],
+                 ["bench", "--level", "2", "--phi", "x"]):
+        r = subprocess.run([cli, *argv], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 2 and "error:" in r.stderr, (argv, r.returncode, r.stderr)

@@ -85,3 +85,31 @@ def test_multi_engine_sharded_stream(eng, oracle):
     assert np.array_equal(sigs, eng.batch_sign(level, sk_a, (flat, off)))
     assert me.batch_verify(level, pk_a, flat, off, sigs, chunk=777).all()
     me.close()
+
+
+@pytest.mark.parametrize("level", [2, 3, 5])
+def test_keyed_batches(eng, oracle, level):
+    """Mixed-key batches (SignJob.key sharing, batch.hpp:41-44): a table of distinct keys plus a
+    key index per task gives the same bytes as one-key-per-task and as the CPU oracle."""
+    n, nk = 3000, 7
+    rng = mt19937_64(4100 + level)
+    zetas = np.frombuffer(rng.bytes(32 * nk), np.uint8).reshape(nk, 32)
+    pks, sks = eng.batch_keygen(level, zetas)
+    lens = [int(rng()) % 48 for _ in range(n)]
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    flat = np.frombuffer(rng.bytes(int(off[-1]) + 1), np.uint8)
+    kidx = np.array([int(rng()) % nk for _ in range(n)], np.uint32)
+    sigs, att, failed, _ = eng.batch_sign(level, sks, (flat, off), key_idx=kidx, return_info=True)
+    assert not failed.any()
+    assert np.array_equal(sigs, eng.batch_sign(level, sks[kidx], (flat, off)))  # one key per task
+    for i in range(0, n, 211):
+        m = flat[int(off[i]):int(off[i + 1])].tobytes()
+        assert (sigs[i].tobytes(), int(att[i])) == oracle.sign(level, sks[kidx[i]].tobytes(), m)
+    assert eng.batch_verify(level, pks, (flat, off), sigs, key_idx=kidx).all()
+    assert np.array_equal(eng.batch_verify(level, pks, (flat, off), sigs, key_idx=kidx),
+                          eng.batch_verify(level, pks[kidx], (flat, off), sigs))
+    wrong = (kidx + 1) % nk
+    assert not eng.batch_verify(level, pks, (flat, off), sigs, key_idx=wrong).any()
+    with pytest.raises(Exception):  # out-of-range key index is an argument error
+        eng.batch_sign(level, sks, (flat, off), key_idx=np.full(n, nk, np.uint32))

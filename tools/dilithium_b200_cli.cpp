@@ -1,0 +1,464 @@
+// dilithium_b200 -- command-line front end of the B200 engine.
+//
+// Same subcommands, options, file formats and exit codes as the reference tool
+// (proj/tools/dilithium_cli.cpp:136-297 commands, :360-446 bench, :518-607 option table;
+// behaviour pinned by proj/tests/test_cli.cpp:61-175):
+//
+//   keygen       --level L --pk F --sk F [--seed HEX64] [--out-format binary|hex]
+//   sign         --level L --sk F --in MSG --out SIG [--out-format ...]
+//   verify       --level L --pk F --in MSG --sig SIG        exit 0 accept / 1 reject / 2 bad input
+//   batch-sign   --level L --sk F --out-dir D [--psi N] [--workers N] [--trace CSV] MSG...
+//   batch-verify --level L --pk F --sig-dir D [--workers N] MSG...     exit 0 iff all accept
+//   bench        --level L [--phi N] [--psi N] [--workers N] [--streams N] [--reps N]
+//                CSV on stdout: schema,mode,op,level,phi,psi,workers,streams,reps,
+//                               throughput_ops_s,mean_latency_us,attempts_mean
+//
+// Key and signature files are raw bytes or the hex text written with --out-format hex; the
+// expected object length tells them apart.  --workers is accepted and ignored (the GPU grid
+// replaces the worker pool).  --trace writes the device scheduler's aggregate counters (the
+// persistent kernel has no host-visible rounds to trace one by one).
+//
+// The option parser is this file's own (the reference uses CLI11, which this tree does not
+// vendor): a table of named options per subcommand, positionals collected in order.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <random>
+#include <set>
+#include <string>
+
+#include "dilithium_b200/api.hpp"
+
+namespace fs = std::filesystem;
+using namespace dilithium::b200;
+using Bytes = std::vector<uint8_t>;
+
+namespace {
+
+constexpr int kOk = 0, kReject = 1, kBadInput = 2;
+
+// ---- files ---------------------------------------------------------------------------
+
+bool slurp(const std::string& path, Bytes& out) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) return false;
+  out.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+  return true;
+}
+
+bool unhex(const Bytes& text, Bytes& out) {
+  size_t len = text.size();
+  while (len && (text[len - 1] == '\n' || text[len - 1] == '\r' || text[len - 1] == ' ')) --len;
+  if (len % 2) return false;
+  auto val = [](uint8_t c) -> int {
+    if (c >= '0' && c <= '9') return c - '0';
+    c |= 0x20;
+    return (c >= 'a' && c <= 'f') ? c - 'a' + 10 : -1;
+  };
+  out.resize(len / 2);
+  for (size_t i = 0; i < out.size(); ++i) {
+    const int hi = val(text[2 * i]), lo = val(text[2 * i + 1]);
+    if (hi < 0 || lo < 0) return false;
+    out[i] = static_cast<uint8_t>(hi * 16 + lo);
+  }
+  return true;
+}
+
+// raw bytes of the expected length, else hex text of that length
+bool load_object(const std::string& path, size_t want, Bytes& out) {
+  Bytes raw;
+  if (!slurp(path, raw)) return false;
+  if (raw.size() == want) {
+    out.swap(raw);
+    return true;
+  }
+  return unhex(raw, out) && out.size() == want;
+}
+
+bool store(const std::string& path, std::span<const uint8_t> data, bool hex) {
+  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  if (!out) return false;
+  if (!hex) {
+    out.write(reinterpret_cast<const char*>(data.data()), static_cast<std::streamsize>(data.size()));
+  } else {
+    std::string text(2 * data.size() + 1, '\n');
+    for (size_t i = 0; i < data.size(); ++i) {
+      text[2 * i] = "0123456789abcdef"[data[i] >> 4];
+      text[2 * i + 1] = "0123456789abcdef"[data[i] & 15];
+    }
+    out << text;
+  }
+  return static_cast<bool>(out);
+}
+
+// ---- options -------------------------------------------------------------------------
+
+struct Args {
+  std::map<std::string, std::string> opt;
+  std::vector<std::string> positional;
+  bool has(const std::string& k) const { return opt.count(k) != 0; }
+  std::string get(const std::string& k, const std::string& dflt = "") const {
+    auto it = opt.find(k);
+    return it == opt.end() ? dflt : it->second;
+  }
+  bool number(const std::string& k, size_t dflt, size_t& out) const {
+    out = dflt;
+    if (!has(k)) return true;
+    const std::string& v = opt.at(k);
+    if (v.empty() || v.find_first_not_of("0123456789") != std::string::npos) return false;
+    out = std::stoull(v);
+    return true;
+  }
+};
+
+struct Command {
+  std::set<std::string> options, required;
+  bool positionals;
+};
+
+const std::map<std::string, Command>& commands() {
+  static const std::set<std::string> common = {"--level", "--out-format", "--seed"};
+  auto with = [&](std::set<std::string> extra) {
+    extra.insert(common.begin(), common.end());
+    return extra;
+  };
+  static const std::map<std::string, Command> table = {
+      {"keygen", {with({"--pk", "--sk"}), {"--level", "--pk", "--sk"}, false}},
+      {"sign", {with({"--sk", "--in", "--out"}), {"--level", "--sk", "--in", "--out"}, false}},
+      {"verify", {with({"--pk", "--in", "--sig"}), {"--level", "--pk", "--in", "--sig"}, false}},
+      {"batch-sign", {with({"--sk", "--out-dir", "--psi", "--workers", "--trace"}), {"--level", "--sk", "--out-dir"}, true}},
+      {"batch-verify", {with({"--pk", "--sig-dir", "--workers"}), {"--level", "--pk", "--sig-dir"}, true}},
+      {"bench", {with({"--phi", "--psi", "--workers", "--streams", "--reps", "--trace"}), {"--level"}, false}},
+  };
+  return table;
+}
+
+int usage(const std::string& why) {
+  std::cerr << "error: " << why << "\n"
+            << "usage: dilithium_b200 <keygen|sign|verify|batch-sign|batch-verify|bench> --level {2,3,5} ...\n";
+  return kBadInput;
+}
+
+bool parse(int argc, char** argv, const Command& cmd, Args& a, std::string& why) {
+  for (int i = 2; i < argc; ++i) {
+    std::string tok = argv[i];
+    if (tok.rfind("--", 0) == 0) {
+      std::string val;
+      const size_t eq = tok.find('=');
+      if (eq != std::string::npos) {
+        val = tok.substr(eq + 1);
+        tok = tok.substr(0, eq);
+      } else if (i + 1 < argc) {
+        val = argv[++i];
+      } else {
+        why = tok + " needs a value";
+        return false;
+      }
+      if (!cmd.options.count(tok)) {
+        why = "unknown option " + tok;
+        return false;
+      }
+      a.opt[tok] = val;
+    } else if (cmd.positionals) {
+      a.positional.push_back(tok);
+    } else {
+      why = "unexpected argument " + tok;
+      return false;
+    }
+  }
+  for (const auto& r : cmd.required)
+    if (!a.has(r)) {
+      why = r + " is required";
+      return false;
+    }
+  if (cmd.positionals && a.positional.empty()) {
+    why = "at least one message file is required";
+    return false;
+  }
+  const std::string lv = a.get("--level");
+  if (lv != "2" && lv != "3" && lv != "5") {
+    why = "--level must be 2, 3 or 5";
+    return false;
+  }
+  const std::string fmt = a.get("--out-format", "binary");
+  if (fmt != "binary" && fmt != "hex") {
+    why = "--out-format must be binary or hex";
+    return false;
+  }
+  return true;
+}
+
+template <class Fn>
+int with_level(const Args& a, Fn&& fn) {
+  switch (a.get("--level")[0]) {
+    case '2': return fn(std::integral_constant<int, 2>{});
+    case '3': return fn(std::integral_constant<int, 3>{});
+    default: return fn(std::integral_constant<int, 5>{});
+  }
+}
+template <int L>
+constexpr Params params_of() {
+  return L == 2 ? kDilithium2 : (L == 3 ? kDilithium3 : kDilithium5);
+}
+
+// strict hint-section check of a signature (packing.hpp:122-140): what the reference's
+// unpack_sig refuses and its CLI reports as exit 2 rather than "reject"
+template <Params P>
+bool sig_encoding_ok(std::span<const uint8_t> sig) {
+  const uint8_t* h = sig.data() + 32 + P.l * 32 * P.z_bits;
+  size_t prev = 0;
+  for (size_t i = 0; i < P.k; ++i) {
+    const size_t cnt = h[P.omega + i];
+    if (cnt < prev || cnt > P.omega) return false;
+    for (size_t j = prev + 1; j < cnt; ++j)
+      if (h[j] <= h[j - 1]) return false;
+    prev = cnt;
+  }
+  for (size_t j = prev; j < P.omega; ++j)
+    if (h[j] != 0) return false;
+  return true;
+}
+
+// ---- commands ------------------------------------------------------------------------
+
+int cmd_keygen(const Args& a) {
+  SeedArray zeta;
+  if (a.has("--seed")) {
+    Bytes seed;
+    const std::string hex = a.get("--seed");
+    if (!unhex(Bytes(hex.begin(), hex.end()), seed) || seed.size() != kSeedBytes) {
+      std::cerr << "error: --seed must be " << 2 * kSeedBytes << " hex characters\n";
+      return kBadInput;
+    }
+    std::copy(seed.begin(), seed.end(), zeta.begin());
+    std::cerr << "warning: deterministic seed supplied; keys derived from it are for testing only\n";
+  } else {
+    std::random_device rd;
+    for (auto& b : zeta) b = static_cast<uint8_t>(rd());
+  }
+  const bool hex = a.get("--out-format") == "hex";
+  return with_level(a, [&](auto lv) {
+    constexpr Params P = params_of<decltype(lv)::value>();
+    const auto [pk, sk] = keygen<P>(zeta);
+    if (store(a.get("--pk"), pk, hex) && store(a.get("--sk"), sk, hex)) return kOk;
+    std::cerr << "error: cannot write key files\n";
+    return kBadInput;
+  });
+}
+
+int cmd_sign(const Args& a) {
+  const bool hex = a.get("--out-format") == "hex";
+  return with_level(a, [&](auto lv) {
+    constexpr Params P = params_of<decltype(lv)::value>();
+    Bytes sk, msg;
+    if (!load_object(a.get("--sk"), P.sk_bytes(), sk) || !slurp(a.get("--in"), msg)) {
+      std::cerr << "error: cannot read secret key or message\n";
+      return kBadInput;
+    }
+    const auto pre = make_precomp<P>(sk);
+    if (!pre) {
+      std::cerr << "error: malformed secret key\n";
+      return kBadInput;
+    }
+    const auto sig = sign_with_precomp<P>(*pre, msg).sig;
+    if (store(a.get("--out"), sig, hex)) return kOk;
+    std::cerr << "error: cannot write signature\n";
+    return kBadInput;
+  });
+}
+
+int cmd_verify(const Args& a) {
+  return with_level(a, [&](auto lv) {
+    constexpr Params P = params_of<decltype(lv)::value>();
+    Bytes pk, sig, msg;
+    if (!load_object(a.get("--pk"), P.pk_bytes(), pk) || !load_object(a.get("--sig"), P.sig_bytes(), sig) ||
+        !slurp(a.get("--in"), msg)) {
+      std::cerr << "error: malformed or missing input file\n";
+      return kBadInput;
+    }
+    if (!sig_encoding_ok<P>(sig)) {
+      std::cerr << "error: malformed key or signature encoding\n";
+      return kBadInput;
+    }
+    const bool ok = verify<P>(pk, msg, sig);
+    std::cout << (ok ? "accept\n" : "reject\n");
+    return ok ? kOk : kReject;
+  });
+}
+
+void write_trace(const std::string& path, const BatchStats& st, size_t tasks) {
+  if (path.empty()) return;
+  std::ofstream out(path, std::ios::trunc);
+  out << "stream,tasks,rounds,attempts,speculative,idle_slot_rounds,accepted_attempt_sum,failed\n"
+      << 0 << ',' << tasks << ',' << st.rounds << ',' << st.attempts << ',' << st.speculative << ','
+      << st.idle_slot_rounds << ',' << st.accepted_attempt_sum << ',' << st.failed_tasks.size() << '\n';
+}
+
+int cmd_batch_sign(const Args& a) {
+  const bool hex = a.get("--out-format") == "hex";
+  size_t psi = 0;
+  if (!a.number("--psi", 0, psi)) return usage("--psi must be a number");
+  return with_level(a, [&](auto lv) {
+    constexpr Params P = params_of<decltype(lv)::value>();
+    Bytes sk;
+    if (!load_object(a.get("--sk"), P.sk_bytes(), sk)) {
+      std::cerr << "error: cannot read secret key\n";
+      return kBadInput;
+    }
+    const auto pre = make_precomp<P>(sk);
+    if (!pre) {
+      std::cerr << "error: malformed secret key\n";
+      return kBadInput;
+    }
+    std::vector<Bytes> msgs(a.positional.size());
+    for (size_t i = 0; i < msgs.size(); ++i)
+      if (!slurp(a.positional[i], msgs[i])) {
+        std::cerr << "error: cannot read " << a.positional[i] << "\n";
+        return kBadInput;
+      }
+    if (psi > msgs.size()) {  // the reference tool's rule (dilithium_cli.cpp:233)
+      std::cerr << "error: --psi must not exceed the number of messages\n";
+      return kBadInput;
+    }
+    std::vector<SignJob<P>> jobs;
+    for (const auto& m : msgs) jobs.push_back({&*pre, m});
+    BatchConfig cfg;
+    cfg.psi = psi;
+    BatchStats st;
+    const auto sigs = batch_sign<P>(std::span<const SignJob<P>>(jobs), cfg, &st);
+    write_trace(a.get("--trace"), st, jobs.size());
+    if (!st.failed_tasks.empty()) {
+      std::cerr << "error: " << st.failed_tasks.size() << " task(s) exhausted the nonce space\n";
+      return kBadInput;
+    }
+    std::error_code ec;
+    fs::create_directories(a.get("--out-dir"), ec);
+    for (size_t i = 0; i < sigs.size(); ++i) {
+      const auto name = fs::path(a.positional[i]).filename().string() + ".sig";
+      if (!store((fs::path(a.get("--out-dir")) / name).string(), sigs[i], hex)) {
+        std::cerr << "error: cannot write " << name << "\n";
+        return kBadInput;
+      }
+    }
+    return kOk;
+  });
+}
+
+int cmd_batch_verify(const Args& a) {
+  return with_level(a, [&](auto lv) {
+    constexpr Params P = params_of<decltype(lv)::value>();
+    Bytes pk;
+    if (!load_object(a.get("--pk"), P.pk_bytes(), pk)) {
+      std::cerr << "error: cannot read public key\n";
+      return kBadInput;
+    }
+    const size_t n = a.positional.size();
+    std::vector<Bytes> msgs(n), sigs(n);
+    for (size_t i = 0; i < n; ++i) {
+      if (!slurp(a.positional[i], msgs[i])) {
+        std::cerr << "error: cannot read " << a.positional[i] << "\n";
+        return kBadInput;
+      }
+      const auto name = fs::path(a.positional[i]).filename().string() + ".sig";
+      if (!load_object((fs::path(a.get("--sig-dir")) / name).string(), P.sig_bytes(), sigs[i]))
+        sigs[i].clear();  // missing or wrong-size signature: rejected below
+    }
+    std::vector<VerifyJob<P>> jobs(n);
+    for (size_t i = 0; i < n; ++i) jobs[i] = {pk, msgs[i], sigs[i]};
+    const auto flags = batch_verify<P>(std::span<const VerifyJob<P>>(jobs));
+    bool all = true;
+    for (size_t i = 0; i < n; ++i) {
+      std::cout << a.positional[i] << ": " << (flags[i] ? "accept" : "reject") << "\n";
+      all = all && flags[i];
+    }
+    return all ? kOk : kReject;
+  });
+}
+
+template <class Fn>
+double median_seconds(size_t reps, Fn&& fn) {
+  fn();  // warm-up: arenas, first-launch costs
+  std::vector<double> t(reps);
+  for (auto& x : t) {
+    const auto t0 = std::chrono::steady_clock::now();
+    fn();
+    x = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  std::sort(t.begin(), t.end());
+  return t[t.size() / 2];
+}
+
+int cmd_bench(const Args& a) {
+  size_t phi, psi, workers, streams, reps;
+  if (!a.number("--phi", 1000, phi) || !a.number("--psi", 0, psi) || !a.number("--workers", 1, workers) ||
+      !a.number("--streams", 1, streams) || !a.number("--reps", 5, reps) || phi == 0 || reps == 0)
+    return usage("bench options must be positive numbers");
+  if (psi > phi) return usage("--psi must not exceed --phi");
+  return with_level(a, [&](auto lv) {
+    constexpr Params P = params_of<decltype(lv)::value>();
+    std::mt19937_64 rng(20221112);
+    std::vector<SeedArray> zetas(phi);
+    for (auto& z : zetas)
+      for (auto& b : z) b = static_cast<uint8_t>(rng());
+    const auto [pk, sk] = keygen<P>(zetas[0]);
+    const auto pre = make_precomp<P>(sk);
+    // the reference bench signs 59-byte messages (dilithium_cli.cpp:366-370)
+    std::vector<Bytes> msgs(phi, Bytes(59));
+    for (auto& m : msgs)
+      for (auto& b : m) b = static_cast<uint8_t>(rng());
+    std::vector<SignJob<P>> jobs;
+    for (const auto& m : msgs) jobs.push_back({&*pre, m});
+    BatchConfig cfg;
+    cfg.psi = psi;
+    BatchStats st;
+    std::vector<SigBytes<P>> sigs;
+    std::cout << "schema,mode,op,level,phi,psi,workers,streams,reps,throughput_ops_s,mean_latency_us,attempts_mean\n";
+    auto row = [&](const char* op, double sec, const std::string& attempts) {
+      std::printf("1,batch-gpu,%s,%d,%zu,%zu,%zu,%zu,%zu,%.1f,%.3f,%s\n", op, P.level, phi, psi, workers,
+                  streams, reps, phi / sec, sec / phi * 1e6, attempts.c_str());
+    };
+    row("keygen", median_seconds(reps, [&] { batch_keygen<P>(std::span<const SeedArray>(zetas)); }), "");
+    const double ts = median_seconds(reps, [&] { sigs = batch_sign<P>(std::span<const SignJob<P>>(jobs), cfg, &st); });
+    char att[32];
+    std::snprintf(att, sizeof att, "%.3f", double(st.accepted_attempt_sum) / phi);
+    row("sign", ts, att);
+    write_trace(a.get("--trace"), st, phi);
+    std::vector<VerifyJob<P>> vj(phi);
+    for (size_t i = 0; i < phi; ++i) vj[i] = {pk, msgs[i], sigs[i]};
+    std::vector<uint8_t> flags;
+    row("verify", median_seconds(reps, [&] { flags = batch_verify<P>(std::span<const VerifyJob<P>>(vj)); }), "");
+    for (auto f : flags)
+      if (!f) {
+        std::cerr << "error: bench produced a signature that does not verify\n";
+        return kBadInput;
+      }
+    return kOk;
+  });
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) return usage("missing subcommand");
+  const std::string name = argv[1];
+  const auto it = commands().find(name);
+  if (it == commands().end()) return usage("unknown subcommand " + name);
+  Args a;
+  std::string why;
+  if (!parse(argc, argv, it->second, a, why)) return usage(why);
+  try {
+    if (name == "keygen") return cmd_keygen(a);
+    if (name == "sign") return cmd_sign(a);
+    if (name == "verify") return cmd_verify(a);
+    if (name == "batch-sign") return cmd_batch_sign(a);
+    if (name == "batch-verify") return cmd_batch_verify(a);
+    return cmd_bench(a);
+  } catch (const std::exception& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return kBadInput;
+  }
+}
