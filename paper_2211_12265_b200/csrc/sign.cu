@@ -341,6 +341,9 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
     ++pp.k;
     cp_async_wait<1>();
     __syncwarp();
+    // The exact product c*s1 has coefficients in [-beta, beta] (tau non-zero challenge
+    // entries times eta) and c*t0 in (-2^22, 2^22), so the inverse NTT's output in (-q, q) is
+    // that small value or the same +-q: reduce32 returns the centred value itself.
     bool bad = false;
     if (p < P::K) {
       const int32_t* wrow = reinterpret_cast<const int32_t*>(cur);
@@ -359,7 +362,7 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int32_t y = P::GAMMA1 - (int32_t)raw[e];
-        const int32_t z = center(freeze(y + t[e]));
+        const int32_t z = y + reduce32(t[e]);  // |y| <= gamma1, |c s1| <= beta: no wrap, centred
         bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
         ws.vhat[p - P::K][e][lane] = z;
       }
@@ -378,7 +381,7 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
     bool bad = false;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int32_t vt = center(caddq(t[e]));
+      const int32_t vt = reduce32(t[e]);  // |c t0| <= tau * 2^12 < 2^22: already centred
       bad = bad || abs(vt) >= P::GAMMA2;
       const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != highbits<P::GAMMA2>(wcs2[e]);
       const unsigned mask = __ballot_sync(FULL, h);

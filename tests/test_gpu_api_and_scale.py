@@ -113,3 +113,32 @@ def test_keyed_batches(eng, oracle, level):
     assert not eng.batch_verify(level, pks, (flat, off), sigs, key_idx=wrong).any()
     with pytest.raises(Exception):  # out-of-range key index is an argument error
         eng.batch_sign(level, sks, (flat, off), key_idx=np.full(n, nk, np.uint32))
+
+
+@pytest.mark.parametrize("level,n", [(2, 1000000), (3, 250000), (5, 250000)])
+def test_streamed_large_batch(oracle, level, n):
+    """configs[4] at full size (level 2: one million tasks; 3 / 5 bounded for test time):
+    streamed in 64k-task chunks through the sharded front end.  Size-independent
+    properties: every signature verifies, 1 % injected bit flips are all rejected and only
+    they, a 1e-3 sample of signatures and of verdicts equals the CPU oracle's."""
+    from paper_2211_12265_b200.sharding import MultiEngine
+    rs = np.random.default_rng(7000 + level)
+    pk, sk = oracle.keygen(level, rs.integers(0, 256, 32, dtype=np.uint8).tobytes())
+    flat = rs.integers(0, 256, 32 * n, dtype=np.uint8)
+    off = np.arange(n + 1, dtype=np.uint64) * 32
+    sk_a, pk_a = np.frombuffer(sk, np.uint8), np.frombuffer(pk, np.uint8)
+    me = MultiEngine([0])
+    sigs = me.batch_sign(level, sk_a, flat, off)
+    for i in range(0, n, n // 100):  # byte compare against the CPU oracle
+        assert sigs[i].tobytes() == oracle.sign(level, sk, flat[32 * i:32 * i + 32].tobytes())[0]
+    assert me.batch_verify(level, pk_a, flat, off, sigs).all()
+    idx = rs.choice(n, n // 100, replace=False)
+    bad = sigs.copy()
+    bad[idx, rs.integers(0, bad.shape[1], idx.size)] ^= (1 << rs.integers(0, 8, idx.size)).astype(np.uint8)
+    flags = me.batch_verify(level, pk_a, flat, off, bad)
+    expect = np.ones(n, np.uint8)
+    expect[idx] = 0
+    assert np.array_equal(flags, expect)
+    for i in idx[:50]:
+        assert oracle.verify(level, pk, flat[32 * i:32 * i + 32].tobytes(), bad[i].tobytes()) == 0
+    me.close()
