@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -103,6 +104,24 @@ inline int dalloc(dlb_ctx* c, const char* name, size_t count, T** out) {
 }
 
 inline unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
+
+// One L1 / shared-memory split for every kernel of a pipeline.  The split is a per-SM
+// setting that cannot change under resident CTAs: a kernel that prefers another split than
+// the one an SM is running waits until that SM (measured: the whole previous grid) has
+// drained, which serialises kernels that should overlap -- the chunk lanes of keygen /
+// verify, or two engine contexts (scripts/ubench/overlap.cu).  percent = share of the
+// 256 KB given to shared memory (cudaSharedmemCarveoutMaxShared = 100).
+template <class K>
+inline void prefer_carveout(K kernel, int percent) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, percent);
+}
+inline int pipeline_carveout() {
+  static const int v = [] {
+    const char* e = getenv("DLB_CARVEOUT");  // experiments: -1 leaves the driver's per-kernel choice
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
 
 #define DLB_TRY(x)            \
   do {                        \
