@@ -312,7 +312,10 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
   };
   auto ring_bytes = [&](int r) -> unsigned { return r < P::K ? kN * 4 : S::Z_POLY; };
 
-  // ring chunk 0, then the next slot's head; then wait for everything older (our head)
+  // ring chunk 0, then the next slot's head; then wait for everything older (our head).
+  // (The buffer it lands in was read by the whole warp while finishing the previous slot;
+  // that slot ended on a warp vote -- the explicit barrier states the ordering.)
+  __syncwarp();
   warp_fetch(pp.ring(pp.k), ring_src(0), ring_bytes(0), lane);
   cp_async_commit();
   ++pp.k;
@@ -403,7 +406,8 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
     pack_tile<P::Z_BITS>(ws.tile, pp.ring(pp.k), stage_sig + 32 + j * S::Z_POLY, lane);
   }
   uint8_t* hint = stage_sig + 32 + P::L * S::Z_POLY;
-  for (int b = lane; b < S::HINT; b += 32) hint[b] = 0;
+  // (the padding behind the signature is cleared too: the word-wise commit copy reads it)
+  for (int b = lane; b < S::HINT + (SignSizes<P>::SIG_PAD - S::SIG); b += 32) hint[b] = 0;
   __syncwarp();
   unsigned count = 0;
 #pragma unroll 1

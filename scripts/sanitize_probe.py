@@ -1,4 +1,5 @@
 """Small end-to-end pass used under compute-sanitizer (memcheck / racecheck / initcheck)."""
+import os
 import sys
 import numpy as np
 sys.path.insert(0, ".")
@@ -13,4 +14,9 @@ for level, n in ((2, 300), (3, 150), (5, 130)):
     sigs2 = eng.batch_sign(level, sks[0], msgs, psi=256)
     assert eng.batch_verify(level, pks, msgs, sigs).all()
     assert eng.batch_verify(level, pks[0], msgs, sigs2).all()
+    if os.environ.get("DLB_NO_KEYED"):
+        continue
+    kidx = rng.integers(0, 5, n).astype(np.uint32)  # mixed-key batch over a 5-key table
+    sigs3 = eng.batch_sign(level, sks[:5], msgs, key_idx=kidx)
+    assert eng.batch_verify(level, pks[:5], msgs, sigs3, key_idx=kidx).all()
     print("level", level, "ok, mean attempts %.2f" % att.mean())
