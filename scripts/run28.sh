@@ -2,7 +2,7 @@ set -e
 cd /root/repo
 mkdir -p gpurun_out
 export DLB_NO_PEAK=1
-T=r01b
+T=r01c
 timeout 600 ncu --set full --clock-control none -k regex:"k_" -c 60 -o /tmp/prof_kv -f python scripts/perf_probe.py 2 32768 keygen,verify 0 > gpurun_out/ncu_kv.log 2>&1 || (tail -5 gpurun_out/ncu_kv.log; exit 1)
 python scripts/ncu_summary.py /tmp/prof_kv.ncu-rep gpurun_out/${T}_kernels_keygen_verify > /dev/null
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_sign|k_hash_mu" -c 4 -o gpurun_out/prof_sign_$T -f python scripts/perf_probe.py 2 100000 sign 0 > gpurun_out/ncu_sign.log 2>&1 || (tail -5 gpurun_out/ncu_sign.log; exit 1)
@@ -13,3 +13,4 @@ python scripts/ncu_summary.py /tmp/prof_sign_l$lv.ncu-rep gpurun_out/${T}_kernel
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-levels --no-stream > gpurun_out/bench_under_ncu.json 2> gpurun_out/bench_under_ncu.err || (tail -5 gpurun_out/bench_under_ncu.err; exit 1)
 ls gpurun_out
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/r01c_bench.json 2> gpurun_out/r01c_bench.err || tail -5 gpurun_out/r01c_bench.err
