@@ -751,12 +751,19 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
                                                                kSignThreads, smem_bytes));
   if (occ < 1) occ = 1;
   const size_t grid_max = (size_t)c->sm_count * occ;
-  // Psi = resident attempt slots (BatchConfig::psi).  Default: about three slots per open
-  // task while the batch is smaller than the machine (measured optimum of the Psi sweep,
-  // profiles/r01_summary.md), every resident slot otherwise.  A Psi below the machine's
-  // capacity is spread over as many CTAs as possible, each using fewer of its 128 slots:
-  // the warp-per-slot stages of a round then take proportionally less time.
-  size_t want_slots = psi ? psi : (speculate ? 3 * n : n);
+  // Psi = resident attempt slots (BatchConfig::psi).  Default (measured, profiles/
+  // r01_summary.md): nine slots per task -- the speculation depth cap plus one -- while that
+  // fits one warp's worth of slots per CTA (batches up to ~2,000 tasks: latency is what
+  // matters there and the unluckiest task should advance nine nonces per round), about three
+  // per task up to the machine's capacity, every resident slot beyond.  A Psi below the
+  // machine's capacity is spread over as many CTAs as there are tasks (up to the resident
+  // maximum), each using fewer of its 128 slots: the warp-per-slot stages of a round then
+  // take proportionally less time.
+  size_t want_slots = psi;
+  if (!want_slots) {
+    if (!speculate) want_slots = n;
+    else want_slots = 9 * n <= grid_max * 32 ? 9 * n : 3 * n;
+  }
   if (want_slots < 1) want_slots = 1;
   size_t slots_per = kSignThreads, grid = grid_max;
   if (want_slots < grid_max * kSignThreads) {
@@ -764,6 +771,11 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
     slots_per = (slots_per + 31) / 32 * 32;
     if (slots_per > (size_t)kSignThreads) slots_per = kSignThreads;
     grid = (want_slots + slots_per - 1) / slots_per;
+    const size_t spread = n < grid_max ? n : grid_max;  // one task per CTA while CTAs are free
+    if (grid < spread) {
+      grid = spread;
+      slots_per = ((want_slots + grid - 1) / grid + 31) / 32 * 32;
+    }
     if (grid > grid_max) grid = grid_max;
   }
   size_t tcap = (n + grid - 1) / grid;
@@ -783,7 +795,7 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   a.speculate = single_round ? 0 : speculate;
   // Deepest speculative attempt a task may run in one round.  Filling every idle slot
   // (the reference's pass 2) wastes work once few tasks remain: attempt d is only needed
-  // with probability (1-p)^d.  Measured on B200 (profiles/r02_summary.md): cap 8 gives the
+  // with probability (1-p)^d.  Measured on B200 (profiles/r01_summary.md): cap 8 gives the
   // best batch-10k latency and batch-100k throughput; speculate > 1 sets the cap explicitly.
   a.spec_depth = speculate > 1 ? (unsigned)speculate : 8u;
   if (const char* e = getenv("DLB_SPEC_DEPTH")) a.spec_depth = (unsigned)atoi(e);  // experiments
