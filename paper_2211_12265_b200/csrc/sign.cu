@@ -501,13 +501,26 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
     const unsigned my_task = sm.slot_task[tid];
 
     // ---- S1: masks ---------------------------------------------------------------
-    if (my_task != kNoSlot) {
-      const unsigned k0 = a.kappa0 ? a.kappa0[my_task] : 0u;
-      const unsigned kappa = k0 + sm.slot_attempt[tid] * P::L;
+    // One sponge per (slot, polynomial): the L mask polynomials of an attempt are independent
+    // streams (nonces kappa .. kappa + L - 1), so when a round runs fewer slots than the CTA
+    // has threads -- small batches, the tail of a large one -- they spread over the idle
+    // threads and the round's longest sequential Keccak chain shrinks from 5 L permutations
+    // towards 5.  Active slots are a prefix [0, span); items are laid out polynomial-major so
+    // the lanes of a warp share j.  With all 128 slots active this is thread t -> slot t,
+    // j = 0 .. L-1, as before.
+    {
+      const unsigned cap = a.speculate ? a.spec_depth + 1u : 1u;
+      const unsigned span = min(a.slots, U * cap);
 #pragma unroll 1
-      for (int j = 0; j < P::L; ++j)
-        expand_mask_stream<P>(a.rho_prime + (size_t)my_task * 8, kappa + j,
-                              ybytes + (size_t)tid * Z::Y_SLOT + j * S::Z_POLY);
+      for (unsigned item = tid; item < span * P::L; item += kSignThreads) {
+        const unsigned slot = item % span, j = item / span;
+        const unsigned task = sm.slot_task[slot];
+        if (task == kNoSlot) continue;
+        const unsigned k0 = a.kappa0 ? a.kappa0[task] : 0u;
+        const unsigned kappa = k0 + sm.slot_attempt[slot] * P::L;
+        expand_mask_stream<P>(a.rho_prime + (size_t)task * 8, kappa + j,
+                              ybytes + (size_t)slot * Z::Y_SLOT + j * S::Z_POLY);
+      }
     }
     __syncthreads();
 
