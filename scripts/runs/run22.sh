@@ -1,0 +1,5 @@
+cd /root/repo
+export DLB_NO_PEAK=1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+LEVELS=2,3,5 SIZES=100000 VARIANTS=base bash scripts/runs/ab.sh
+SIZES=10000,1000000 VARIANTS=base bash scripts/runs/ab.sh

@@ -1,5 +1,5 @@
 cd /root/repo
 export DLB_NO_PEAK=1
 timeout 600 python -m pytest tests/test_gpu_sign.py tests/test_gpu_edges.py -m gpu -x -q 2>&1 | tail -2
-LEVELS=2,3,5 SIZES=100000 VARIANTS=base2 bash scripts/ab.sh
-SIZES=10000,1000000 VARIANTS=base2 bash scripts/ab.sh
+LEVELS=2,3,5 SIZES=100000 VARIANTS=base2 bash scripts/runs/ab.sh
+SIZES=10000,1000000 VARIANTS=base2 bash scripts/runs/ab.sh
