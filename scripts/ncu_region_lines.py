@@ -21,8 +21,19 @@ for l in dis_all.splitlines():
         lines.append(cur)
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-hdr = rows[1]
-body = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+want = "k_sign_persistent" if "k_sign_persistent" in kern else ""
+start = 0
+for i, r in enumerate(rows):  # the report may hold several kernels: pick the matching block
+    if len(r) >= 2 and r[0] == "Kernel Name" and want in r[1]:
+        start = i
+        break
+hdr = rows[start + 1]
+body = []
+for r in rows[start + 2:]:
+    if len(r) >= 2 and r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        body.append(dict(zip(hdr, r)))
 assert len(body) == len(lines), (len(body), len(lines))
 tot = sum(float(d["Instructions Executed"] or 0) for d in body)
 reg = 0
