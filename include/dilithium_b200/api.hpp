@@ -18,12 +18,17 @@
 // accepted and ignored (the GPU grid replaces the worker pool); cfg.psi = resident
 // attempt slots; cfg.speculate honoured.  Header-only, C++20, links libdilithium_b200.so.
 #pragma once
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <cstring>
+#include <exception>
+#include <memory>
 #include <optional>
 #include <span>
 #include <stdexcept>
+#include <string>
+#include <thread>
 #include <utility>
 #include <unordered_map>
 #include <vector>
@@ -301,5 +306,96 @@ bool verify(std::span<const uint8_t> pk_bytes, std::span<const uint8_t> msg,
     return false;  // verify never throws (scheme.hpp:277-318 is fail-closed)
   }
 }
+
+// ---- several GPUs of one box ------------------------------------------------------------
+// The path has no exchange step: a batch is cut into contiguous ranges lo = n*g/G,
+// hi = n*(g+1)/G exactly like the reference tool's multi-engine mode
+// (tools/dilithium_cli.cpp:319-339), one Engine and one host thread per device, results
+// land in order.  No collective, no NCCL.  (Listing a device twice gives two contexts on
+// that GPU -- used by the tests, which see a single GPU.)
+class ShardedEngine {
+ public:
+  explicit ShardedEngine(const std::vector<int>& devices) {
+    for (int d : devices) engines_.push_back(std::make_unique<Engine>(d));
+    if (engines_.empty()) throw std::invalid_argument("ShardedEngine: no devices");
+  }
+  size_t size() const { return engines_.size(); }
+
+  template <Params P>
+  std::vector<std::pair<PkBytes<P>, SkBytes<P>>> batch_keygen(std::span<const SeedArray> zetas) {
+    std::vector<std::pair<PkBytes<P>, SkBytes<P>>> out(zetas.size());
+    run(zetas.size(), [&](Engine& e, size_t lo, size_t hi) {
+      auto part = b200::batch_keygen<P>(zetas.subspan(lo, hi - lo), 1, e);
+      std::move(part.begin(), part.end(), out.begin() + lo);
+    });
+    return out;
+  }
+
+  template <Params P>
+  std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const BatchConfig& cfg = {},
+                                      BatchStats* stats = nullptr) {
+    std::vector<SigBytes<P>> out(jobs.size());
+    std::vector<BatchStats> part_stats(engines_.size());
+    std::vector<size_t> los(engines_.size(), 0);
+    run(jobs.size(), [&](Engine& e, size_t lo, size_t hi) {
+      const size_t g = index_of(e);
+      los[g] = lo;
+      auto part = b200::batch_sign<P>(jobs.subspan(lo, hi - lo), cfg, &part_stats[g], e);
+      std::copy(part.begin(), part.end(), out.begin() + lo);
+    });
+    if (stats) {
+      *stats = BatchStats{};
+      for (size_t g = 0; g < engines_.size(); ++g) {
+        const BatchStats& s = part_stats[g];
+        stats->rounds += s.rounds;
+        stats->attempts += s.attempts;
+        stats->speculative += s.speculative;
+        stats->idle_slot_rounds += s.idle_slot_rounds;
+        stats->accepted_attempt_sum += s.accepted_attempt_sum;
+        for (size_t t : s.failed_tasks) stats->failed_tasks.push_back(los[g] + t);
+      }
+    }
+    return out;
+  }
+
+  template <Params P>
+  std::vector<uint8_t> batch_verify(std::span<const VerifyJob<P>> jobs) {
+    std::vector<uint8_t> flags(jobs.size(), 0);
+    run(jobs.size(), [&](Engine& e, size_t lo, size_t hi) {
+      auto part = b200::batch_verify<P>(jobs.subspan(lo, hi - lo), 1, e);
+      std::copy(part.begin(), part.end(), flags.begin() + lo);
+    });
+    return flags;
+  }
+
+ private:
+  size_t index_of(const Engine& e) const {
+    for (size_t g = 0; g < engines_.size(); ++g)
+      if (engines_[g].get() == &e) return g;
+    return 0;
+  }
+  // fork-join over the shards; the first exception is rethrown like WorkerPool::parallel_for
+  template <class Fn>
+  void run(size_t n, Fn&& fn) {
+    const size_t G = engines_.size();
+    std::vector<std::thread> threads;
+    std::vector<std::exception_ptr> errs(G);
+    for (size_t g = 0; g < G; ++g) {
+      const size_t lo = n * g / G, hi = n * (g + 1) / G;
+      if (hi == lo) continue;
+      threads.emplace_back([&, g, lo, hi] {
+        try {
+          fn(*engines_[g], lo, hi);
+        } catch (...) {
+          errs[g] = std::current_exception();
+        }
+      });
+    }
+    for (auto& t : threads) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+  }
+  std::vector<std::unique_ptr<Engine>> engines_;
+};
 
 }  // namespace dilithium::b200

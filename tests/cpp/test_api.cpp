@@ -84,11 +84,45 @@ void level_test(std::mt19937_64& rng) {
   CHECK(keys[3] == keygen<P>(zs[3]));
 }
 
+// several engines over a partitioned batch (the reference tool's multi-engine mode,
+// tools/dilithium_cli.cpp:319-339): same bytes and order as one engine
+template <Params P>
+void sharded_test(std::mt19937_64& rng) {
+  ShardedEngine sh({0, 0, 0});  // three contexts on the one GPU the tests see
+  const size_t n = 301;
+  std::vector<SeedArray> zs(n);
+  for (auto& z : zs) for (auto& b : z) b = static_cast<uint8_t>(rng());
+  auto keys = sh.batch_keygen<P>(std::span<const SeedArray>(zs));
+  auto keys1 = batch_keygen<P>(std::span<const SeedArray>(zs));
+  CHECK(keys == keys1);
+  auto pre = make_precomp<P>(keys[7].second);
+  std::vector<std::vector<uint8_t>> msgs(n);
+  std::vector<SignJob<P>> jobs(n);
+  for (size_t i = 0; i < n; ++i) {
+    msgs[i].resize(rng() % 80);
+    for (auto& b : msgs[i]) b = static_cast<uint8_t>(rng());
+    jobs[i] = {&*pre, msgs[i]};
+  }
+  BatchStats st, st1;
+  auto sigs = sh.batch_sign<P>(std::span<const SignJob<P>>(jobs), {}, &st);
+  auto sigs1 = batch_sign<P>(std::span<const SignJob<P>>(jobs), {}, &st1);
+  CHECK(sigs == sigs1 && st.accepted_attempt_sum == st1.accepted_attempt_sum && st.failed_tasks.empty());
+  std::vector<VerifyJob<P>> vj(n);
+  for (size_t i = 0; i < n; ++i) vj[i] = {keys[7].first, msgs[i], sigs[i]};
+  auto bad = sigs[200];
+  bad[33] ^= 2;
+  vj[200].sig = bad;
+  auto flags = sh.batch_verify<P>(std::span<const VerifyJob<P>>(vj));
+  for (size_t i = 0; i < n; ++i) CHECK(flags[i] == (i == 200 ? 0 : 1));
+}
+
 int main() {
   std::mt19937_64 rng(4242);
   level_test<kDilithium2>(rng);
   level_test<kDilithium3>(rng);
   level_test<kDilithium5>(rng);
+  sharded_test<kDilithium2>(rng);
+  sharded_test<kDilithium5>(rng);
   std::printf(fails ? "api test: %d failures\n" : "api test: all passed\n", fails);
   return fails ? 1 : 0;
 }

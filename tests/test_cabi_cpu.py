@@ -56,7 +56,7 @@ def test_fails_loudly_without_gpu(lib):
 
 def test_cpp_shim_compiles(lib):
     out = "/tmp/dlb_test_api"
-    cmd = ["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"),
+    cmd = ["g++", "-std=c++20", "-O1", "-pthread", "-I" + os.path.join(ROOT, "include"),
            os.path.join(ROOT, "tests", "cpp", "test_api.cpp"), "-o", out,
            "-L" + os.path.join(ROOT, "paper_2211_12265_b200"), "-ldilithium_b200",
            "-Wl,-rpath," + os.path.join(ROOT, "paper_2211_12265_b200")]

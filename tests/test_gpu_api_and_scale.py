@@ -24,7 +24,7 @@ def eng():
 def test_cpp_shim_runs():
     out = "/tmp/dlb_test_api_gpu"
     lib = os.path.join(ROOT, "paper_2211_12265_b200")
-    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"),
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-pthread", "-I" + os.path.join(ROOT, "include"),
                         os.path.join(ROOT, "tests", "cpp", "test_api.cpp"), "-o", out, "-L" + lib,
                         "-ldilithium_b200", "-Wl,-rpath," + lib], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
