@@ -116,3 +116,5 @@ def test_bench_csv():
                         "mean_latency_us,attempts_mean")
     assert [l.split(",")[2] for l in lines[1:]] == ["keygen", "sign", "verify"]
     assert all(l.split(",")[0] == "1" and float(l.split(",")[9]) > 0 for l in lines[1:])
+    rc, out, _ = run("bench", "--level", 3, "--phi", 50, "--streams", 3, "--reps", 1)
+    assert rc == 0 and [l.split(",")[7] for l in out.strip().splitlines()[1:]] == ["3", "3", "3"]

@@ -27,6 +27,7 @@
 #include <fstream>
 #include <iostream>
 #include <map>
+#include <memory>
 #include <random>
 #include <set>
 #include <string>
@@ -398,6 +399,7 @@ int cmd_bench(const Args& a) {
       !a.number("--streams", 1, streams) || !a.number("--reps", 5, reps) || phi == 0 || reps == 0)
     return usage("bench options must be positive numbers");
   if (psi > phi) return usage("--psi must not exceed --phi");
+  if (streams > 64) return usage("--streams must be at most 64");
   return with_level(a, [&](auto lv) {
     constexpr Params P = params_of<decltype(lv)::value>();
     std::mt19937_64 rng(20221112);
@@ -421,8 +423,18 @@ int cmd_bench(const Args& a) {
       std::printf("1,batch-gpu,%s,%d,%zu,%zu,%zu,%zu,%zu,%.1f,%.3f,%s\n", op, P.level, phi, psi, workers,
                   streams, reps, phi / sec, sec / phi * 1e6, attempts.c_str());
     };
-    row("keygen", median_seconds(reps, [&] { batch_keygen<P>(std::span<const SeedArray>(zetas)); }), "");
-    const double ts = median_seconds(reps, [&] { sigs = batch_sign<P>(std::span<const SignJob<P>>(jobs), cfg, &st); });
+    // --streams S: S independent engines over a contiguous task partition (the reference
+    // tool's multi-engine mode, dilithium_cli.cpp:319-339); here S contexts on GPU 0
+    std::unique_ptr<ShardedEngine> sharded;
+    if (streams > 1) sharded = std::make_unique<ShardedEngine>(std::vector<int>(streams, 0));
+    row("keygen", median_seconds(reps, [&] {
+          if (sharded) sharded->batch_keygen<P>(std::span<const SeedArray>(zetas));
+          else batch_keygen<P>(std::span<const SeedArray>(zetas));
+        }), "");
+    const double ts = median_seconds(reps, [&] {
+      sigs = sharded ? sharded->batch_sign<P>(std::span<const SignJob<P>>(jobs), cfg, &st)
+                     : batch_sign<P>(std::span<const SignJob<P>>(jobs), cfg, &st);
+    });
     char att[32];
     std::snprintf(att, sizeof att, "%.3f", double(st.accepted_attempt_sum) / phi);
     row("sign", ts, att);
@@ -430,7 +442,10 @@ int cmd_bench(const Args& a) {
     std::vector<VerifyJob<P>> vj(phi);
     for (size_t i = 0; i < phi; ++i) vj[i] = {pk, msgs[i], sigs[i]};
     std::vector<uint8_t> flags;
-    row("verify", median_seconds(reps, [&] { flags = batch_verify<P>(std::span<const VerifyJob<P>>(vj)); }), "");
+    row("verify", median_seconds(reps, [&] {
+          flags = sharded ? sharded->batch_verify<P>(std::span<const VerifyJob<P>>(vj))
+                          : batch_verify<P>(std::span<const VerifyJob<P>>(vj));
+        }), "");
     for (auto f : flags)
       if (!f) {
         std::cerr << "error: bench produced a signature that does not verify\n";
