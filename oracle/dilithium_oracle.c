@@ -19,17 +19,23 @@
 
 /* ------------------------------------------------------------------ params */
 
-static const orc_params kParams[3] = {
+static const orc_params kParams[6] = {
     /* params.hpp:53 */
-    {2, 4, 4, 2, 39, 78, 1 << 17, (Q - 1) / 88, 80, 3, 18, 6, 1312, 2528, 2420},
+    {2, 4, 4, 2, 39, 78, 1 << 17, (Q - 1) / 88, 80, 3, 18, 6, 1312, 2528, 2420, 0, 32, 32},
     /* params.hpp:54 */
-    {3, 6, 5, 4, 49, 196, 1 << 19, (Q - 1) / 32, 55, 4, 20, 4, 1952, 4000, 3293},
+    {3, 6, 5, 4, 49, 196, 1 << 19, (Q - 1) / 32, 55, 4, 20, 4, 1952, 4000, 3293, 0, 32, 32},
     /* params.hpp:55 */
-    {5, 8, 7, 2, 60, 120, 1 << 19, (Q - 1) / 32, 75, 3, 20, 4, 2592, 4864, 4595},
+    {5, 8, 7, 2, 60, 120, 1 << 19, (Q - 1) / 32, 75, 3, 20, 4, 2592, 4864, 4595, 0, 32, 32},
+    /* FIPS 204 table 1 / table 2 (ML-DSA-44 / 65 / 87): same ring and bounds; tr is 64
+     * bytes, c~ is lambda/4 = 32 / 48 / 64 bytes.  Not part of the reference (its README
+     * declares FIPS 204 a non-goal); restated from the standard, see the header. */
+    {44, 4, 4, 2, 39, 78, 1 << 17, (Q - 1) / 88, 80, 3, 18, 6, 1312, 2560, 2420, 1, 64, 32},
+    {65, 6, 5, 4, 49, 196, 1 << 19, (Q - 1) / 32, 55, 4, 20, 4, 1952, 4032, 3309, 1, 64, 48},
+    {87, 8, 7, 2, 60, 120, 1 << 19, (Q - 1) / 32, 75, 3, 20, 4, 2592, 4896, 4627, 1, 64, 64},
 };
 
 const orc_params* orc_get_params(int level) {
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 6; ++i)
     if (kParams[i].level == level) return &kParams[i];
   return NULL;
 }
@@ -220,11 +226,16 @@ void orc_expand_mask(int32_t out[256], const uint8_t rho_prime[64], unsigned non
 
 /* sampling.hpp:97-120: 8 sign bytes (LE, consumed LSB first), then for
  * i = 256-tau..255 draw byte b <= i (reject b > i); c[i] = c[b]; c[b] = +-1. */
+static void sample_in_ball_n(int32_t out[256], const uint8_t* c_tilde, size_t ct_len, int tau);
 void orc_sample_in_ball(int32_t out[256], const uint8_t c_tilde[32], int tau) {
+  sample_in_ball_n(out, c_tilde, 32, tau);
+}
+/* FIPS 204 Alg. 29 absorbs the whole commitment hash (lambda/4 bytes) */
+static void sample_in_ball_n(int32_t out[256], const uint8_t* c_tilde, size_t ct_len, int tau) {
   xof_t x;
   uint8_t sb[8];
   xof_init(&x, 136);
-  xof_absorb(&x, c_tilde, 32);
+  xof_absorb(&x, c_tilde, ct_len);
   xof_squeeze(&x, sb, 8);
   uint64_t signs = 0;
   for (int i = 0; i < 8; ++i) signs |= (uint64_t)sb[i] << (8 * i);
@@ -418,7 +429,7 @@ static int decode_hint(int32_t* h, const uint8_t* in, const orc_params* P) {
 #define LMAX 7
 
 typedef struct {
-  uint8_t rho[32], key[32], tr[32];
+  uint8_t rho[32], key[32], tr[64];
   int32_t s1[LMAX][N], s2[KMAX][N], t0[KMAX][N];
 } sk_view;
 
@@ -426,8 +437,8 @@ typedef struct {
 static int unpack_sk(sk_view* v, const uint8_t* sk, const orc_params* P) {
   memcpy(v->rho, sk, 32);
   memcpy(v->key, sk + 32, 32);
-  memcpy(v->tr, sk + 64, 32);
-  size_t off = 96, eb = (size_t)N * P->eta_bits / 8;
+  memcpy(v->tr, sk + 64, (size_t)P->tr_bytes);
+  size_t off = 64 + (size_t)P->tr_bytes, eb = (size_t)N * P->eta_bits / 8;
   int ok = 1;
   for (int i = 0; i < P->l; ++i, off += eb)
     for (int m = 0; m < N; ++m) {
@@ -465,7 +476,12 @@ int orc_keygen(int level, const uint8_t zeta[32], uint8_t* pk, uint8_t* sk) {
   const orc_params* P = orc_get_params(level);
   if (!P) return -1;
   uint8_t seed[128];
-  orc_shake256(seed, 128, zeta, 32);
+  if (P->mldsa) { /* FIPS 204 Alg. 6 line 1: H(xi || k || l, 128) */
+    const uint8_t kl[2] = {(uint8_t)P->k, (uint8_t)P->l};
+    hash2(seed, 128, zeta, 32, kl, 2);
+  } else {
+    orc_shake256(seed, 128, zeta, 32);
+  }
   const uint8_t *rho = seed, *rho_prime = seed + 32, *key = seed + 96; /* scheme.hpp:70-76 */
   static _Thread_local int32_t s1[LMAX][N], s2[KMAX][N], s1h[LMAX][N], t[KMAX][N], t1[KMAX][N],
       t0[KMAX][N];
@@ -485,12 +501,12 @@ int orc_keygen(int level, const uint8_t zeta[32], uint8_t* pk, uint8_t* sk) {
   }
   memcpy(pk, rho, 32);
   for (int i = 0; i < P->k; ++i) pack_t1(pk + 32 + 320 * i, t1[i]);
-  uint8_t tr[32];
-  orc_shake256(tr, 32, pk, P->pk_bytes); /* scheme.hpp:102 */
+  uint8_t tr[64];
+  orc_shake256(tr, (size_t)P->tr_bytes, pk, P->pk_bytes); /* scheme.hpp:102 */
   memcpy(sk, rho, 32);
   memcpy(sk + 32, key, 32);
-  memcpy(sk + 64, tr, 32);
-  size_t off = 96, eb = (size_t)N * P->eta_bits / 8;
+  memcpy(sk + 64, tr, (size_t)P->tr_bytes);
+  size_t off = 64 + (size_t)P->tr_bytes, eb = (size_t)N * P->eta_bits / 8;
   for (int i = 0; i < P->l; ++i, off += eb) pack_eta(sk + off, s1[i], P);
   for (int i = 0; i < P->k; ++i, off += eb) pack_eta(sk + off, s2[i], P);
   for (int i = 0; i < P->k; ++i, off += 416) pack_t0(sk + off, t0[i]);
@@ -529,7 +545,7 @@ static void mul_c(int32_t out[N], const int32_t chat[N], const int32_t shat[N]) 
 
 /* scheme.hpp:133-219 with the production bounds of :225-230 */
 static int attempt(const precomp* pre, const orc_params* P, const uint8_t mu[64],
-                   const uint8_t rho_prime[64], uint32_t kappa, int* stage, uint8_t c_tilde[32],
+                   const uint8_t rho_prime[64], uint32_t kappa, int* stage, uint8_t* c_tilde,
                    int32_t z[][N], int32_t hints[][N]) {
   static _Thread_local int32_t y[LMAX][N], yh[LMAX][N], w[KMAX][N], w1[KMAX][N], wcs2[KMAX][N],
       vt[KMAX][N];
@@ -548,8 +564,8 @@ static int attempt(const precomp* pre, const orc_params* P, const uint8_t mu[64]
     for (int m = 0; m < N; ++m) w1[i][m] = highbits(w[i][m], P->gamma2);
     pack_w1(hin + 64 + w1b * i, w1[i], P);
   }
-  orc_shake256(c_tilde, 32, hin, 64 + w1b * P->k); /* scheme.hpp:158-163 */
-  orc_sample_in_ball(c, c_tilde, P->tau);
+  orc_shake256(c_tilde, (size_t)P->ct_bytes, hin, 64 + w1b * P->k); /* scheme.hpp:158-163 */
+  sample_in_ball_n(c, c_tilde, (size_t)P->ct_bytes, P->tau);
   for (int m = 0; m < N; ++m) chat[m] = modq(c[m]);
   orc_ntt(chat);
 
@@ -597,7 +613,7 @@ static int attempt(const precomp* pre, const orc_params* P, const uint8_t mu[64]
 
 int orc_sign_attempt(int level, const uint8_t* sk, const uint8_t mu[64],
                      const uint8_t rho_prime[64], uint32_t kappa, int* stage,
-                     uint8_t c_tilde[32], int32_t* z, int32_t* hints) {
+                     uint8_t* c_tilde, int32_t* z, int32_t* hints) {
   const orc_params* P = orc_get_params(level);
   if (!P) return -1;
   precomp* pre = malloc(sizeof *pre);
@@ -628,18 +644,33 @@ int orc_sign(int level, const uint8_t* sk, const uint8_t* msg, size_t msglen,
     free(pre);
     return -1;
   }
-  uint8_t mu[64], rho_prime[64], c_tilde[32];
-  hash2(mu, 64, pre->v.tr, 32, msg, msglen);                       /* scheme.hpp:240-243 */
+  uint8_t mu[64], rho_prime[64], c_tilde[64];
+  if (P->mldsa) {
+    /* FIPS 204 Alg. 2 / 7 with an empty context string, deterministic variant:
+     * M' = 0 || 0 || M, mu = H(tr || M', 64), rho'' = H(K || rnd || mu, 64), rnd = 0^32 */
+    xof_t x;
+    const uint8_t pfx[2] = {0, 0};
+    xof_init(&x, 136);
+    xof_absorb(&x, pre->v.tr, 64);
+    xof_absorb(&x, pfx, 2);
+    xof_absorb(&x, msg, msglen);
+    xof_squeeze(&x, mu, 64);
+    uint8_t krnd[64] = {0};
+    memcpy(krnd, pre->v.key, 32);
+    hash2(rho_prime, 64, krnd, 64, mu, 64);
+  } else {
+    hash2(mu, 64, pre->v.tr, 32, msg, msglen);        /* scheme.hpp:240-243 */
+    hash2(rho_prime, 64, pre->v.key, 32, mu, 64);     /* scheme.hpp:245-248 */
+  }
   if (rho_prime_override) memcpy(rho_prime, rho_prime_override, 64); /* scheme.hpp:257-258 */
-  else hash2(rho_prime, 64, pre->v.key, 32, mu, 64);                /* scheme.hpp:245-248 */
   int32_t(*z)[N] = calloc(LMAX, sizeof *z);
   int32_t(*h)[N] = calloc(KMAX, sizeof *h);
   int rc = -2;
   for (uint32_t a = 0; a < (1u << 14); ++a) { /* scheme.hpp:238,259 */
     int st;
     if (attempt(pre, P, mu, rho_prime, a * (uint32_t)P->l, &st, c_tilde, z, h)) {
-      memcpy(sig, c_tilde, 32); /* packing.hpp:236-254 */
-      size_t off = 32, zb = (size_t)N * P->z_bits / 8;
+      memcpy(sig, c_tilde, (size_t)P->ct_bytes); /* packing.hpp:236-254 */
+      size_t off = (size_t)P->ct_bytes, zb = (size_t)N * P->z_bits / 8;
       for (int j = 0; j < P->l; ++j, off += zb) pack_z(sig + off, z[j], P);
       encode_hint(sig + off, &h[0][0], P);
       if (attempts) *attempts = a + 1;
@@ -663,17 +694,27 @@ int orc_verify(int level, const uint8_t* pk, size_t pklen, const uint8_t* msg, s
   size_t zb = (size_t)N * P->z_bits / 8;
   for (int j = 0; j < P->l; ++j)
     for (int m = 0; m < N; ++m)
-      z[j][m] = P->gamma1 - (int32_t)get_bits(sig + 32 + zb * j, m, P->z_bits);
-  if (!decode_hint(&h[0][0], sig + 32 + zb * P->l, P)) return 0;
+      z[j][m] = P->gamma1 - (int32_t)get_bits(sig + P->ct_bytes + zb * j, m, P->z_bits);
+  if (!decode_hint(&h[0][0], sig + P->ct_bytes + zb * P->l, P)) return 0;
   for (int j = 0; j < P->l; ++j)
     if (norm_ge(z[j], P->gamma1 - P->beta)) return 0; /* scheme.hpp:284 */
 
-  uint8_t tr[32], mu[64];
-  orc_shake256(tr, 32, pk, pklen);
-  hash2(mu, 64, tr, 32, msg, msglen);
+  uint8_t tr[64], mu[64];
+  orc_shake256(tr, (size_t)P->tr_bytes, pk, pklen);
+  if (P->mldsa) { /* FIPS 204 Alg. 3 / 8, empty context: mu = H(tr || 0 || 0 || M, 64) */
+    xof_t x;
+    const uint8_t pfx[2] = {0, 0};
+    xof_init(&x, 136);
+    xof_absorb(&x, tr, 64);
+    xof_absorb(&x, pfx, 2);
+    xof_absorb(&x, msg, msglen);
+    xof_squeeze(&x, mu, 64);
+  } else {
+    hash2(mu, 64, tr, 32, msg, msglen);
+  }
 
   int32_t c[N], chat[N], t1h[N];
-  orc_sample_in_ball(c, sig, P->tau);
+  sample_in_ball_n(c, sig, (size_t)P->ct_bytes, P->tau);
   for (int m = 0; m < N; ++m) chat[m] = modq(c[m]);
   orc_ntt(chat);
   for (int j = 0; j < P->l; ++j) {
@@ -693,7 +734,7 @@ int orc_verify(int level, const uint8_t* pk, size_t pklen, const uint8_t* msg, s
     for (int m = 0; m < N; ++m) w1[i][m] = orc_use_hint(h[i][m], acc[i][m], P->gamma2);
     pack_w1(hin + 64 + w1b * i, w1[i], P);
   }
-  uint8_t expect[32];
-  orc_shake256(expect, 32, hin, 64 + w1b * P->k);
-  return memcmp(expect, sig, 32) == 0;
+  uint8_t expect[64];
+  orc_shake256(expect, (size_t)P->ct_bytes, hin, 64 + w1b * P->k);
+  return memcmp(expect, sig, (size_t)P->ct_bytes) == 0;
 }

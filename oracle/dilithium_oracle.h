@@ -29,9 +29,16 @@ typedef struct {
   int level, k, l, eta, tau, beta, gamma1, gamma2, omega;
   int eta_bits, z_bits, w1_bits;
   size_t pk_bytes, sk_bytes, sig_bytes;
+  int mldsa;              /* 1 = FIPS 204 hashing conventions (levels 44 / 65 / 87) */
+  int tr_bytes, ct_bytes; /* 32, 32 for round 3; 64 and lambda/4 for FIPS 204 */
 } orc_params;
 
-/* level in {2,3,5}; returns NULL otherwise (params.hpp:53-55,91-106) */
+/* level in {2,3,5} (the reference's round-3 parameter sets; params.hpp:53-55,91-106) or
+ * {44,65,87} (ML-DSA-44/65/87, FIPS 204 -- NOT in the reference, which declares it a
+ * non-goal: restated from the standard, keygen and verify pinned against OpenSSL 4.0 through
+ * the fixtures of tests/golden/make_mldsa_golden.py; deterministic signing with an empty
+ * context only, its signature bytes are cross-verified but have no independent KAT);
+ * returns NULL otherwise */
 const orc_params* orc_get_params(int level);
 
 /* keccak.hpp:70-93 */
@@ -70,10 +77,11 @@ int orc_verify(int level, const uint8_t* pk, size_t pklen, const uint8_t* msg, s
 
 /* scheme.hpp:133-219 one rejection-loop iteration.  Returns 1 accepted, 0 rejected;
  * *stage = 0 ZNorm, 1 R0Norm, 2 VtNorm, 3 HintWeight when rejected.  z (l*256,
- * centered) and hints (k*256) are filled as far as the reference computes them. */
+ * centered) and hints (k*256) are filled as far as the reference computes them.
+ * c_tilde: ct_bytes (32; up to 64 for the FIPS 204 levels). */
 int orc_sign_attempt(int level, const uint8_t* sk, const uint8_t mu[64],
                      const uint8_t rho_prime[64], uint32_t kappa, int* stage,
-                     uint8_t c_tilde[32], int32_t* z, int32_t* hints);
+                     uint8_t* c_tilde, int32_t* z, int32_t* hints);
 
 #ifdef __cplusplus
 }

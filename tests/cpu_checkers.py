@@ -25,6 +25,12 @@ PARAMS = {
     5: dict(k=8, l=7, eta=2, tau=60, beta=120, gamma1=1 << 19, gamma2=(8380417 - 1) // 32,
             omega=75, eta_bits=3, z_bits=20, w1_bits=4, pk=2592, sk=4864, sig=4595),
 }
+# FIPS 204 parameter sets (ML-DSA-44 / 65 / 87): same ring and bounds, 64-byte tr,
+# lambda/4-byte commitment hash (oracle only: the compiled reference has no FIPS 204)
+for _lv, _base, _sk, _sig, _ct in ((44, 2, 2560, 2420, 32), (65, 3, 4032, 3309, 48), (87, 5, 4896, 4627, 64)):
+    PARAMS[_lv] = dict(PARAMS[_base], sk=_sk, sig=_sig, ct=_ct)
+for _lv in (2, 3, 5):
+    PARAMS[_lv]["ct"] = 32
 Q = 8380417
 
 _u8p = C.POINTER(C.c_uint8)
@@ -210,7 +216,7 @@ class _Checker:
         P = PARAMS[level]
         z = np.zeros((P["l"], 256), np.int32)
         h = np.zeros((P["k"], 256), np.int32)
-        ct = np.zeros(32, np.uint8)
+        ct = np.zeros(P["ct"], np.uint8)
         st = C.c_int(0)
         i32p = C.POINTER(C.c_int32)
         rc = self._sign_attempt(level, _p(bytes(sk)), _p(bytes(mu)), _p(bytes(rho_prime)), kappa,

@@ -8,6 +8,7 @@ Three anchors, per the parity contract:
   * the reference compiled in place (oracle/_ref) on fresh random inputs
 """
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -178,3 +179,32 @@ def test_malformed_sk(oracle, ref):
         oracle.sign(2, bytes(bad), b"m")
     with pytest.raises(ValueError):
         ref.sign(2, bytes(bad), b"m")
+
+
+# ---- FIPS 204 (ML-DSA-44 / 65 / 87) mode of the oracle -----------------------------------
+# Not in the reference (proj/README.md:120-121 declares it a non-goal): pinned against
+# OpenSSL through the fixtures written by tests/golden/make_mldsa_golden.py.
+
+@pytest.fixture(scope="module")
+def mldsa_golden():
+    import json
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "mldsa_openssl.json")))
+
+
+@pytest.mark.parametrize("level", [44, 65, 87])
+def test_mldsa_oracle_against_openssl_vectors(oracle, mldsa_golden, level):
+    for case in mldsa_golden["levels"][str(level)]:
+        seed, pk = bytes.fromhex(case["seed"]), bytes.fromhex(case["pk"])
+        opk, osk = oracle.keygen(level, seed)
+        assert opk == pk and len(osk) == case["sk_sha_len"]  # OpenSSL's public key for this seed
+        for s in case["sigs"]:
+            msg = bytes.fromhex(s["msg"])
+            theirs = bytes.fromhex(s["openssl_sig"])
+            assert oracle.verify(level, pk, msg, theirs) == 1          # OpenSSL's signature verifies
+            assert oracle.verify(level, pk, msg + b"x", theirs) == 0
+            flipped = bytearray(theirs)
+            flipped[len(flipped) // 3] ^= 4
+            assert oracle.verify(level, pk, msg, bytes(flipped)) == 0
+            ours, att = oracle.sign(level, osk, msg)                    # OpenSSL accepted these bytes
+            assert ours.hex() == s["oracle_sig"] and att == s["oracle_attempts"]
+            assert oracle.verify(level, pk, msg, ours) == 1
