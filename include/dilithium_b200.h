@@ -11,6 +11,13 @@
  * level is 2, 3 or 5 (params.hpp:53-55; runtime dispatch as with_params, params.hpp:91-106).
  * Byte sizes per level: pk 1312/1952/2592, sk 2528/4000/4864, sig 2420/3293/4595.
  *
+ * level 44, 65 or 87 selects ML-DSA-44/65/87 (FIPS 204) on the same engine: the standard's
+ * hashing conventions (H(xi||k||l), 64-byte tr, M' = 0||0||M i.e. the empty context string,
+ * rho'' = H(K||0^32||mu) i.e. the deterministic variant, lambda/4-byte commitment hash).
+ * Sizes: pk 1312/1952/2592, sk 2560/4032/4896, sig 2420/3309/4627.  Not part of the
+ * reference (proj/README.md:120-121); pinned against OpenSSL, see oracle/dilithium_oracle.h.
+ * rho_prime_override, where given, replaces rho'' (hedged signing: pass 64 fresh random bytes).
+ *
  * Status codes: 0 ok; DLB_E_ARG bad argument; DLB_E_LEVEL unsupported level;
  * DLB_E_KEY malformed secret key (packing.hpp:79-86,215-233 -- the C++ shim turns this
  * into std::invalid_argument / nullopt); <= -1000: -(1000 + cudaError_t).

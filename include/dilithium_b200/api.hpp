@@ -45,15 +45,24 @@ struct Params {
   size_t k, l;
   int eta;
   size_t eta_bits, z_bits, omega;
+  size_t tr_bytes = 32, ctilde_bytes = 32;  // 64 and lambda/4 for the FIPS 204 sets
   constexpr size_t pk_bytes() const { return 32 + k * 320; }
-  constexpr size_t sk_bytes() const { return 96 + (k + l) * 32 * eta_bits + k * 416; }
-  constexpr size_t sig_bytes() const { return 32 + l * 32 * z_bits + omega + k; }
+  constexpr size_t sk_bytes() const { return 64 + tr_bytes + (k + l) * 32 * eta_bits + k * 416; }
+  constexpr size_t sig_bytes() const { return ctilde_bytes + l * 32 * z_bits + omega + k; }
   friend constexpr bool operator==(const Params&, const Params&) = default;
 };
 
 inline constexpr Params kDilithium2{2, 4, 4, 2, 3, 18, 80};
 inline constexpr Params kDilithium3{3, 6, 5, 4, 4, 20, 55};
 inline constexpr Params kDilithium5{5, 8, 7, 2, 3, 20, 75};
+// FIPS 204 parameter sets (not in the reference, which declares them a non-goal): the same
+// engine with the standard's hashing conventions; deterministic signing, empty context.
+inline constexpr Params kMLDSA44{44, 4, 4, 2, 3, 18, 80, 64, 32};
+inline constexpr Params kMLDSA65{65, 6, 5, 4, 4, 20, 55, 64, 48};
+inline constexpr Params kMLDSA87{87, 8, 7, 2, 3, 20, 75, 64, 64};
+static_assert(kMLDSA44.sk_bytes() == 2560 && kMLDSA44.sig_bytes() == 2420);
+static_assert(kMLDSA65.sk_bytes() == 4032 && kMLDSA65.sig_bytes() == 3309);
+static_assert(kMLDSA87.sk_bytes() == 4896 && kMLDSA87.sig_bytes() == 4627);
 static_assert(kDilithium2.pk_bytes() == 1312 && kDilithium2.sk_bytes() == 2528 && kDilithium2.sig_bytes() == 2420);
 static_assert(kDilithium3.pk_bytes() == 1952 && kDilithium3.sk_bytes() == 4000 && kDilithium3.sig_bytes() == 3293);
 static_assert(kDilithium5.pk_bytes() == 2592 && kDilithium5.sk_bytes() == 4864 && kDilithium5.sig_bytes() == 4595);
@@ -93,7 +102,8 @@ inline void check(int rc, const char* what) {
 template <Params P>
 struct SignPrecomp {
   SkBytes<P> sk{};
-  SeedArray rho{}, key{}, tr{};
+  SeedArray rho{}, key{};
+  std::array<uint8_t, P.tr_bytes> tr{};
 };
 
 // scheme.hpp:106-125 + the eta range check of packing.hpp:79-86
@@ -103,7 +113,7 @@ std::optional<SignPrecomp<P>> make_precomp(std::span<const uint8_t> sk_bytes) {
   const size_t n_eta = (P.k + P.l) * 256;
   uint64_t acc = 0;
   unsigned nbits = 0;
-  size_t seen = 0, pos = 96;
+  size_t seen = 0, pos = 64 + P.tr_bytes;
   while (seen < n_eta) {
     acc |= static_cast<uint64_t>(sk_bytes[pos++]) << nbits;
     nbits += 8;
@@ -118,7 +128,7 @@ std::optional<SignPrecomp<P>> make_precomp(std::span<const uint8_t> sk_bytes) {
   std::memcpy(pre.sk.data(), sk_bytes.data(), P.sk_bytes());
   std::memcpy(pre.rho.data(), sk_bytes.data(), 32);
   std::memcpy(pre.key.data(), sk_bytes.data() + 32, 32);
-  std::memcpy(pre.tr.data(), sk_bytes.data() + 64, 32);
+  std::memcpy(pre.tr.data(), sk_bytes.data() + 64, P.tr_bytes);
   return pre;
 }
 

@@ -38,6 +38,32 @@ struct Params<5> {
                        GAMMA2 = (kQ - 1) / 32, OMEGA = 75, ETA_BITS = 3, Z_BITS = 20,
                        W1_BITS = 4;
 };
+// FIPS 204 (ML-DSA-44 / 65 / 87): the ring, samplers, bounds and codecs of the round-3 sets;
+// what differs is hashing only -- H(xi || k || l) in key generation, a 64-byte tr, the
+// message prefix 0 || |ctx| || ctx, rho'' = H(K || rnd || mu), and a commitment hash of
+// lambda/4 = 32 / 48 / 64 bytes that SampleInBall absorbs whole (FIPS 204 Alg. 6-8, 29).
+// Selected through the flags below; the round-3 instantiations compile to the same code as
+// before.  Deterministic signing (rnd = 0) with an empty context string.
+template <>
+struct Params<44> : Params<2> {
+  static constexpr int LEVEL = 44;
+};
+template <>
+struct Params<65> : Params<3> {
+  static constexpr int LEVEL = 65;
+};
+template <>
+struct Params<87> : Params<5> {
+  static constexpr int LEVEL = 87;
+};
+
+template <class P>
+struct Hashing {
+  static constexpr bool MLDSA = P::LEVEL > 5;
+  static constexpr int TR = MLDSA ? 64 : 32;                                      // bytes of tr
+  static constexpr int CT = P::LEVEL == 65 ? 48 : (P::LEVEL == 87 ? 64 : 32);     // bytes of c~
+  static constexpr int TRW = TR / 8, CTW = CT / 8;                                // 64-bit words
+};
 
 // derived wire sizes (params.hpp:36-50)
 template <class P>
@@ -47,12 +73,13 @@ struct Sizes {
   static constexpr int W1_POLY = kN * P::W1_BITS / 8;
   static constexpr int T1_POLY = 320, T0_POLY = 416;
   static constexpr int PK = 32 + P::K * T1_POLY;
-  static constexpr int SK = 96 + (P::K + P::L) * ETA_POLY + P::K * T0_POLY;
-  static constexpr int HINT = P::OMEGA + P::K;
-  static constexpr int SIG = 32 + P::L * Z_POLY + HINT;
-  static constexpr int W1_ALL = P::K * W1_POLY;
-  static constexpr int SK_S1 = 96, SK_S2 = SK_S1 + P::L * ETA_POLY,
+  static constexpr int SK_S1 = 64 + Hashing<P>::TR, SK_S2 = SK_S1 + P::L * ETA_POLY,
                        SK_T0 = SK_S2 + P::K * ETA_POLY;
+  static constexpr int SK = SK_T0 + P::K * T0_POLY;
+  static constexpr int HINT = P::OMEGA + P::K;
+  static constexpr int SIG_Z = Hashing<P>::CT;  // offset of z behind the commitment hash
+  static constexpr int SIG = SIG_Z + P::L * Z_POLY + HINT;
+  static constexpr int W1_ALL = P::K * W1_POLY;
 };
 static_assert(Sizes<Params<2>>::PK == 1312 && Sizes<Params<2>>::SK == 2528 &&
               Sizes<Params<2>>::SIG == 2420, "level 2 sizes");
@@ -60,6 +87,12 @@ static_assert(Sizes<Params<3>>::PK == 1952 && Sizes<Params<3>>::SK == 4000 &&
               Sizes<Params<3>>::SIG == 3293, "level 3 sizes");
 static_assert(Sizes<Params<5>>::PK == 2592 && Sizes<Params<5>>::SK == 4864 &&
               Sizes<Params<5>>::SIG == 4595, "level 5 sizes");
+static_assert(Sizes<Params<44>>::PK == 1312 && Sizes<Params<44>>::SK == 2560 &&
+              Sizes<Params<44>>::SIG == 2420, "ML-DSA-44 sizes (FIPS 204 table 2)");
+static_assert(Sizes<Params<65>>::PK == 1952 && Sizes<Params<65>>::SK == 4032 &&
+              Sizes<Params<65>>::SIG == 3309, "ML-DSA-65 sizes");
+static_assert(Sizes<Params<87>>::PK == 2592 && Sizes<Params<87>>::SK == 4896 &&
+              Sizes<Params<87>>::SIG == 4627, "ML-DSA-87 sizes");
 
 // ---- Montgomery arithmetic, R = 2^32 (values as reduce.hpp:44-51) ---------------
 

@@ -14,6 +14,9 @@ int with_level(int level, Fn&& fn) {
     case 2: return fn(Params<2>{});
     case 3: return fn(Params<3>{});
     case 5: return fn(Params<5>{});
+    case 44: return fn(Params<44>{});  // ML-DSA-44 / 65 / 87 (FIPS 204)
+    case 65: return fn(Params<65>{});
+    case 87: return fn(Params<87>{});
     default: return DLB_E_LEVEL;
   }
 }
@@ -660,10 +663,11 @@ int dlb_dbg_sample_in_ball(dlb_ctx* c, int level, size_t n, const uint8_t* c_til
     using P = decltype(p);
     uint8_t* dc;
     int8_t* dout;
-    DLB_TRY(dalloc(c, "dbg.a", n * 32, &dc));
+    constexpr size_t CT = Hashing<P>::CT;  // 32 bytes, or lambda/4 at the FIPS 204 levels
+    DLB_TRY(dalloc(c, "dbg.a", n * CT, &dc));
     DLB_TRY(dalloc(c, "dbg.b", n * kN, &dout));
-    DLB_TRY(h2d(c, dc, c_tildes, n * 32));
-    k_sample_in_ball<P, 4><<<cdiv(n, 128), 128, 0, c->s()>>>(dc, 32, (unsigned)n, dout);
+    DLB_TRY(h2d(c, dc, c_tildes, n * CT));
+    k_sample_in_ball<P, 4><<<cdiv(n, 128), 128, 0, c->s()>>>(dc, CT, (unsigned)n, dout);
     DLB_LAUNCH_CHECK();
     DLB_TRY(d2h(c, out, dout, n * kN));
     return sync(c);

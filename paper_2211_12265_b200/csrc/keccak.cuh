@@ -116,15 +116,25 @@ __device__ __forceinline__ uint64_t padded_word(const uint8_t* p, size_t len, si
 
 // Absorb an arbitrary-length message (prefix words already XORed by the caller are
 // expressed through `pre`/`pre_words`: the first pre_words 64-bit words of the
-// message come from registers, the rest from global memory at msg[0..msg_len)).
+// message come from registers, then GAP zero bytes (FIPS 204's 0 || |ctx| prefix with an
+// empty context), the rest from global memory at msg[0..msg_len)).
 // Leaves the sponge finalized and permuted once: s holds the first squeeze block.
-template <int RATE_WORDS, int PRE_WORDS>
+template <int RATE_WORDS, int PRE_WORDS, int GAP = 0>
 __device__ __forceinline__ void shake_absorb_pre(uint64_t (&s)[25], const uint64_t (&pre)[PRE_WORDS],
                                                  const uint8_t* msg, size_t msg_len) {
   static_assert(PRE_WORDS < RATE_WORDS, "prefix must fit the first block");
+  static_assert(GAP >= 0 && GAP < 8, "gap is shorter than a word");
   keccak_clear(s);
-  const size_t total = (size_t)PRE_WORDS * 8 + msg_len;
+  // the tail behind the register prefix is the virtual message  0^GAP || msg
+  const size_t tail_len = (size_t)GAP + msg_len;
+  const size_t total = (size_t)PRE_WORDS * 8 + tail_len;
   const size_t nblocks = total / (RATE_WORDS * 8) + 1;  // padding always adds a byte
+  auto tail_word = [&](size_t off) -> uint64_t {  // 8 bytes of the padded tail at `off`
+    if (GAP == 0) return padded_word(msg, msg_len, off);
+    if (off >= (size_t)GAP) return padded_word(msg, msg_len, off - GAP);
+    // off == 0: GAP zero bytes, then the first 8 - GAP bytes of the padded message
+    return padded_word(msg, msg_len, 0) << (8 * GAP);
+  };
 #pragma unroll 1
   for (size_t blk = 0; blk < nblocks; ++blk) {
     const size_t base = blk * RATE_WORDS * 8;
@@ -132,9 +142,9 @@ __device__ __forceinline__ void shake_absorb_pre(uint64_t (&s)[25], const uint64
     for (int w = 0; w < RATE_WORDS; ++w) {
       uint64_t v;
       if (w < PRE_WORDS) {
-        v = blk == 0 ? pre[w] : padded_word(msg, msg_len, base + 8 * w - PRE_WORDS * 8);
+        v = blk == 0 ? pre[w] : tail_word(base + 8 * w - PRE_WORDS * 8);
       } else {
-        v = padded_word(msg, msg_len, base + 8 * w - PRE_WORDS * 8);
+        v = tail_word(base + 8 * w - PRE_WORDS * 8);
       }
       s[w] ^= v;
     }

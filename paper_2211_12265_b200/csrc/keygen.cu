@@ -55,13 +55,16 @@ int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uin
     const uint8_t* seedb = reinterpret_cast<const uint8_t*>(seeds[b]);
     uint8_t* pks = d_pks + lo * S::PK;
     uint8_t* sks = d_sks + lo * S::SK;
-    k_keygen_seed<<<cdiv(cnt, 128), 128, 0, st>>>(d_zetas + lo * 32, (unsigned)cnt, seeds[b]);
+    k_keygen_seed<<<cdiv(cnt, 128), 128, 0, st>>>(
+        d_zetas + lo * 32, (unsigned)cnt, seeds[b],
+        Hashing<P>::MLDSA ? ((unsigned)P::K | ((unsigned)P::L << 8) | (1u << 16)) : 0u);
     k_expand_s<P, HW><<<cdiv(cnt * PV, HW * 32), HW * 32, 0, st>>>(seedb + 32, 128,
                                                                     (unsigned)(cnt * PV), s8[b]);
     k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(seedb, 128, (unsigned)(cnt * KL),
                                                                     A[b]);
     k_keygen_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>((unsigned)cnt, seedb, s8[b], A[b], pks, sks);
-    k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, S::PK, S::PK, (unsigned)cnt, sks + 64, S::SK);
+    k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, S::PK, S::PK, (unsigned)cnt, sks + 64, S::SK,
+                                              Hashing<P>::TRW);
     c->launches += 5;
     DLB_LAUNCH_CHECK();
   }
@@ -75,5 +78,8 @@ int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uin
 template int keygen_dev<Params<2>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
 template int keygen_dev<Params<3>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
 template int keygen_dev<Params<5>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
+template int keygen_dev<Params<44>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
+template int keygen_dev<Params<65>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
+template int keygen_dev<Params<87>>(dlb_ctx*, size_t, const uint8_t*, uint8_t*, uint8_t*);
 
 }  // namespace dlb

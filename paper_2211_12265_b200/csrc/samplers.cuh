@@ -185,14 +185,14 @@ __device__ __forceinline__ void expand_mask_stream(const uint64_t* __restrict__ 
 // needs a randomly indexed 256-entry array per stream: a padded int8 row in shared
 // memory.  Squeezed bytes are consumed straight from the state registers (static
 // indices; every lane walks all byte positions under predication).
-template <int TAU>
-__device__ __forceinline__ void sample_in_ball_words(const uint64_t (&ct)[4],
+template <int TAU, int CTW>
+__device__ __forceinline__ void sample_in_ball_words(const uint64_t (&ct)[CTW],
                                                      int8_t* row /* smem, 256 entries */) {
   uint64_t s[25];
   keccak_clear(s);
 #pragma unroll
-  for (int w = 0; w < 4; ++w) s[w] = ct[w];
-  s[4] = 0x1F;
+  for (int w = 0; w < CTW; ++w) s[w] = ct[w];  // 32 bytes (round 3), lambda/4 bytes (FIPS 204)
+  s[CTW] = 0x1F;
   s[16] = 0x8000000000000000ull;
   uint32_t* row32 = reinterpret_cast<uint32_t*>(row);
 #pragma unroll
@@ -227,13 +227,13 @@ __device__ __forceinline__ void sample_in_ball_words(const uint64_t (&ct)[4],
   }
 }
 
-template <int TAU>
+template <int TAU, int CTW>
 __device__ __forceinline__ void sample_in_ball_stream(const uint8_t* __restrict__ c_tilde,
                                                       int8_t* row) {
-  uint64_t ct[4];
+  uint64_t ct[CTW];
 #pragma unroll
-  for (int w = 0; w < 4; ++w) ct[w] = load_u64_unaligned(c_tilde + 8 * w);
-  sample_in_ball_words<TAU>(ct, row);
+  for (int w = 0; w < CTW; ++w) ct[w] = load_u64_unaligned(c_tilde + 8 * w);
+  sample_in_ball_words<TAU, CTW>(ct, row);
 }
 
 template <class P, int WARPS>
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   const unsigned p0 = (blockIdx.x * WARPS + warp) * 32;
   if (p0 >= n) return;
   const unsigned p = min(p0 + lane, n - 1);  // tail lanes redo the last stream (no divergence)
-  sample_in_ball_stream<P::TAU>(ct_base + (size_t)p * ct_stride, stage[warp][lane]);
+  sample_in_ball_stream<P::TAU, Hashing<P>::CTW>(ct_base + (size_t)p * ct_stride, stage[warp][lane]);
   __syncwarp();
 #pragma unroll 1
   for (int src = 0; src < 32; ++src) {
@@ -261,15 +261,16 @@ __global__ void __launch_bounds__(WARPS * 32)
 
 // keygen seed expansion: SHAKE256(zeta, 128) -> rho(32) | rho'(64) | K(32)
 // (scheme.hpp:70-76).  zetas packed 32 bytes per task; out 128 bytes per task.
+// `domain`: 0 for round 3; (k | l << 8) | 1 << 16 for FIPS 204, whose Alg. 6 hashes xi || k || l.
 static __global__ void k_keygen_seed(const uint8_t* __restrict__ zetas, unsigned n,
-                              uint64_t* __restrict__ out) {
+                              uint64_t* __restrict__ out, unsigned domain) {
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   uint64_t s[25];
   keccak_clear(s);
 #pragma unroll
   for (int w = 0; w < 4; ++w) s[w] = load_u64_unaligned(zetas + (size_t)t * 32 + 8 * w);
-  s[4] = 0x1F;
+  s[4] = (domain >> 16) ? ((uint64_t)(domain & 0xFFFF) | ((uint64_t)0x1F << 16)) : 0x1F;
   s[16] = 0x8000000000000000ull;
   keccak_f1600(s);
 #pragma unroll
@@ -277,8 +278,10 @@ static __global__ void k_keygen_seed(const uint8_t* __restrict__ zetas, unsigned
 }
 
 // tr = SHAKE256(pk, 32)  (scheme.hpp:102,287).  One thread per key.
+// tr_words: 4 (32-byte tr, round 3) or 8 (64 bytes, FIPS 204).
 static __global__ void k_hash_tr(const uint8_t* __restrict__ pk, size_t pk_stride, unsigned pk_bytes,
-                          unsigned n, uint8_t* __restrict__ tr_out, size_t tr_stride) {
+                          unsigned n, uint8_t* __restrict__ tr_out, size_t tr_stride,
+                          int tr_words) {
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   uint64_t s[25];
@@ -297,28 +300,33 @@ static __global__ void k_hash_tr(const uint8_t* __restrict__ pk, size_t pk_strid
   }
   uint64_t* o = reinterpret_cast<uint64_t*>(tr_out + (size_t)t * tr_stride);
 #pragma unroll
-  for (int w = 0; w < 4; ++w) o[w] = s[w];
+  for (int w = 0; w < 8; ++w)
+    if (w < tr_words) o[w] = s[w];
 }
 
 // mu = SHAKE256(tr || M, 64) and optionally rho' = SHAKE256(K || mu, 64)
-// (scheme.hpp:240-248).  tr (32 B) and K (32 B) per key, 8-byte aligned; task t uses key
+// (scheme.hpp:240-248).  tr and K (32 B) per key, 8-byte aligned; task t uses key
 // key_idx[t] (key_idx == nullptr: key t), strides 0 = one shared key.
+// MLDSA (FIPS 204 Alg. 2 / 7, empty context, deterministic): tr is 64 bytes,
+// mu = H(tr || 0 || 0 || M, 64) and rho'' = H(K || 0^32 || mu, 64).
+template <bool MLDSA>
 static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_stride,
                           const uint8_t* __restrict__ key_base, size_t key_stride,
                           const uint32_t* __restrict__ key_idx,
                           const uint8_t* __restrict__ msgs, const uint64_t* __restrict__ msg_off,
                           unsigned n, uint64_t* __restrict__ mu_out,
                           uint64_t* __restrict__ rho_prime_out) {
+  constexpr int TRW = MLDSA ? 8 : 4;
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   uint64_t s[25];
-  uint64_t pre[4];
+  uint64_t pre[TRW];
   const size_t kt = key_idx ? (size_t)__ldg(key_idx + t) : (size_t)t;
   const uint64_t* tr = reinterpret_cast<const uint64_t*>(tr_base + kt * tr_stride);
 #pragma unroll
-  for (int w = 0; w < 4; ++w) pre[w] = __ldg(tr + w);
+  for (int w = 0; w < TRW; ++w) pre[w] = __ldg(tr + w);
   const uint64_t m0 = msg_off[t], m1 = msg_off[t + 1];
-  shake_absorb_pre<kWords256, 4>(s, pre, msgs + m0, (size_t)(m1 - m0));
+  shake_absorb_pre<kWords256, TRW, MLDSA ? 2 : 0>(s, pre, msgs + m0, (size_t)(m1 - m0));
   uint64_t mu[8];
 #pragma unroll
   for (int w = 0; w < 8; ++w) {
@@ -330,10 +338,11 @@ static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_
     keccak_clear(s);
 #pragma unroll
     for (int w = 0; w < 4; ++w) s[w] = __ldg(key + w);
+    constexpr int MU0 = MLDSA ? 8 : 4;  // rnd = 0^32 sits between K and mu
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s[4 + w] = mu[w];
-    s[12] = 0x1F;
-    s[16] = 0x8000000000000000ull;
+    for (int w = 0; w < 8; ++w) s[MU0 + w] = mu[w];
+    s[MU0 + 8] = 0x1F;
+    s[16] ^= 0x8000000000000000ull;
     keccak_f1600(s);
 #pragma unroll
     for (int w = 0; w < 8; ++w) rho_prime_out[(size_t)t * 8 + w] = s[w];
@@ -342,9 +351,9 @@ static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_
 
 // c~ = SHAKE256(mu || w1_packed, 32)  (scheme.hpp:158-163,311-317) for one stream:
 // mu 8 words (global, aligned), w1 W1_ALL bytes (global, 8-byte aligned).
-template <int W1_ALL, bool NC = true>
+template <int W1_ALL, bool NC = true, int CTW = 4>
 __device__ __forceinline__ void hash_ctilde_stream(const uint64_t* __restrict__ mu,
-                                                   const uint64_t* w1, uint64_t (&out)[4]) {
+                                                   const uint64_t* w1, uint64_t (&out)[CTW]) {
   static_assert(W1_ALL % 8 == 0, "w1 block is word aligned");
   constexpr int TOTALW = 8 + W1_ALL / 8;          // message words
   constexpr int NBLK = TOTALW / kWords256 + 1;    // incl. the padding block
@@ -365,7 +374,7 @@ __device__ __forceinline__ void hash_ctilde_stream(const uint64_t* __restrict__ 
     keccak_f1600(s);
   }
 #pragma unroll
-  for (int w = 0; w < 4; ++w) out[w] = s[w];
+  for (int w = 0; w < CTW; ++w) out[w] = s[w];
 }
 
 }  // namespace dlb

@@ -396,16 +396,16 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
   if (weight > (unsigned)P::OMEGA) return false;
 
   // accepted: c~ | z | hints into the staging slot
-  if (lane < 8) reinterpret_cast<uint32_t*>(stage_sig)[lane] =
+  if (lane < 2 * Hashing<P>::CTW) reinterpret_cast<uint32_t*>(stage_sig)[lane] =
       reinterpret_cast<const uint32_t*>(ct)[lane];
 #pragma unroll 1
   for (int j = 0; j < P::L; ++j) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) ws.tile[lane + 36 * e] = P::GAMMA1 - ws.vhat[j][e][lane];
     __syncwarp();
-    pack_tile<P::Z_BITS>(ws.tile, pp.ring(pp.k), stage_sig + 32 + j * S::Z_POLY, lane);
+    pack_tile<P::Z_BITS>(ws.tile, pp.ring(pp.k), stage_sig + S::SIG_Z + j * S::Z_POLY, lane);
   }
-  uint8_t* hint = stage_sig + 32 + P::L * S::Z_POLY;
+  uint8_t* hint = stage_sig + S::SIG_Z + P::L * S::Z_POLY;
   // (the padding behind the signature is cleared too: the word-wise commit copy reads it)
   for (int b = lane; b < S::HINT + (SignSizes<P>::SIG_PAD - S::SIG); b += 32) hint[b] = 0;
   __syncwarp();
@@ -424,7 +424,7 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
 }
 
 template <class P>
-__global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 4)
+__global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44) ? DLB_SIGN_MINB : 4)
     k_sign_persistent(SignArgs a) {
   using S = Sizes<P>;
   using Z = SignSizes<P>;
@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
   uint8_t* ybytes = a.ybytes + cta * kSignThreads * Z::Y_SLOT;
   int32_t* wbuf = a.wbuf + cta * kSignThreads * Z::W_SLOT;
   uint8_t* w1buf = a.w1buf + cta * kSignThreads * S::W1_ALL;
-  uint64_t* ctbuf = a.ctbuf + cta * kSignThreads * 4;
+  constexpr int CTW = Hashing<P>::CTW;  // 64-bit words of the commitment hash c~
+  uint64_t* ctbuf = a.ctbuf + cta * kSignThreads * CTW;
   int8_t* c8buf = a.c8buf + cta * kSignThreads * kN;
   uint8_t* staging = a.staging + cta * kSignThreads * Z::SIG_PAD;
 
@@ -565,13 +566,13 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
     // ---- S3: challenge -----------------------------------------------------------
     {
       if (my_task != kNoSlot) {
-        uint64_t ct[4];
-        hash_ctilde_stream<S::W1_ALL, false>(a.mu + (size_t)my_task * 8,
-                                      reinterpret_cast<const uint64_t*>(w1buf + (size_t)tid * S::W1_ALL),
-                                      ct);
+        uint64_t ct[CTW];
+        hash_ctilde_stream<S::W1_ALL, false, CTW>(
+            a.mu + (size_t)my_task * 8,
+            reinterpret_cast<const uint64_t*>(w1buf + (size_t)tid * S::W1_ALL), ct);
 #pragma unroll
-        for (int w = 0; w < 4; ++w) ctbuf[tid * 4 + w] = ct[w];
-        sample_in_ball_words<P::TAU>(ct, sm.u.rows[tid]);
+        for (int w = 0; w < CTW; ++w) ctbuf[tid * CTW + w] = ct[w];
+        sample_in_ball_words<P::TAU, CTW>(ct, sm.u.rows[tid]);
       }
       __syncwarp();
 #pragma unroll 1
@@ -602,7 +603,7 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
         const bool ok = stage_finish<P>(
             sm.u.a.ws[warp], pp, par, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
             wbuf + (size_t)s * Z::W_SLOT, nx < kSignThreads ? c8buf + (size_t)nx * kN : nullptr,
-            ctbuf + s * 4, a.shat + key * ((P::L + 2 * P::K) * kN),
+            ctbuf + s * CTW, a.shat + key * ((P::L + 2 * P::K) * kN),
             staging + (size_t)s * Z::SIG_PAD);
         if (lane == 0) sm.slot_valid[s] = ok ? 1 : 0;
         s = nx;
@@ -629,9 +630,9 @@ __global__ void __launch_bounds__(kSignThreads, P::LEVEL == 2 ? DLB_SIGN_MINB : 
         }
       }
       if (a.dbg_ctilde) {
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(ctbuf + tid * 4);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(a.dbg_ctilde + (size_t)task * 32);
-        for (int w = 0; w < 8; ++w) dst[w] = src[w];
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(ctbuf + tid * CTW);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(a.dbg_ctilde + (size_t)task * Hashing<P>::CT);
+        for (int w = 0; w < 2 * CTW; ++w) dst[w] = src[w];
       }
       if (win >= 0) {
         const unsigned ordinal = sm.slot_attempt[win] + 1;
@@ -747,9 +748,9 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
     mu_use = d_mu_in;  // stage tests supply mu and rho' directly
     rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
   } else {
-    k_hash_mu<<<cdiv(n, 128), 128, 0, st>>>(d_sks + 64, sk_stride, d_sks + 32, sk_stride, d_key_idx,
-                                            d_msgs, d_msg_off, (unsigned)n, mu,
-                                            d_rho_prime ? nullptr : rp);
+    k_hash_mu<Hashing<P>::MLDSA><<<cdiv(n, 128), 128, 0, st>>>(
+        d_sks + 64, sk_stride, d_sks + 32, sk_stride, d_key_idx, d_msgs, d_msg_off, (unsigned)n, mu,
+        d_rho_prime ? nullptr : rp);
     c->launches += 1;
     if (d_rho_prime) rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
   }
@@ -824,7 +825,7 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   DLB_TRY(dalloc(c, "s.y", slots * Z::Y_SLOT + 16, &a.ybytes));
   DLB_TRY(dalloc(c, "s.w", slots * Z::W_SLOT, &a.wbuf));
   DLB_TRY(dalloc(c, "s.w1", slots * S::W1_ALL, &a.w1buf));
-  DLB_TRY(dalloc(c, "s.ct", slots * 4, &a.ctbuf));
+  DLB_TRY(dalloc(c, "s.ct", slots * Hashing<P>::CTW, &a.ctbuf));
   DLB_TRY(dalloc(c, "s.c8", slots * kN, &a.c8buf));
   DLB_TRY(dalloc(c, "s.stage", slots * Z::SIG_PAD, &a.staging));
   a.sigs = d_sigs;
@@ -876,6 +877,9 @@ int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, size_
 DLB_INST(2)
 DLB_INST(3)
 DLB_INST(5)
+DLB_INST(44)
+DLB_INST(65)
+DLB_INST(87)
 
 }  // namespace dlb
 
@@ -904,7 +908,7 @@ extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8
     DLB_TRY(dalloc(c, "io.sig", n * S::SIG + 8, &dsig));
     DLB_TRY(dalloc(c, "io.att", n, &datt));
     DLB_TRY(dalloc(c, "io.fail", n, &dfail));
-    DLB_TRY(dalloc(c, "dbg.d", n * 32, &dct));
+    DLB_TRY(dalloc(c, "dbg.d", n * Hashing<P>::CT, &dct));
     cudaStream_t st = c->s();
     DLB_CUDA_CHECK(cudaMemcpyAsync(dsk, sks, nk * S::SK, cudaMemcpyHostToDevice, st));
     DLB_CUDA_CHECK(cudaMemcpyAsync(dmu, mus, n * 64, cudaMemcpyHostToDevice, st));
@@ -917,7 +921,7 @@ extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8
     uint8_t* hfail = new uint8_t[n];
     cudaMemcpyAsync(hsig, dsig, n * S::SIG, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(hfail, dfail, n, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(c_tilde, dct, n * 32, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(c_tilde, dct, n * Hashing<P>::CT, cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) {
       memset(z, 0, n * P::L * kN * 4);
@@ -931,10 +935,10 @@ extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8
             const size_t bit = (size_t)m * P::Z_BITS;
             uint32_t raw = 0;
             for (int b = 0; b < P::Z_BITS; ++b)
-              raw |= (uint32_t)((sg[32 + j * S::Z_POLY + ((bit + b) >> 3)] >> ((bit + b) & 7)) & 1) << b;
+              raw |= (uint32_t)((sg[S::SIG_Z + j * S::Z_POLY + ((bit + b) >> 3)] >> ((bit + b) & 7)) & 1) << b;
             z[(t * P::L + j) * kN + m] = P::GAMMA1 - (int32_t)raw;
           }
-        const uint8_t* h = sg + 32 + P::L * S::Z_POLY;
+        const uint8_t* h = sg + S::SIG_Z + P::L * S::Z_POLY;
         unsigned prev = 0;
         for (int i = 0; i < P::K; ++i) {
           const unsigned cnt = h[P::OMEGA + i];
@@ -952,6 +956,9 @@ extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8
     case 2: return run(Params<2>{});
     case 3: return run(Params<3>{});
     case 5: return run(Params<5>{});
+    case 44: return run(Params<44>{});
+    case 65: return run(Params<65>{});
+    case 87: return run(Params<87>{});
     default: return DLB_E_LEVEL;
   }
 }

@@ -21,13 +21,14 @@ __global__ void k_verify_final(unsigned n, const uint64_t* __restrict__ mu,
   using S = Sizes<P>;
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  uint64_t ct[4];
-  hash_ctilde_stream<S::W1_ALL>(mu + (size_t)t * 8,
-                                reinterpret_cast<const uint64_t*>(w1buf + (size_t)t * S::W1_ALL), ct);
+  constexpr int CTW = Hashing<P>::CTW;
+  uint64_t ct[CTW];
+  hash_ctilde_stream<S::W1_ALL, true, CTW>(
+      mu + (size_t)t * 8, reinterpret_cast<const uint64_t*>(w1buf + (size_t)t * S::W1_ALL), ct);
   const uint8_t* ts = sig + (size_t)t * sig_stride;
   bool eq = true;
 #pragma unroll
-  for (int w = 0; w < 4; ++w) eq = eq && (load_u64_unaligned(ts + 8 * w) == ct[w]);
+  for (int w = 0; w < CTW; ++w) eq = eq && (load_u64_unaligned(ts + 8 * w) == ct[w]);
   flags[t] = (eq && pre_ok[t]) ? 1 : 0;
 }
 
@@ -75,7 +76,7 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
       tr[1] = tr[0];
     } else {
       DLB_TRY(dalloc(c, nm[b][0], keys_cap * KL * kN, &A[b]));
-      DLB_TRY(dalloc(c, nm[b][1], keys_cap * 32, &tr[b]));
+      DLB_TRY(dalloc(c, nm[b][1], keys_cap * Hashing<P>::TR, &tr[b]));
     }
     DLB_TRY(dalloc(c, nm[b][2], chunk * 8, &mu[b]));
     DLB_TRY(dalloc(c, nm[b][3], chunk * kN, &c8[b]));
@@ -85,7 +86,7 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
   if (const int co = pipeline_carveout(); co >= 0) {
     prefer_carveout(k_expand_a<P, HW>, co);
     prefer_carveout(k_hash_tr, co);
-    prefer_carveout(k_hash_mu, co);
+    prefer_carveout(k_hash_mu<Hashing<P>::MLDSA>, co);
     prefer_carveout(k_sample_in_ball<P, HW>, co);
     prefer_carveout(k_verify_arith<P, 4>, co);
     prefer_carveout(k_verify_final<P>, co);
@@ -93,7 +94,8 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
   if (shared_key) {  // expand once on the caller's stream, before the fork
     k_expand_a<P, HW><<<cdiv(n_keys * KL, HW * 32), HW * 32, 0, main>>>(d_pks, pk_stride,
                                                                         (unsigned)(n_keys * KL), A[0]);
-    k_hash_tr<<<cdiv(n_keys, 128), 128, 0, main>>>(d_pks, pk_stride, S::PK, (unsigned)n_keys, tr[0], 32);
+    k_hash_tr<<<cdiv(n_keys, 128), 128, 0, main>>>(d_pks, pk_stride, S::PK, (unsigned)n_keys, tr[0],
+                                                   Hashing<P>::TR, Hashing<P>::TRW);
     c->launches += 2;
   }
   DLB_CUDA_CHECK(cudaEventRecord(c->ev_fork, main));
@@ -111,11 +113,13 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
     if (!shared_key) {
       k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(pks, pk_stride,
                                                                      (unsigned)(cnt * KL), A[b]);
-      k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, pk_stride, S::PK, (unsigned)cnt, tr[b], 32);
+      k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, pk_stride, S::PK, (unsigned)cnt, tr[b],
+                                                Hashing<P>::TR, Hashing<P>::TRW);
       c->launches += 2;
     }
-    k_hash_mu<<<cdiv(cnt, 128), 128, 0, st>>>(tr[b], key_step * 32, nullptr, 0, kidx, d_msgs,
-                                              d_msg_off + lo, (unsigned)cnt, mu[b], nullptr);
+    k_hash_mu<Hashing<P>::MLDSA><<<cdiv(cnt, 128), 128, 0, st>>>(
+        tr[b], key_step * Hashing<P>::TR, nullptr, 0, kidx, d_msgs, d_msg_off + lo, (unsigned)cnt, mu[b],
+        nullptr);
     k_sample_in_ball<P, HW><<<cdiv(cnt, HW * 32), HW * 32, 0, st>>>(sigs, S::SIG, (unsigned)cnt, c8[b]);
     k_verify_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>(
         (unsigned)cnt, pks, pk_stride, sigs, S::SIG, A[b], key_step * (size_t)KL * kN, kidx, c8[b],
@@ -139,6 +143,9 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
 DLB_INST(2)
 DLB_INST(3)
 DLB_INST(5)
+DLB_INST(44)
+DLB_INST(65)
+DLB_INST(87)
 #undef DLB_INST
 
 }  // namespace dlb

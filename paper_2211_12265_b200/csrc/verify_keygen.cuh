@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 
   // -- strict hint decode into a bitmap (packing.hpp:122-140)
   {
-    const uint8_t* hint = tsig + 32 + P::L * S::Z_POLY;
+    const uint8_t* hint = tsig + S::SIG_Z + P::L * S::Z_POLY;
     unsigned cnt[P::K];
     unsigned prev = 0;
 #pragma unroll
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   // -- z: unpack, infinity-norm check, transform (scheme.hpp:284,291-292)
 #pragma unroll 1
   for (int j = 0; j < P::L; ++j) {
-    const uint8_t* zb = tsig + 32 + j * S::Z_POLY;
+    const uint8_t* zb = tsig + S::SIG_Z + j * S::Z_POLY;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const unsigned c = lane + 32 * i;

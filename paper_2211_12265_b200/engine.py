@@ -9,7 +9,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 # level -> (k, l, pk_bytes, sk_bytes, sig_bytes)   (params.hpp:53-55,77-82)
-LEVELS = {2: (4, 4, 1312, 2528, 2420), 3: (6, 5, 1952, 4000, 3293), 5: (8, 7, 2592, 4864, 4595)}
+LEVELS = {2: (4, 4, 1312, 2528, 2420), 3: (6, 5, 1952, 4000, 3293), 5: (8, 7, 2592, 4864, 4595),
+          # ML-DSA-44 / 65 / 87 (FIPS 204; deterministic signing, empty context string)
+          44: (4, 4, 1312, 2560, 2420), 65: (6, 5, 1952, 4032, 3309), 87: (8, 7, 2592, 4896, 4627)}
 
 _u8p = C.POINTER(C.c_uint8)
 _u64p = C.POINTER(C.c_uint64)
@@ -326,7 +328,7 @@ class Engine:
         n = kap.size
         stride = 0 if sk.ndim == 1 else skb
         acc = np.zeros(n, np.uint8)
-        ct = np.zeros((n, 32), np.uint8)
+        ct = np.zeros((n, {65: 48, 87: 64}.get(level, 32)), np.uint8)  # lambda/4 bytes at the FIPS 204 levels
         z = np.zeros((n, l, 256), np.int32)
         h = np.zeros((n, k, 256), np.int32)
         self._chk(self.lib.dlb_dbg_sign_attempt(self.ctx, level, n, skp, stride, mup, rpp,

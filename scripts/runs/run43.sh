@@ -1,0 +1,2 @@
+cd /root/repo
+timeout 900 python -m pytest tests/test_gpu_mldsa.py -m gpu -x -q 2>&1 | tail -15

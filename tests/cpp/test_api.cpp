@@ -32,7 +32,7 @@ void level_test(std::mt19937_64& rng) {
   CHECK(out.sig == sig && out.attempts >= 1);
   // malformed key
   auto badsk = sk;
-  badsk[96] = 0xFF;
+  badsk[64 + P.tr_bytes] = 0xFF;  // first byte of the packed s1 (behind rho, K, tr)
   CHECK(!make_precomp<P>(badsk).has_value());
   bool threw = false;
   try { sign<P>(badsk, msg); } catch (const std::invalid_argument&) { threw = true; }
@@ -121,6 +121,9 @@ int main() {
   level_test<kDilithium2>(rng);
   level_test<kDilithium3>(rng);
   level_test<kDilithium5>(rng);
+  level_test<kMLDSA44>(rng);  // FIPS 204 parameter sets through the same shim
+  level_test<kMLDSA65>(rng);
+  level_test<kMLDSA87>(rng);
   sharded_test<kDilithium2>(rng);
   sharded_test<kDilithium5>(rng);
   std::printf(fails ? "api test: %d failures\n" : "api test: all passed\n", fails);

@@ -23,7 +23,7 @@ def built():
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools")], check=True)
 
 
-@pytest.mark.parametrize("level", [2, 3, 5])
+@pytest.mark.parametrize("level", [2, 3, 5, 65])  # 65 = ML-DSA-65 (FIPS 204 mode)
 def test_roundtrip(tmp_path, level, oracle):
     pk, sk, sig, msg, msg2 = (tmp_path / n for n in ("pk.bin", "sk.bin", "sig.bin", "msg.bin", "msg2.bin"))
     msg.write_bytes(b"hello dilithium\n")

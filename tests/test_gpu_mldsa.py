@@ -1,0 +1,100 @@
+"""ML-DSA-44 / 65 / 87 (FIPS 204) on the device: levels 44 / 65 / 87 of the same engine.
+Not in the reference; the checker is the oracle's FIPS 204 mode, itself pinned against
+OpenSSL (tests/test_oracle.py::test_mldsa_oracle_against_openssl_vectors), plus OpenSSL's
+own vectors directly (tests/golden/mldsa_openssl.json).  -m gpu."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests.cpu_checkers import PARAMS, mt19937_64
+
+pytestmark = pytest.mark.gpu
+LEVELS = [44, 65, 87]
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_2211_12265_b200 import Engine
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "mldsa_openssl.json")))
+
+
+@pytest.mark.parametrize("level", LEVELS)
+def test_openssl_vectors(eng, golden, level):
+    """OpenSSL's public key for a seed, OpenSSL's signatures verify, the signature bytes
+    OpenSSL accepted at fixture time are reproduced bit for bit."""
+    for case in golden["levels"][str(level)]:
+        seed, pk = bytes.fromhex(case["seed"]), bytes.fromhex(case["pk"])
+        gpk, gsk = eng.keygen(level, seed)
+        assert gpk == pk and len(gsk) == PARAMS[level]["sk"]
+        for s in case["sigs"]:
+            msg = bytes.fromhex(s["msg"])
+            assert eng.verify(level, pk, msg, bytes.fromhex(s["openssl_sig"])) == 1
+            assert eng.verify(level, pk, msg + b"!", bytes.fromhex(s["openssl_sig"])) == 0
+            sig, att = eng.sign(level, gsk, msg)
+            assert sig.hex() == s["oracle_sig"] and att == s["oracle_attempts"]
+
+
+@pytest.mark.parametrize("level", LEVELS)
+def test_batches_match_oracle(eng, oracle, level):
+    n, nk = 400, 5
+    rng = mt19937_64(8800 + level)
+    zetas = np.frombuffer(rng.bytes(32 * nk), np.uint8).reshape(nk, 32)
+    pks, sks = eng.batch_keygen(level, zetas)
+    for i in range(nk):
+        assert (pks[i].tobytes(), sks[i].tobytes()) == oracle.keygen(level, zetas[i].tobytes())
+    lens = [int(rng()) % 300 for _ in range(n)]  # crosses the 136-byte block boundary of mu
+    lens[:6] = [0, 1, 5, 6, 7, 70]               # around the two-byte M' prefix and tr || M' = one block
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    flat = np.frombuffer(rng.bytes(int(off[-1]) + 1), np.uint8)
+    kidx = np.array([int(rng()) % nk for _ in range(n)], np.uint32)
+    sigs, att, failed, _ = eng.batch_sign(level, sks, (flat, off), key_idx=kidx, return_info=True)
+    assert not failed.any()
+    for i in range(n):
+        m = flat[int(off[i]):int(off[i + 1])].tobytes()
+        assert (sigs[i].tobytes(), int(att[i])) == oracle.sign(level, sks[kidx[i]].tobytes(), m), i
+    assert np.array_equal(sigs[:64], eng.batch_sign(level, sks[kidx[:64]], (flat[:int(off[64])], off[:65])))
+    shared = eng.batch_sign(level, sks[0], (flat, off))
+    assert shared[3].tobytes() == oracle.sign(level, sks[0].tobytes(), flat[int(off[3]):int(off[4])].tobytes())[0]
+    assert eng.batch_verify(level, pks, (flat, off), sigs, key_idx=kidx).all()
+    assert eng.batch_verify(level, pks[0], (flat, off), shared).all()
+    bad = sigs.copy()
+    pos = [0, PARAMS[level]["ct"] - 1, PARAMS[level]["ct"], bad.shape[1] - 1, bad.shape[1] // 2]
+    for t, p in enumerate(pos):
+        bad[t, p] ^= 1
+    flags = eng.batch_verify(level, pks, (flat, off), bad, key_idx=kidx)
+    for t in range(n):
+        m = flat[int(off[t]):int(off[t + 1])].tobytes()
+        if t < 32:
+            assert flags[t] == oracle.verify(level, pks[kidx[t]].tobytes(), m, bad[t].tobytes())
+    assert not flags[:len(pos)].any() and flags[len(pos):].all()
+
+
+@pytest.mark.parametrize("level", LEVELS)
+def test_single_attempts_and_malformed_key(eng, oracle, level):
+    rng = mt19937_64(8900 + level)
+    pk, sk = oracle.keygen(level, rng.bytes(32))
+    n = 48
+    mus = np.frombuffer(rng.bytes(64 * n), np.uint8).reshape(n, 64)
+    rps = np.frombuffer(rng.bytes(64 * n), np.uint8).reshape(n, 64)
+    kappas = np.array([int(rng()) % 60000 for _ in range(n)], np.uint32)
+    acc, ct, z, h = eng.dbg_sign_attempt(level, np.frombuffer(sk, np.uint8), mus, rps, kappas)
+    for i in range(n):
+        ok, stage, oct_, oz, oh = oracle.sign_attempt(level, sk, mus[i].tobytes(), rps[i].tobytes(), int(kappas[i]))
+        assert int(acc[i]) == ok
+        assert ct[i].tobytes() == oct_
+        if ok:
+            assert np.array_equal(z[i], oz) and np.array_equal(h[i], oh)
+    bad = bytearray(sk)
+    bad[64 + 64] = 0xFF  # first eta field byte (the secret vectors start behind the 64-byte tr)
+    with pytest.raises(ValueError):
+        eng.sign(level, bytes(bad), b"x")

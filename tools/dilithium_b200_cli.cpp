@@ -140,7 +140,7 @@ const std::map<std::string, Command>& commands() {
 
 int usage(const std::string& why) {
   std::cerr << "error: " << why << "\n"
-            << "usage: dilithium_b200 <keygen|sign|verify|batch-sign|batch-verify|bench> --level {2,3,5} ...\n";
+            << "usage: dilithium_b200 <keygen|sign|verify|batch-sign|batch-verify|bench> --level {2,3,5,44,65,87} ...\n";
   return kBadInput;
 }
 
@@ -181,8 +181,8 @@ bool parse(int argc, char** argv, const Command& cmd, Args& a, std::string& why)
     return false;
   }
   const std::string lv = a.get("--level");
-  if (lv != "2" && lv != "3" && lv != "5") {
-    why = "--level must be 2, 3 or 5";
+  if (lv != "2" && lv != "3" && lv != "5" && lv != "44" && lv != "65" && lv != "87") {
+    why = "--level must be 2, 3 or 5 (Dilithium round 3) or 44, 65 or 87 (ML-DSA, FIPS 204)";
     return false;
   }
   const std::string fmt = a.get("--out-format", "binary");
@@ -195,22 +195,32 @@ bool parse(int argc, char** argv, const Command& cmd, Args& a, std::string& why)
 
 template <class Fn>
 int with_level(const Args& a, Fn&& fn) {
-  switch (a.get("--level")[0]) {
-    case '2': return fn(std::integral_constant<int, 2>{});
-    case '3': return fn(std::integral_constant<int, 3>{});
-    default: return fn(std::integral_constant<int, 5>{});
+  switch (std::stoi(a.get("--level"))) {
+    case 2: return fn(std::integral_constant<int, 2>{});
+    case 3: return fn(std::integral_constant<int, 3>{});
+    case 5: return fn(std::integral_constant<int, 5>{});
+    case 44: return fn(std::integral_constant<int, 44>{});
+    case 65: return fn(std::integral_constant<int, 65>{});
+    default: return fn(std::integral_constant<int, 87>{});
   }
 }
 template <int L>
 constexpr Params params_of() {
-  return L == 2 ? kDilithium2 : (L == 3 ? kDilithium3 : kDilithium5);
+  switch (L) {
+    case 2: return kDilithium2;
+    case 3: return kDilithium3;
+    case 5: return kDilithium5;
+    case 44: return kMLDSA44;
+    case 65: return kMLDSA65;
+    default: return kMLDSA87;
+  }
 }
 
 // strict hint-section check of a signature (packing.hpp:122-140): what the reference's
 // unpack_sig refuses and its CLI reports as exit 2 rather than "reject"
 template <Params P>
 bool sig_encoding_ok(std::span<const uint8_t> sig) {
-  const uint8_t* h = sig.data() + 32 + P.l * 32 * P.z_bits;
+  const uint8_t* h = sig.data() + P.ctilde_bytes + P.l * 32 * P.z_bits;
   size_t prev = 0;
   for (size_t i = 0; i < P.k; ++i) {
     const size_t cnt = h[P.omega + i];
