@@ -12,7 +12,8 @@
  * Byte sizes per level: pk 1312/1952/2592, sk 2528/4000/4864, sig 2420/3293/4595.
  *
  * level 44, 65 or 87 selects ML-DSA-44/65/87 (FIPS 204) on the same engine: the standard's
- * hashing conventions (H(xi||k||l), 64-byte tr, M' = 0||0||M i.e. the empty context string,
+ * hashing conventions (H(xi||k||l), 64-byte tr, M' = 0||len||ctx||M with the context string of
+ * dlb_set_mldsa_context, empty by default,
  * rho'' = H(K||0^32||mu) i.e. the deterministic variant, lambda/4-byte commitment hash).
  * Sizes: pk 1312/1952/2592, sk 2560/4032/4896, sig 2420/3309/4627.  Not part of the
  * reference (proj/README.md:120-121); pinned against OpenSSL, see oracle/dilithium_oracle.h.
@@ -76,6 +77,11 @@ int dlb_set_stream(dlb_ctx* ctx, void* cuda_stream);
 int dlb_measure_int32_peak(dlb_ctx* ctx, double out[4]);
 /* out[0] mul.hi.s32 (IMAD.HI), out[1] mul.wide.s32 (IMAD.WIDE), same unit. */
 int dlb_measure_imad_hi_peak(dlb_ctx* ctx, double out[2]);
+
+/* FIPS 204 context string for the ML-DSA levels (44 / 65 / 87): signing and verification
+ * hash M' = 0 || len || ctx || M.  len <= 255; the default is the empty string.  Sticky per
+ * context until changed; ignored by the round-3 levels. */
+int dlb_set_mldsa_context(dlb_ctx* ctx, const uint8_t* context_string, size_t len);
 
 /* Pinned host memory for callers that want zero-staging transfers (the engine copies
  * straight from/to these buffers with cudaMemcpyAsync). */

@@ -84,12 +84,19 @@ class Engine {
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
   dlb_ctx* ctx() const { return ctx_; }
+  // FIPS 204 context string (<= 255 bytes) for the ML-DSA parameter sets; sticky, default empty
+  void set_mldsa_context(std::span<const uint8_t> context) {
+    check_rc(dlb_set_mldsa_context(ctx_, context.data(), context.size()));
+  }
   static Engine& instance() {
     static Engine e(0);
     return e;
   }
 
  private:
+  static void check_rc(int rc) {
+    if (rc != 0) throw std::invalid_argument("dlb_set_mldsa_context: status " + std::to_string(rc));
+  }
   dlb_ctx* ctx_ = nullptr;
 };
 

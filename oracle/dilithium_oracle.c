@@ -634,6 +634,26 @@ int orc_sign_attempt(int level, const uint8_t* sk, const uint8_t mu[64],
   return ok;
 }
 
+/* FIPS 204 context string (ML-DSA levels only): M' = 0 || len || ctx || M */
+static uint8_t g_ctx[255];
+static size_t g_ctx_len = 0;
+int orc_set_mldsa_context(const uint8_t* ctx, size_t len) {
+  if (len > 255) return -1;
+  if (len) memcpy(g_ctx, ctx, len);
+  g_ctx_len = len;
+  return 0;
+}
+static void mldsa_mu(uint8_t mu[64], const uint8_t tr[64], const uint8_t* msg, size_t msglen) {
+  xof_t x;
+  const uint8_t pfx[2] = {0, (uint8_t)g_ctx_len};
+  xof_init(&x, 136);
+  xof_absorb(&x, tr, 64);
+  xof_absorb(&x, pfx, 2);
+  xof_absorb(&x, g_ctx, g_ctx_len);
+  xof_absorb(&x, msg, msglen);
+  xof_squeeze(&x, mu, 64);
+}
+
 /* scheme.hpp:240-273 */
 int orc_sign(int level, const uint8_t* sk, const uint8_t* msg, size_t msglen,
              const uint8_t* rho_prime_override, uint8_t* sig, uint32_t* attempts) {
@@ -646,15 +666,9 @@ int orc_sign(int level, const uint8_t* sk, const uint8_t* msg, size_t msglen,
   }
   uint8_t mu[64], rho_prime[64], c_tilde[64];
   if (P->mldsa) {
-    /* FIPS 204 Alg. 2 / 7 with an empty context string, deterministic variant:
-     * M' = 0 || 0 || M, mu = H(tr || M', 64), rho'' = H(K || rnd || mu, 64), rnd = 0^32 */
-    xof_t x;
-    const uint8_t pfx[2] = {0, 0};
-    xof_init(&x, 136);
-    xof_absorb(&x, pre->v.tr, 64);
-    xof_absorb(&x, pfx, 2);
-    xof_absorb(&x, msg, msglen);
-    xof_squeeze(&x, mu, 64);
+    /* FIPS 204 Alg. 2 / 7, deterministic variant: M' = 0 || |ctx| || ctx || M,
+     * mu = H(tr || M', 64), rho'' = H(K || rnd || mu, 64), rnd = 0^32 */
+    mldsa_mu(mu, pre->v.tr, msg, msglen);
     uint8_t krnd[64] = {0};
     memcpy(krnd, pre->v.key, 32);
     hash2(rho_prime, 64, krnd, 64, mu, 64);
@@ -701,14 +715,8 @@ int orc_verify(int level, const uint8_t* pk, size_t pklen, const uint8_t* msg, s
 
   uint8_t tr[64], mu[64];
   orc_shake256(tr, (size_t)P->tr_bytes, pk, pklen);
-  if (P->mldsa) { /* FIPS 204 Alg. 3 / 8, empty context: mu = H(tr || 0 || 0 || M, 64) */
-    xof_t x;
-    const uint8_t pfx[2] = {0, 0};
-    xof_init(&x, 136);
-    xof_absorb(&x, tr, 64);
-    xof_absorb(&x, pfx, 2);
-    xof_absorb(&x, msg, msglen);
-    xof_squeeze(&x, mu, 64);
+  if (P->mldsa) { /* FIPS 204 Alg. 3 / 8: mu = H(tr || 0 || |ctx| || ctx || M, 64) */
+    mldsa_mu(mu, tr, msg, msglen);
   } else {
     hash2(mu, 64, tr, 32, msg, msglen);
   }

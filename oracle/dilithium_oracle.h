@@ -64,6 +64,10 @@ void orc_decompose(int32_t r, int32_t gamma2, int32_t* r1, int32_t* r0);
 int orc_make_hint(int32_t z, int32_t r, int32_t gamma2);
 int32_t orc_use_hint(int h, int32_t r, int32_t gamma2);
 
+/* FIPS 204 context string used by sign / verify at levels 44 / 65 / 87 (len <= 255; default
+ * empty; process-wide, not thread-safe -- tests only) */
+int orc_set_mldsa_context(const uint8_t* ctx, size_t len);
+
 /* scheme.hpp:68-104 */
 int orc_keygen(int level, const uint8_t zeta[32], uint8_t* pk, uint8_t* sk);
 /* scheme.hpp:253-273 (make_precomp + sign_with_precomp).  rho_prime_override may be

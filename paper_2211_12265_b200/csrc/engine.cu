@@ -218,6 +218,16 @@ int dlb_set_stream(dlb_ctx* c, void* cuda_stream) {
   return 0;
 }
 
+int dlb_set_mldsa_context(dlb_ctx* c, const uint8_t* ctx_bytes, size_t len) {
+  if (!c || len > 255 || (len && !ctx_bytes)) return DLB_E_ARG;  // FIPS 204: |ctx| <= 255
+  c->mldsa_pfx[0] = 0;
+  c->mldsa_pfx[1] = (uint8_t)len;
+  if (len) memcpy(c->mldsa_pfx + 2, ctx_bytes, len);
+  c->mldsa_plen = 2 + (unsigned)len;
+  c->mldsa_pfx_dirty = true;
+  return 0;
+}
+
 void* dlb_host_alloc(size_t bytes) {
   void* p = nullptr;
   if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {

@@ -43,6 +43,12 @@ struct dlb_ctx {
   float last_ms = 0.f, last_main_ms = 0.f;  // whole call / dominant kernel only
   unsigned launches = 0;
   int sm_count = 148;
+  // FIPS 204 message prefix 0 || |ctx| || ctx (2..257 bytes) for the ML-DSA levels: host copy
+  // and its device mirror; the default is the empty context string
+  uint8_t mldsa_pfx[264] = {0, 0};
+  unsigned mldsa_plen = 2;
+  uint8_t* d_mldsa_pfx = nullptr;
+  bool mldsa_pfx_dirty = true;
   std::map<std::string, dlb::DevBuf> dev;
   std::map<std::string, dlb::HostBuf> pinned;
 
@@ -104,6 +110,25 @@ inline int dalloc(dlb_ctx* c, const char* name, size_t count, T** out) {
 }
 
 inline unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
+
+// device mirror of the ML-DSA message prefix, refreshed on `st` when the context string changed
+inline int mldsa_prefix(dlb_ctx* c, cudaStream_t st, const uint8_t** d_pfx, unsigned* plen) {
+  if (!c->d_mldsa_pfx) {
+    const int rc = dalloc(c, "mldsa.pfx", sizeof c->mldsa_pfx, &c->d_mldsa_pfx);
+    if (rc != 0) return rc;
+    c->mldsa_pfx_dirty = true;
+  }
+  if (c->mldsa_pfx_dirty) {
+    if (cudaMemcpyAsync(c->d_mldsa_pfx, c->mldsa_pfx, sizeof c->mldsa_pfx, cudaMemcpyHostToDevice, st) !=
+        cudaSuccess)
+      return -1000 - (int)cudaGetLastError();
+    cudaStreamSynchronize(st);  // the host copy may change again right after this call
+    c->mldsa_pfx_dirty = false;
+  }
+  *d_pfx = c->d_mldsa_pfx;
+  *plen = c->mldsa_plen;
+  return 0;
+}
 
 // One L1 / shared-memory split for every kernel of a pipeline.  The split is a per-SM
 // setting that cannot change under resident CTAs: a kernel that prefers another split than

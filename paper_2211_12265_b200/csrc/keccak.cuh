@@ -114,26 +114,28 @@ __device__ __forceinline__ uint64_t padded_word(const uint8_t* p, size_t len, si
   return w;
 }
 
-// Absorb an arbitrary-length message (prefix words already XORed by the caller are
-// expressed through `pre`/`pre_words`: the first pre_words 64-bit words of the
-// message come from registers, then GAP zero bytes (FIPS 204's 0 || |ctx| prefix with an
-// empty context), the rest from global memory at msg[0..msg_len)).
+// Absorb an arbitrary-length message: the first PRE_WORDS 64-bit words come from registers
+// (`pre`), then `plen` bytes from `pfx` (global memory; FIPS 204's 0 || |ctx| || ctx in front
+// of the message, plen = 0 for round 3), then msg[0..msg_len) from global memory.
 // Leaves the sponge finalized and permuted once: s holds the first squeeze block.
-template <int RATE_WORDS, int PRE_WORDS, int GAP = 0>
+template <int RATE_WORDS, int PRE_WORDS>
 __device__ __forceinline__ void shake_absorb_pre(uint64_t (&s)[25], const uint64_t (&pre)[PRE_WORDS],
+                                                 const uint8_t* pfx, unsigned plen,
                                                  const uint8_t* msg, size_t msg_len) {
   static_assert(PRE_WORDS < RATE_WORDS, "prefix must fit the first block");
-  static_assert(GAP >= 0 && GAP < 8, "gap is shorter than a word");
   keccak_clear(s);
-  // the tail behind the register prefix is the virtual message  0^GAP || msg
-  const size_t tail_len = (size_t)GAP + msg_len;
-  const size_t total = (size_t)PRE_WORDS * 8 + tail_len;
+  // the tail behind the register prefix is the virtual message  pfx || msg
+  const size_t total = (size_t)PRE_WORDS * 8 + plen + msg_len;
   const size_t nblocks = total / (RATE_WORDS * 8) + 1;  // padding always adds a byte
   auto tail_word = [&](size_t off) -> uint64_t {  // 8 bytes of the padded tail at `off`
-    if (GAP == 0) return padded_word(msg, msg_len, off);
-    if (off >= (size_t)GAP) return padded_word(msg, msg_len, off - GAP);
-    // off == 0: GAP zero bytes, then the first 8 - GAP bytes of the padded message
-    return padded_word(msg, msg_len, 0) << (8 * GAP);
+    if (plen == 0) return padded_word(msg, msg_len, off);
+    if (off >= plen) return padded_word(msg, msg_len, off - plen);
+    const unsigned nb = plen - (unsigned)off;  // prefix bytes from this word on
+    if (nb >= 8)
+      return (uint64_t)load_u32_unaligned(pfx + off) | ((uint64_t)load_u32_unaligned(pfx + off + 4) << 32);
+    uint64_t w = 0;
+    for (unsigned i = 0; i < nb; ++i) w |= (uint64_t)__ldg(pfx + off + i) << (8 * i);
+    return w | (padded_word(msg, msg_len, 0) << (8 * nb));  // the bytes shifted out lead the next word
   };
 #pragma unroll 1
   for (size_t blk = 0; blk < nblocks; ++blk) {

@@ -307,12 +307,14 @@ static __global__ void k_hash_tr(const uint8_t* __restrict__ pk, size_t pk_strid
 // mu = SHAKE256(tr || M, 64) and optionally rho' = SHAKE256(K || mu, 64)
 // (scheme.hpp:240-248).  tr and K (32 B) per key, 8-byte aligned; task t uses key
 // key_idx[t] (key_idx == nullptr: key t), strides 0 = one shared key.
-// MLDSA (FIPS 204 Alg. 2 / 7, empty context, deterministic): tr is 64 bytes,
-// mu = H(tr || 0 || 0 || M, 64) and rho'' = H(K || 0^32 || mu, 64).
+// MLDSA (FIPS 204 Alg. 2 / 7, deterministic variant): tr is 64 bytes,
+// mu = H(tr || 0 || |ctx| || ctx || M, 64) with the 2 + |ctx| prefix bytes at `pfx`
+// (plen of them), and rho'' = H(K || 0^32 || mu, 64).  Round 3: pfx unused, plen = 0.
 template <bool MLDSA>
 static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_stride,
                           const uint8_t* __restrict__ key_base, size_t key_stride,
                           const uint32_t* __restrict__ key_idx,
+                          const uint8_t* __restrict__ pfx, unsigned plen,
                           const uint8_t* __restrict__ msgs, const uint64_t* __restrict__ msg_off,
                           unsigned n, uint64_t* __restrict__ mu_out,
                           uint64_t* __restrict__ rho_prime_out) {
@@ -326,7 +328,7 @@ static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_
 #pragma unroll
   for (int w = 0; w < TRW; ++w) pre[w] = __ldg(tr + w);
   const uint64_t m0 = msg_off[t], m1 = msg_off[t + 1];
-  shake_absorb_pre<kWords256, TRW, MLDSA ? 2 : 0>(s, pre, msgs + m0, (size_t)(m1 - m0));
+  shake_absorb_pre<kWords256, TRW>(s, pre, pfx, MLDSA ? plen : 0u, msgs + m0, (size_t)(m1 - m0));
   uint64_t mu[8];
 #pragma unroll
   for (int w = 0; w < 8; ++w) {

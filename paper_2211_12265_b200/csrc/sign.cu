@@ -748,9 +748,12 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
     mu_use = d_mu_in;  // stage tests supply mu and rho' directly
     rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
   } else {
+    const uint8_t* pfx = nullptr;
+    unsigned plen = 0;
+    if (Hashing<P>::MLDSA) DLB_TRY(mldsa_prefix(c, st, &pfx, &plen));
     k_hash_mu<Hashing<P>::MLDSA><<<cdiv(n, 128), 128, 0, st>>>(
-        d_sks + 64, sk_stride, d_sks + 32, sk_stride, d_key_idx, d_msgs, d_msg_off, (unsigned)n, mu,
-        d_rho_prime ? nullptr : rp);
+        d_sks + 64, sk_stride, d_sks + 32, sk_stride, d_key_idx, pfx, plen, d_msgs, d_msg_off,
+        (unsigned)n, mu, d_rho_prime ? nullptr : rp);
     c->launches += 1;
     if (d_rho_prime) rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
   }

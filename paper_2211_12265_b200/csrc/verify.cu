@@ -91,6 +91,9 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
     prefer_carveout(k_verify_arith<P, 4>, co);
     prefer_carveout(k_verify_final<P>, co);
   }
+  const uint8_t* pfx = nullptr;
+  unsigned plen = 0;
+  if (Hashing<P>::MLDSA) DLB_TRY(mldsa_prefix(c, main, &pfx, &plen));
   if (shared_key) {  // expand once on the caller's stream, before the fork
     k_expand_a<P, HW><<<cdiv(n_keys * KL, HW * 32), HW * 32, 0, main>>>(d_pks, pk_stride,
                                                                         (unsigned)(n_keys * KL), A[0]);
@@ -118,8 +121,8 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
       c->launches += 2;
     }
     k_hash_mu<Hashing<P>::MLDSA><<<cdiv(cnt, 128), 128, 0, st>>>(
-        tr[b], key_step * Hashing<P>::TR, nullptr, 0, kidx, d_msgs, d_msg_off + lo, (unsigned)cnt, mu[b],
-        nullptr);
+        tr[b], key_step * Hashing<P>::TR, nullptr, 0, kidx, pfx, plen, d_msgs, d_msg_off + lo,
+        (unsigned)cnt, mu[b], nullptr);
     k_sample_in_ball<P, HW><<<cdiv(cnt, HW * 32), HW * 32, 0, st>>>(sigs, S::SIG, (unsigned)cnt, c8[b]);
     k_verify_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>(
         (unsigned)cnt, pks, pk_stride, sigs, S::SIG, A[b], key_step * (size_t)KL * kN, kidx, c8[b],

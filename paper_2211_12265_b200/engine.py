@@ -60,6 +60,7 @@ def load_library():
         "dlb_set_stream": (C.c_int, [vp, vp]),
         "dlb_measure_int32_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "dlb_measure_imad_hi_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "dlb_set_mldsa_context": (C.c_int, [vp, _u8p, sz]),
         "dlb_host_alloc": (vp, [sz]),
         "dlb_host_free": (None, [vp]),
         "dlb_keygen_batch": (C.c_int, [vp, C.c_int, sz, _u8p, _u8p, _u8p]),
@@ -95,7 +96,7 @@ def load_library():
 
 EXPORTED_SYMBOLS = [
     "dlb_create", "dlb_destroy", "dlb_version", "dlb_last_kernel_ms", "dlb_last_main_kernel_ms", "dlb_last_launches",
-    "dlb_set_stream", "dlb_measure_int32_peak", "dlb_measure_imad_hi_peak", "dlb_host_alloc", "dlb_host_free", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
+    "dlb_set_stream", "dlb_set_mldsa_context", "dlb_measure_int32_peak", "dlb_measure_imad_hi_peak", "dlb_host_alloc", "dlb_host_free", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
     "dlb_sign_batch_keyed", "dlb_verify_batch_keyed", "dlb_sign_batch_keyed_dev", "dlb_verify_batch_keyed_dev",
     "dlb_keygen_batch_dev", "dlb_sign_batch_dev", "dlb_verify_batch_dev", "dlb_dbg_keccak_f1600",
     "dlb_dbg_shake256", "dlb_dbg_expand_a", "dlb_dbg_expand_s", "dlb_dbg_expand_mask",
@@ -169,6 +170,12 @@ class Engine:
         self._chk(self.lib.dlb_measure_imad_hi_peak(self.ctx, hi), "dlb_measure_imad_hi_peak")
         return {"lop3": out[0], "imad": out[1], "shf": out[2], "lop3_imad_mix": out[3],
                 "imad_hi": hi[0], "imad_wide": hi[1]}
+
+    def set_mldsa_context(self, context=b""):
+        """FIPS 204 context string (<= 255 bytes) for levels 44 / 65 / 87; sticky, default empty."""
+        buf = np.frombuffer(bytes(context), np.uint8)
+        self._chk(self.lib.dlb_set_mldsa_context(self.ctx, buf.ctypes.data_as(_u8p) if len(buf) else None,
+                                                 len(buf)), "dlb_set_mldsa_context")
 
     # ---- batch.hpp:159-166
     def batch_keygen(self, level, zetas):

@@ -226,6 +226,12 @@ class _Checker:
 
 
 class Oracle(_Checker):
+    def set_mldsa_context(self, ctx=b""):
+        """FIPS 204 context string for levels 44 / 65 / 87 (oracle only)."""
+        fn = self.lib.orc_set_mldsa_context
+        fn.restype, fn.argtypes = C.c_int, [_u8p, C.c_size_t]
+        assert fn(_p(bytes(ctx)) if ctx else None, len(ctx)) == 0
+
     prefix = "orc_"
 
 

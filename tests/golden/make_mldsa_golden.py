@@ -53,7 +53,21 @@ for level, cls in KEYS.items():
                 pass
             sigs.append({"msg": m.hex(), "openssl_sig": theirs.hex(), "oracle_sig": ours.hex(),
                          "oracle_attempts": attempts})
-        cases.append({"seed": seed.hex(), "pk": pk.hex(), "sk_sha_len": len(osk), "sigs": sigs})
+        # non-empty context strings (FIPS 204 Alg. 2 / 3): one short, one of maximal length
+        ctx_sigs = []
+        for ctx in (b"ctx-%d" % s, bytes((i * 7 + level) & 0xFF for i in range(255))):
+            m = b"message under a context string %d" % s
+            oracle.set_mldsa_context(ctx)
+            theirs = sk_obj.sign(m, ctx)
+            assert oracle.verify(level, pk, m, theirs) == 1
+            ours, attempts = oracle.sign(level, osk, m)
+            sk_obj.public_key().verify(ours, m, ctx)
+            oracle.set_mldsa_context(b"")
+            assert oracle.verify(level, pk, m, theirs) == 0  # wrong context rejects
+            ctx_sigs.append({"ctx": ctx.hex(), "msg": m.hex(), "openssl_sig": theirs.hex(),
+                             "oracle_sig": ours.hex(), "oracle_attempts": attempts})
+        cases.append({"seed": seed.hex(), "pk": pk.hex(), "sk_sha_len": len(osk), "sigs": sigs,
+                      "ctx_sigs": ctx_sigs})
     out["levels"][str(level)] = cases
 path = os.path.join(ROOT, "tests", "golden", "mldsa_openssl.json")
 json.dump(out, open(path, "w"), indent=0)

@@ -41,6 +41,18 @@ def test_openssl_vectors(eng, golden, level):
             assert eng.verify(level, pk, msg + b"!", bytes.fromhex(s["openssl_sig"])) == 0
             sig, att = eng.sign(level, gsk, msg)
             assert sig.hex() == s["oracle_sig"] and att == s["oracle_attempts"]
+        for s in case["ctx_sigs"]:  # context strings: 5 and 255 bytes
+            ctx, msg, theirs = (bytes.fromhex(s[k]) for k in ("ctx", "msg", "openssl_sig"))
+            assert eng.verify(level, pk, msg, theirs) == 0
+            eng.set_mldsa_context(ctx)
+            try:
+                assert eng.verify(level, pk, msg, theirs) == 1
+                sig, att = eng.sign(level, gsk, msg)
+                assert sig.hex() == s["oracle_sig"] and att == s["oracle_attempts"]
+            finally:
+                eng.set_mldsa_context(b"")
+            with pytest.raises(Exception):
+                eng.set_mldsa_context(bytes(256))
 
 
 @pytest.mark.parametrize("level", LEVELS)
@@ -98,3 +110,27 @@ def test_single_attempts_and_malformed_key(eng, oracle, level):
     bad[64 + 64] = 0xFF  # first eta field byte (the secret vectors start behind the 64-byte tr)
     with pytest.raises(ValueError):
         eng.sign(level, bytes(bad), b"x")
+
+
+@pytest.mark.parametrize("level", LEVELS)
+def test_context_strings_match_oracle(eng, oracle, level):
+    """Every prefix length 2 .. 257 shifts the message differently inside the first Keccak
+    blocks of mu; a few lengths around word and block boundaries, ragged messages."""
+    rng = mt19937_64(9100 + level)
+    pk, sk = oracle.keygen(level, rng.bytes(32))
+    sk_a, pk_a = np.frombuffer(sk, np.uint8), np.frombuffer(pk, np.uint8)
+    msgs = [rng.bytes(int(rng()) % 200) for _ in range(24)]
+    try:
+        for clen in (0, 1, 5, 6, 7, 13, 70, 71, 134, 254, 255):
+            ctx = rng.bytes(clen)
+            eng.set_mldsa_context(ctx)
+            oracle.set_mldsa_context(ctx)
+            sigs = eng.batch_sign(level, sk_a, msgs)
+            for m, sg in zip(msgs, sigs):
+                assert sg.tobytes() == oracle.sign(level, sk, m)[0], clen
+            assert eng.batch_verify(level, pk_a, msgs, sigs).all()
+            eng.set_mldsa_context(ctx + b"\x00" if clen < 255 else ctx[:-1])
+            assert not eng.batch_verify(level, pk_a, msgs, sigs).any()
+    finally:
+        eng.set_mldsa_context(b"")
+        oracle.set_mldsa_context(b"")

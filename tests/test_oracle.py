@@ -208,3 +208,13 @@ def test_mldsa_oracle_against_openssl_vectors(oracle, mldsa_golden, level):
             ours, att = oracle.sign(level, osk, msg)                    # OpenSSL accepted these bytes
             assert ours.hex() == s["oracle_sig"] and att == s["oracle_attempts"]
             assert oracle.verify(level, pk, msg, ours) == 1
+        for s in case["ctx_sigs"]:  # FIPS 204 context strings
+            ctx, msg, theirs = (bytes.fromhex(s[k]) for k in ("ctx", "msg", "openssl_sig"))
+            assert oracle.verify(level, pk, msg, theirs) == 0      # empty context: reject
+            oracle.set_mldsa_context(ctx)
+            try:
+                assert oracle.verify(level, pk, msg, theirs) == 1
+                ours, att = oracle.sign(level, osk, msg)
+                assert ours.hex() == s["oracle_sig"] and att == s["oracle_attempts"]
+            finally:
+                oracle.set_mldsa_context(b"")
