@@ -49,6 +49,10 @@ WORK = {  # level: perms, NTTs, INTTs, mul-acc polys
 }
 
 
+for _ml, _r3 in ((44, 2), (65, 3), (87, 5)):  # ML-DSA: the round-3 sets' work (+1 permutation for the 64-byte tr)
+    WORK[_ml] = WORK[_r3]
+
+
 def int_ops(t):
     perms, ntt, intt, mac = t
     return perms * W_PERM + ntt * W_NTT + intt * W_INTT + mac * 256 * W_MAC
@@ -545,7 +549,7 @@ def run_ours(args, dist):
     if not args.no_levels and world == 1:
         eng.set_stream(side.cuda_stream)
         levels = {}
-        for lv in (3, 5):
+        for lv in (3, 5, 44, 65, 87):  # configs[2], configs[3]; 44/65/87 = ML-DSA (FIPS 204 mode)
             r = other_level_numbers(eng, torch, dev, lv, n, max(2, K // 2), dist.rank)
             for op in ("sign", "verify", "keygen"):
                 r[op]["roofline_frac"] = r[op]["value"] * r[op]["int32_ops_per_unit"] / 1e12 / peaks["lop3"]
