@@ -175,6 +175,10 @@ int dlb_dbg_expand_mask(dlb_ctx* ctx, int level, size_t n, const uint8_t* rho_pr
                         const uint32_t* kappas /* n */, int32_t* out /* n*L*256 */);
 int dlb_dbg_sample_in_ball(dlb_ctx* ctx, int level, size_t n, const uint8_t* c_tildes /* n*32 */,
                            int8_t* out /* n*256 */);
+/* rounding.hpp:13-59 for the n values first, first+1, ... (canonical, in [0,q)) with
+ * gamma2 = (q-1)/gamma2_divisor (88 or 32).  out6: six arrays of n: Power2Round high, low;
+ * Decompose high, low; UseHint with hint 0, hint 1. */
+int dlb_dbg_rounding(dlb_ctx* ctx, int gamma2_divisor, int32_t first, size_t n, int32_t* out6);
 /* forward NTT (output canonical [0,q)) and inverse NTT of canonical input (output
  * canonical): value-level parity with ntt.hpp:74-126 */
 int dlb_dbg_ntt(dlb_ctx* ctx, size_t n, int32_t* polys /* n*256 in place */, int inverse);

@@ -142,6 +142,20 @@ __global__ void k_dbg_ntt(unsigned n, int32_t* polys, int inverse) {
   }
 }
 
+// rounding.hpp:13-59 on the device, one value per thread: Power2Round, Decompose and
+// UseHint with hint 0 / 1, for the exhaustive value test over [0, q)
+template <int GAMMA2>
+__global__ void k_dbg_rounding(unsigned n, int32_t first, int32_t* p2r_hi, int32_t* p2r_lo,
+                               int32_t* dec_hi, int32_t* dec_lo, int32_t* use0, int32_t* use1) {
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t a = first + (int32_t)i;
+  power2round(a, p2r_hi[i], p2r_lo[i]);
+  dec_hi[i] = decompose<GAMMA2>(a, dec_lo[i]);
+  use0[i] = use_hint<GAMMA2>(0, a);
+  use1[i] = use_hint<GAMMA2>(1, a);
+}
+
 }  // namespace
 
 extern "C" {
@@ -682,6 +696,22 @@ int dlb_dbg_sample_in_ball(dlb_ctx* c, int level, size_t n, const uint8_t* c_til
     DLB_TRY(d2h(c, out, dout, n * kN));
     return sync(c);
   });
+}
+
+int dlb_dbg_rounding(dlb_ctx* c, int gamma2_divisor, int32_t first, size_t n, int32_t* out6) {
+  if (!c || !out6 || (gamma2_divisor != 88 && gamma2_divisor != 32)) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  int32_t* d;
+  DLB_TRY(dalloc(c, "dbg.a", 6 * n, &d));
+  if (gamma2_divisor == 88)
+    k_dbg_rounding<(kQ - 1) / 88><<<cdiv(n, 256), 256, 0, c->s()>>>((unsigned)n, first, d, d + n, d + 2 * n,
+                                                                    d + 3 * n, d + 4 * n, d + 5 * n);
+  else
+    k_dbg_rounding<(kQ - 1) / 32><<<cdiv(n, 256), 256, 0, c->s()>>>((unsigned)n, first, d, d + n, d + 2 * n,
+                                                                    d + 3 * n, d + 4 * n, d + 5 * n);
+  DLB_LAUNCH_CHECK();
+  DLB_TRY(d2h(c, out6, d, 6 * n * 4));
+  return sync(c);
 }
 
 int dlb_dbg_ntt(dlb_ctx* c, size_t n, int32_t* polys, int inverse) {

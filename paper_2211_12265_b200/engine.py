@@ -83,6 +83,7 @@ def load_library():
         "dlb_dbg_expand_s": (C.c_int, [vp, C.c_int, sz, _u8p, _i8p]),
         "dlb_dbg_expand_mask": (C.c_int, [vp, C.c_int, sz, _u8p, _u32p, _i32p]),
         "dlb_dbg_sample_in_ball": (C.c_int, [vp, C.c_int, sz, _u8p, _i8p]),
+        "dlb_dbg_rounding": (C.c_int, [vp, C.c_int, C.c_int32, sz, _i32p]),
         "dlb_dbg_ntt": (C.c_int, [vp, sz, _i32p, C.c_int]),
         "dlb_dbg_sign_attempt": (C.c_int, [vp, C.c_int, sz, _u8p, sz, _u8p, _u8p, _u32p, _u8p,
                                            _u8p, _i32p, _i32p]),
@@ -100,7 +101,7 @@ EXPORTED_SYMBOLS = [
     "dlb_sign_batch_keyed", "dlb_verify_batch_keyed", "dlb_sign_batch_keyed_dev", "dlb_verify_batch_keyed_dev",
     "dlb_keygen_batch_dev", "dlb_sign_batch_dev", "dlb_verify_batch_dev", "dlb_dbg_keccak_f1600",
     "dlb_dbg_shake256", "dlb_dbg_expand_a", "dlb_dbg_expand_s", "dlb_dbg_expand_mask",
-    "dlb_dbg_sample_in_ball", "dlb_dbg_ntt", "dlb_dbg_sign_attempt",
+    "dlb_dbg_sample_in_ball", "dlb_dbg_rounding", "dlb_dbg_ntt", "dlb_dbg_sign_attempt",
 ]
 
 
@@ -319,6 +320,13 @@ class Engine:
         n = r.size // 32
         out = np.zeros((n, 256), np.int8)
         self._chk(self.lib.dlb_dbg_sample_in_ball(self.ctx, level, n, rp, out.ctypes.data_as(_i8p)), "sib")
+        return out
+
+    def dbg_rounding(self, gamma2_divisor, first, n):
+        """(p2r_hi, p2r_lo, dec_hi, dec_lo, use_hint0, use_hint1) for first .. first+n-1."""
+        out = np.zeros((6, n), np.int32)
+        self._chk(self.lib.dlb_dbg_rounding(self.ctx, gamma2_divisor, first, n, out.ctypes.data_as(_i32p)),
+                  "rounding")
         return out
 
     def dbg_ntt(self, polys, inverse=False):

@@ -115,3 +115,52 @@ def test_device_resident_api_matches_host_api(eng, oracle):
     assert eng.lib.dlb_verify_batch_dev(eng.ctx, level, n, p(d_pk), pkb, p(d_m), p(d_off), p(d_sig), p(d_fl)) == 0
     eng.set_stream(0)
     assert bool(d_fl.all().item())
+
+
+@pytest.mark.parametrize("level", [2, 3, 5, 65])
+def test_hint_section_every_byte(eng, oracle, level):
+    """Strict hint decoding (packing.hpp:122-140; tests/test_packing.cpp:111-184): every byte
+    of the hint section of a valid signature is replaced by a few values -- out-of-order
+    positions, counts that shrink / exceed omega, non-zero slack -- and the device verdict
+    must equal the oracle's for each mutant."""
+    P = PARAMS[level]
+    rng = mt19937_64(6100 + level)
+    pk, sk = oracle.keygen(level, rng.bytes(32))
+    msg = rng.bytes(40)
+    sig = np.frombuffer(oracle.sign(level, sk, msg)[0], np.uint8)
+    hint0 = P["sig"] - (P["omega"] + P["k"])
+    mutants = []
+    for pos in range(hint0, P["sig"]):
+        for val in (0, 1, 255, (int(sig[pos]) + 1) & 255, (int(sig[pos]) - 1) & 255, P["omega"], P["omega"] + 1):
+            if val != sig[pos]:
+                m = sig.copy()
+                m[pos] = val
+                mutants.append(m)
+    mutants = np.stack(mutants)
+    n = len(mutants)
+    flags = eng.batch_verify(level, np.frombuffer(pk, np.uint8), [msg] * n, mutants)
+    expect = np.array([oracle.verify(level, pk, msg, m.tobytes()) for m in mutants], np.uint8)
+    assert np.array_equal(flags, expect)
+    assert expect.sum() < n // 4  # nearly every mutation must be fatal
+
+
+def test_random_batch_shapes(eng, oracle):
+    """acceptance.cpp:186-244 / test_batch.cpp:190-228: random (level, Phi, Psi, speculate)
+    batches are byte-identical to sequential signing whatever the slot count."""
+    rng = mt19937_64(55)
+    keys = {lv: oracle.keygen(lv, rng.bytes(32)) for lv in (2, 3, 5)}
+    for it in range(36):
+        level = (2, 3, 5)[it % 3]
+        phi = 1 + int(rng()) % 160
+        psi = 1 + int(rng()) % phi if it % 4 else 0
+        spec = bool(int(rng()) & 1)
+        pk, sk = keys[level]
+        msgs = [rng.bytes(int(rng()) % 64) for _ in range(phi)]
+        sigs, att, failed, st = eng.batch_sign(level, np.frombuffer(sk, np.uint8), msgs, psi=psi,
+                                               speculate=spec, return_info=True)
+        assert not failed.any()
+        for i in range(phi):
+            assert (sigs[i].tobytes(), int(att[i])) == oracle.sign(level, sk, msgs[i]), (it, level, phi, psi, spec, i)
+        assert st["accepted_attempt_sum"] == int(att.sum()) and st["attempts"] >= st["accepted_attempt_sum"]
+        if not spec:
+            assert st["speculative"] == 0

@@ -122,3 +122,34 @@ def test_ntt_values(eng, oracle):
     b = eng.dbg_ntt(a, inverse=True)
     for i in range(len(a)):
         assert np.array_equal(b[i], oracle.intt(a[i])), i
+
+
+@pytest.mark.parametrize("divisor", [88, 32])
+def test_rounding_exhaustive(eng, oracle, divisor):
+    """Power2Round, Decompose and UseHint on the device for EVERY r in [0, q)
+    (tests/test_rounding.cpp:17-49,93-105; acceptance.cpp:109-145), against the definitions
+    written out in numpy, themselves spot-checked against the oracle's functions."""
+    q = 8380417
+    gamma2 = (q - 1) // divisor
+    alpha = 2 * gamma2
+    m = (q - 1) // alpha
+    r = np.arange(q, dtype=np.int64)
+    # definitions (SPEC / FIPS 204 Alg. 35-40): centred remainders
+    lo13 = ((r + 4095) % 8192) - 4095                      # r mod+- 2^13 in (-2^12, 2^12]
+    p2_hi, p2_lo = (r - lo13) >> 13, lo13
+    r0 = ((r + gamma2 - 1) % alpha) - (gamma2 - 1)          # r mod+- alpha in (-gamma2, gamma2]
+    wrap = (r - r0) == q - 1
+    d_hi = np.where(wrap, 0, (r - r0) // alpha)
+    d_lo = np.where(wrap, r0 - 1, r0)
+    u1 = np.where(d_lo > 0, (d_hi + 1) % m, (d_hi - 1) % m)
+    got = np.concatenate([eng.dbg_rounding(divisor, lo, min(1 << 22, q - lo)) for lo in range(0, q, 1 << 22)], axis=1)
+    for name, exp, g in (("p2r_hi", p2_hi, got[0]), ("p2r_lo", p2_lo, got[1]), ("dec_hi", d_hi, got[2]),
+                         ("dec_lo", d_lo, got[3]), ("use0", d_hi, got[4]), ("use1", u1, got[5])):
+        bad = np.flatnonzero(exp != g)
+        assert bad.size == 0, (name, bad[:5], exp[bad[:5]], g[bad[:5]])
+    rs = np.random.default_rng(5)
+    for v in np.concatenate([rs.integers(0, q, 3000), [0, 1, q - 1, q - 2, gamma2, gamma2 + 1, q - 1 - gamma2, q - gamma2]]):
+        v = int(v)
+        assert oracle.power2round(v) == (int(p2_hi[v]), int(p2_lo[v]))
+        assert oracle.decompose(v, gamma2) == (int(d_hi[v]), int(d_lo[v]))
+        assert oracle.use_hint(1, v, gamma2) == int(u1[v]) and oracle.use_hint(0, v, gamma2) == int(d_hi[v])
