@@ -6,7 +6,7 @@ sys.path.insert(0, ".")
 from paper_2211_12265_b200 import Engine
 eng = Engine(0)
 rng = np.random.default_rng(5)
-for level, n in ((2, 300), (3, 150), (5, 130)):
+for level, n in ((2, 300), (3, 150), (5, 130), (65, 120)):  # 65 = ML-DSA-65 (FIPS 204 mode)
     zetas = rng.integers(0, 256, (n, 32), dtype=np.uint8)
     msgs = [bytes(rng.integers(0, 256, int(rng.integers(0, 300)), dtype=np.uint8)) for _ in range(n)]
     pks, sks = eng.batch_keygen(level, zetas)
@@ -19,4 +19,9 @@ for level, n in ((2, 300), (3, 150), (5, 130)):
     kidx = rng.integers(0, 5, n).astype(np.uint32)  # mixed-key batch over a 5-key table
     sigs3 = eng.batch_sign(level, sks[:5], msgs, key_idx=kidx)
     assert eng.batch_verify(level, pks[:5], msgs, sigs3, key_idx=kidx).all()
+    if level == 65:  # a context string exercises the prefix gather of the mu hash
+        eng.set_mldsa_context(b"sanitizer context")
+        s4 = eng.batch_sign(level, sks[0], msgs[:40])
+        assert eng.batch_verify(level, pks[0], msgs[:40], s4).all()
+        eng.set_mldsa_context(b"")
     print("level", level, "ok, mean attempts %.2f" % att.mean())
