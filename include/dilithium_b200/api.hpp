@@ -266,19 +266,34 @@ std::vector<uint8_t> batch_verify(std::span<const VerifyJob<P>> jobs, size_t /*w
     if (jobs[i].pk.size() == P.pk_bytes() && jobs[i].sig.size() == P.sig_bytes()) live.push_back(i);
   if (live.empty()) return flags;
   const size_t m = live.size();
-  std::vector<uint8_t> pks(m * P.pk_bytes()), sigs(m * P.sig_bytes() + 8), flat, f(m);
+  // jobs that point at the same public key bytes share one expanded key on the device
+  std::unordered_map<const uint8_t*, uint32_t> key_of;
+  std::vector<const uint8_t*> keys;
+  std::vector<uint32_t> key_idx(m);
+  for (size_t a = 0; a < m; ++a) {
+    const uint8_t* pkp = jobs[live[a]].pk.data();
+    auto [it, fresh] = key_of.try_emplace(pkp, static_cast<uint32_t>(keys.size()));
+    if (fresh) keys.push_back(pkp);
+    key_idx[a] = it->second;
+  }
+  std::vector<uint8_t> pks(keys.size() * P.pk_bytes()), sigs(m * P.sig_bytes() + 8), flat, f(m);
+  for (size_t k = 0; k < keys.size(); ++k) std::memcpy(pks.data() + k * P.pk_bytes(), keys[k], P.pk_bytes());
   std::vector<uint64_t> off(m + 1, 0);
   for (size_t a = 0; a < m; ++a) off[a + 1] = off[a] + jobs[live[a]].message.size();
   flat.resize(off.back() + 8);
   for (size_t a = 0; a < m; ++a) {
     const auto& j = jobs[live[a]];
-    std::memcpy(pks.data() + a * P.pk_bytes(), j.pk.data(), P.pk_bytes());
     std::memcpy(sigs.data() + a * P.sig_bytes(), j.sig.data(), P.sig_bytes());
     if (!j.message.empty()) std::memcpy(flat.data() + off[a], j.message.data(), j.message.size());
   }
-  check(dlb_verify_batch(eng.ctx(), P.level, m, pks.data(), P.pk_bytes(), flat.data(), off.data(),
-                         sigs.data(), f.data()),
-        "dlb_verify_batch");
+  if (keys.size() == 1)
+    check(dlb_verify_batch(eng.ctx(), P.level, m, pks.data(), 0, flat.data(), off.data(), sigs.data(),
+                           f.data()),
+          "dlb_verify_batch");
+  else
+    check(dlb_verify_batch_keyed(eng.ctx(), P.level, keys.size(), pks.data(), m, key_idx.data(),
+                                 flat.data(), off.data(), sigs.data(), f.data()),
+          "dlb_verify_batch_keyed");
   for (size_t a = 0; a < m; ++a) flags[live[a]] = f[a];
   return flags;
 }
