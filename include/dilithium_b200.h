@@ -78,6 +78,20 @@ int dlb_measure_int32_peak(dlb_ctx* ctx, double out[4]);
 /* out[0] mul.hi.s32 (IMAD.HI), out[1] mul.wide.s32 (IMAD.WIDE), same unit. */
 int dlb_measure_imad_hi_peak(dlb_ctx* ctx, double out[2]);
 
+/* Per-round scheduler trace (BatchConfig::trace, RoundTrace scheduler.hpp:21-28; the tool's
+ * --trace CSV, dilithium_cli.cpp:128-134).  The device scheduler runs one independent round
+ * loop per CTA, so a record is one round of one CTA: `stream` is the CTA, `round` its round
+ * counter, the other fields as in RoundTrace restricted to that CTA's tasks and slots.
+ * dlb_set_trace(ctx, cap): the next sign calls log up to cap records (0 switches the trace
+ * off; default off -- logging costs one 32-byte store per CTA round).  dlb_get_trace copies
+ * the records of the last sign call, in no particular order, and returns how many the call
+ * produced (which may exceed cap: the surplus was dropped). */
+typedef struct dlb_round_trace {
+  uint32_t stream, round, unfinished, assigned, speculative, idle_slots, newly_done, reserved;
+} dlb_round_trace;
+int dlb_set_trace(dlb_ctx* ctx, size_t cap);
+long long dlb_get_trace(dlb_ctx* ctx, dlb_round_trace* out, size_t max_records);
+
 /* FIPS 204 context string for the ML-DSA levels (44 / 65 / 87): signing and verification
  * hash M' = 0 || len || ctx || M.  len <= 255; the default is the empty string.  Sticky per
  * context until changed; ignored by the round-3 levels. */

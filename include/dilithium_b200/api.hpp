@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <span>
@@ -139,10 +140,20 @@ std::optional<SignPrecomp<P>> make_precomp(std::span<const uint8_t> sk_bytes) {
   return pre;
 }
 
-struct BatchConfig {  // batch.hpp:23-29 (trace / assignment_hook: device counters in BatchStats)
+// scheduler.hpp:21-28.  The device scheduler runs one round loop per CTA, so a record is one
+// round of one CTA (`stream`); the remaining fields are RoundTrace's, restricted to that CTA.
+struct RoundTrace {
+  uint64_t round;
+  size_t unfinished, assigned, speculative, idle_slots, newly_done;
+  size_t stream = 0;
+};
+
+struct BatchConfig {  // batch.hpp:23-29
   size_t psi = 0;
   size_t workers = 1;
   bool speculate = true;
+  std::function<void(const RoundTrace&)> trace;  // called once per logged round after the batch
+  size_t trace_capacity = 1 << 20;               // records kept per call when `trace` is set
 };
 
 struct BatchStats {  // batch.hpp:31-38
@@ -233,12 +244,25 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
   dlb_sign_stats st{};
   static_assert(sizeof(SigBytes<P>) == P.sig_bytes());
   const uint8_t* rp = rho_prime_override ? rho_prime_override->data() : nullptr;
+  if (cfg.trace) check(dlb_set_trace(eng.ctx(), cfg.trace_capacity), "dlb_set_trace");
   const int rc =
       shared ? dlb_sign_batch(eng.ctx(), P.level, n, skp, 0, flat.data(), off.data(), rp, cfg.psi,
                               cfg.speculate ? 1 : 0, out[0].data(), att.data(), failed.data(), &st)
              : dlb_sign_batch_keyed(eng.ctx(), P.level, keys.size(), skp, n, key_idx.data(), flat.data(),
                                     off.data(), rp, cfg.psi, cfg.speculate ? 1 : 0, out[0].data(),
                                     att.data(), failed.data(), &st);
+  if (cfg.trace) {
+    std::vector<dlb_round_trace> recs(cfg.trace_capacity);
+    const long long total = rc == 0 ? dlb_get_trace(eng.ctx(), recs.data(), recs.size()) : 0;
+    dlb_set_trace(eng.ctx(), 0);
+    const size_t have = total < 0 ? 0 : std::min<size_t>(static_cast<size_t>(total), recs.size());
+    std::sort(recs.begin(), recs.begin() + have, [](const dlb_round_trace& a, const dlb_round_trace& b) {
+      return a.stream != b.stream ? a.stream < b.stream : a.round < b.round;
+    });
+    for (size_t i = 0; i < have; ++i)
+      cfg.trace(RoundTrace{recs[i].round, recs[i].unfinished, recs[i].assigned, recs[i].speculative,
+                           recs[i].idle_slots, recs[i].newly_done, recs[i].stream});
+  }
   if (rc == DLB_E_KEY) throw std::invalid_argument("batch_sign: malformed secret key");
   check(rc, "dlb_sign_batch");
   if (stats) {

@@ -232,6 +232,27 @@ int dlb_set_stream(dlb_ctx* c, void* cuda_stream) {
   return 0;
 }
 
+int dlb_set_trace(dlb_ctx* c, size_t cap) {
+  if (!c || cap > (1u << 26)) return DLB_E_ARG;
+  c->trace_cap = cap;
+  c->trace_count = 0;
+  return 0;
+}
+
+long long dlb_get_trace(dlb_ctx* c, dlb_round_trace* out, size_t max_records) {
+  if (!c) return DLB_E_ARG;
+  const unsigned long long have = c->trace_count < c->trace_cap ? c->trace_count : c->trace_cap;
+  const size_t ncopy = have < max_records ? (size_t)have : max_records;
+  if (ncopy && out) {
+    auto it = c->dev.find("s.trace");
+    if (it == c->dev.end() || !it->second.p) return DLB_E_ARG;
+    cudaSetDevice(c->device);
+    const cudaError_t e = cudaMemcpy(out, it->second.p, ncopy * sizeof(dlb_round_trace), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return -1000 - (int)e;
+  }
+  return (long long)c->trace_count;
+}
+
 int dlb_set_mldsa_context(dlb_ctx* c, const uint8_t* ctx_bytes, size_t len) {
   if (!c || len > 255 || (len && !ctx_bytes)) return DLB_E_ARG;  // FIPS 204: |ctx| <= 255
   c->mldsa_pfx[0] = 0;

@@ -43,6 +43,8 @@ struct dlb_ctx {
   float last_ms = 0.f, last_main_ms = 0.f;  // whole call / dominant kernel only
   unsigned launches = 0;
   int sm_count = 148;
+  size_t trace_cap = 0;          // per-round scheduler trace (dlb_set_trace); 0 = off
+  unsigned long long trace_count = 0;  // records the last sign call produced
   // FIPS 204 message prefix 0 || |ctx| || ctx (2..257 bytes) for the ML-DSA levels: host copy
   // and its device mirror; the default is the empty context string
   uint8_t mldsa_pfx[264] = {0, 0};

@@ -85,6 +85,7 @@ struct SignQueue {
   unsigned key_bad;       // some secret key failed the eta range check
   unsigned long long rounds, attempts, speculative, idle_slots, accepted_sum, failed;
   unsigned long long t_first_start, t_last_start, t_first_exit, t_last_exit;  // %globaltimer, ns
+  unsigned long long trace_count;  // per-round trace records produced (may exceed the capacity)
 };
 
 struct SignArgs {
@@ -103,6 +104,8 @@ struct SignArgs {
   const int32_t* shat;        // keys * (L+2K)*256
   unsigned key_stride;        // 0 shared key, 1 per-task keys (when key_idx == nullptr)
   const uint32_t* key_idx;    // nullable: key table index of each task
+  uint32_t* trace;            // nullable: per-round records of 8 words (dlb_round_trace)
+  unsigned trace_cap;
   // per-CTA scratch in HBM/L2, indexed [cta][slot]
   uint8_t* ybytes;
   int32_t* wbuf;
@@ -156,6 +159,7 @@ struct SignSmem {
   uint32_t warp_sums[kSignWarps];
   unsigned U, newU, got, base;
   unsigned cursor2, cursor4;  // next unclaimed slot of stages S2 / S4 (warps pull slots)
+  unsigned r_on, r_spec;      // this round's assigned / speculative slots (trace)
   unsigned long long st_rounds, st_attempts, st_spec, st_idle;  // per-CTA counters
 };
 
@@ -497,6 +501,8 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
         sm.st_attempts += n_on;
         sm.st_spec += n_spec;
         sm.st_idle += a.slots - n_on;
+        sm.r_on = n_on;
+        sm.r_spec = n_spec;
       }
     }
     const unsigned my_task = sm.slot_task[tid];
@@ -690,7 +696,17 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
         sm.utask[pos] = my_u_task;
         sm.unext[pos] = my_u_next;
       }
-      if (tid == 0) sm.U = total;
+      if (tid == 0) {
+        if (a.trace) {  // RoundTrace of this CTA's round (scheduler.hpp:21-28)
+          const unsigned long long idx = atomicAdd(&a.q->trace_count, 1ull);
+          if (idx < a.trace_cap) {
+            uint4* rec = reinterpret_cast<uint4*>(a.trace + idx * 8);
+            rec[0] = make_uint4(blockIdx.x, (unsigned)sm.st_rounds - 1u, U, sm.r_on);
+            rec[1] = make_uint4(sm.r_spec, a.slots - sm.r_on, U - total, 0u);
+          }
+        }
+        sm.U = total;
+      }
       __syncthreads();
     }
   }
@@ -824,6 +840,10 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   a.shat = shat;
   a.key_stride = sk_stride ? 1u : 0u;
   a.key_idx = d_key_idx;
+  if (c->trace_cap && !single_round) {
+    DLB_TRY(dalloc(c, "s.trace", c->trace_cap * 8, &a.trace));
+    a.trace_cap = (unsigned)(c->trace_cap > 0xFFFFFFFFu ? 0xFFFFFFFFu : c->trace_cap);
+  }
   const size_t slots = grid * kSignThreads;
   DLB_TRY(dalloc(c, "s.y", slots * Z::Y_SLOT + 16, &a.ybytes));
   DLB_TRY(dalloc(c, "s.w", slots * Z::W_SLOT, &a.wbuf));
@@ -858,6 +878,7 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
     stats->t_first_exit_ns = hq.t_first_exit;
     stats->t_last_exit_ns = hq.t_last_exit;
   }
+  c->trace_count = a.trace ? hq.trace_count : 0;
   if (hq.key_bad) return DLB_E_KEY;
   return 0;
 }

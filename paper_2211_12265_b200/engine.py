@@ -61,6 +61,8 @@ def load_library():
         "dlb_measure_int32_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "dlb_measure_imad_hi_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "dlb_set_mldsa_context": (C.c_int, [vp, _u8p, sz]),
+        "dlb_set_trace": (C.c_int, [vp, sz]),
+        "dlb_get_trace": (C.c_longlong, [vp, vp, sz]),
         "dlb_host_alloc": (vp, [sz]),
         "dlb_host_free": (None, [vp]),
         "dlb_keygen_batch": (C.c_int, [vp, C.c_int, sz, _u8p, _u8p, _u8p]),
@@ -97,7 +99,7 @@ def load_library():
 
 EXPORTED_SYMBOLS = [
     "dlb_create", "dlb_destroy", "dlb_version", "dlb_last_kernel_ms", "dlb_last_main_kernel_ms", "dlb_last_launches",
-    "dlb_set_stream", "dlb_set_mldsa_context", "dlb_measure_int32_peak", "dlb_measure_imad_hi_peak", "dlb_host_alloc", "dlb_host_free", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
+    "dlb_set_stream", "dlb_set_mldsa_context", "dlb_set_trace", "dlb_get_trace", "dlb_measure_int32_peak", "dlb_measure_imad_hi_peak", "dlb_host_alloc", "dlb_host_free", "dlb_keygen_batch", "dlb_sign_batch", "dlb_verify_batch",
     "dlb_sign_batch_keyed", "dlb_verify_batch_keyed", "dlb_sign_batch_keyed_dev", "dlb_verify_batch_keyed_dev",
     "dlb_keygen_batch_dev", "dlb_sign_batch_dev", "dlb_verify_batch_dev", "dlb_dbg_keccak_f1600",
     "dlb_dbg_shake256", "dlb_dbg_expand_a", "dlb_dbg_expand_s", "dlb_dbg_expand_mask",
@@ -171,6 +173,21 @@ class Engine:
         self._chk(self.lib.dlb_measure_imad_hi_peak(self.ctx, hi), "dlb_measure_imad_hi_peak")
         return {"lop3": out[0], "imad": out[1], "shf": out[2], "lop3_imad_mix": out[3],
                 "imad_hi": hi[0], "imad_wide": hi[1]}
+
+    TRACE_FIELDS = ("stream", "round", "unfinished", "assigned", "speculative", "idle_slots", "newly_done")
+
+    def set_trace(self, cap):
+        """Per-round scheduler trace of the following sign calls (BatchConfig::trace); 0 = off."""
+        self._chk(self.lib.dlb_set_trace(self.ctx, cap), "dlb_set_trace")
+        self._trace_cap = cap
+
+    def get_trace(self):
+        """(records as an (m, 7) uint32 array in TRACE_FIELDS order, records produced)."""
+        buf = np.zeros((max(1, getattr(self, "_trace_cap", 0)), 8), np.uint32)
+        total = self.lib.dlb_get_trace(self.ctx, buf.ctypes.data_as(C.c_void_p), len(buf))
+        if total < 0:
+            raise EngineError("dlb_get_trace failed: %d" % total)
+        return buf[:min(total, len(buf)), :7].copy(), int(total)
 
     def set_mldsa_context(self, context=b""):
         """FIPS 204 context string (<= 255 bytes) for levels 44 / 65 / 87; sticky, default empty."""

@@ -77,7 +77,10 @@ def test_batch_sign_verify(tmp_path, oracle):
     for m in msgs:
         s = (sigs / (m.name + ".sig")).read_bytes()
         assert s == oracle.sign(level, sk.read_bytes(), m.read_bytes())[0]
-    assert trace.read_text().startswith("stream,tasks,rounds,attempts")
+    rows = trace.read_text().strip().splitlines()
+    assert rows[0] == "stream,round,unfinished,assigned,speculative,idle_slots,newly_done"
+    recs = [list(map(int, r.split(","))) for r in rows[1:]]
+    assert sum(r[6] for r in recs) == 12 and all(r[3] >= 1 and r[3] <= r[2] * 9 for r in recs)
     rc, out, _ = run("batch-verify", "--level", level, "--pk", pk, "--sig-dir", sigs, *msgs)
     assert rc == 0 and out.count("accept") == 12
     victim = sigs / (msgs[4].name + ".sig")

@@ -164,3 +164,33 @@ def test_random_batch_shapes(eng, oracle):
         assert st["accepted_attempt_sum"] == int(att.sum()) and st["attempts"] >= st["accepted_attempt_sum"]
         if not spec:
             assert st["speculative"] == 0
+
+
+@pytest.mark.parametrize("level,n,psi,spec", [(2, 3000, 0, True), (3, 700, 512, False), (5, 90, 0, True), (2, 40000, 0, True)])
+def test_round_trace_accounts_for_every_attempt(eng, level, n, psi, spec):
+    """BatchConfig::trace (batch.hpp:27,114; RoundTrace scheduler.hpp:21-28): the per-round
+    records of all CTAs add up to the batch statistics, every CTA's rounds are numbered
+    0, 1, 2, ... and every task is reported done exactly once."""
+    rng = mt19937_64(7300 + n)
+    pk, sk = eng.keygen(level, rng.bytes(32))
+    msgs = np.frombuffer(rng.bytes(32 * n), np.uint8)
+    off = np.arange(n + 1, dtype=np.uint64) * 32
+    ref_sigs = eng.batch_sign(level, np.frombuffer(sk, np.uint8), (msgs, off), psi=psi, speculate=spec)
+    eng.set_trace(1 << 18)
+    try:
+        sigs, att, failed, st = eng.batch_sign(level, np.frombuffer(sk, np.uint8), (msgs, off), psi=psi,
+                                               speculate=spec, return_info=True)
+        recs, total = eng.get_trace()
+    finally:
+        eng.set_trace(0)
+    assert np.array_equal(sigs, ref_sigs)  # tracing never changes an output
+    assert total == len(recs) == st["rounds"]
+    f = {name: recs[:, i].astype(np.int64) for i, name in enumerate(eng.TRACE_FIELDS)}
+    assert f["assigned"].sum() == st["attempts"] and f["speculative"].sum() == st["speculative"]
+    assert f["idle_slots"].sum() == st["idle_slot_rounds"] and f["newly_done"].sum() == n
+    assert (f["assigned"] >= np.minimum(f["unfinished"], 1)).all() and (f["newly_done"] <= f["unfinished"]).all()
+    if not spec:
+        assert (f["speculative"] == 0).all() and (f["assigned"] <= f["unfinished"]).all()
+    for s in np.unique(f["stream"]):
+        rounds = np.sort(f["round"][f["stream"] == s])
+        assert np.array_equal(rounds, np.arange(len(rounds)))

@@ -15,8 +15,9 @@
 //
 // Key and signature files are raw bytes or the hex text written with --out-format hex; the
 // expected object length tells them apart.  --workers is accepted and ignored (the GPU grid
-// replaces the worker pool).  --trace writes the device scheduler's aggregate counters (the
-// persistent kernel has no host-visible rounds to trace one by one).
+// replaces the worker pool).  --trace writes one row per scheduler round with the reference
+// tool's columns; `stream` is the CTA whose round it was (the device scheduler runs one
+// independent round loop per CTA).
 //
 // The option parser is this file's own (the reference uses CLI11, which this tree does not
 // vendor): a table of named options per subcommand, positionals collected in order.
@@ -301,13 +302,23 @@ int cmd_verify(const Args& a) {
   });
 }
 
-void write_trace(const std::string& path, const BatchStats& st, size_t tasks) {
-  if (path.empty()) return;
-  std::ofstream out(path, std::ios::trunc);
-  out << "stream,tasks,rounds,attempts,speculative,idle_slot_rounds,accepted_attempt_sum,failed\n"
-      << 0 << ',' << tasks << ',' << st.rounds << ',' << st.attempts << ',' << st.speculative << ','
-      << st.idle_slot_rounds << ',' << st.accepted_attempt_sum << ',' << st.failed_tasks.size() << '\n';
-}
+// --trace: one CSV row per scheduler round, the reference tool's columns
+// (dilithium_cli.cpp:128-134); `stream` is the CTA that ran the round
+struct TraceFile {
+  std::ofstream out;
+  explicit TraceFile(const std::string& path) {
+    if (path.empty()) return;
+    out.open(path, std::ios::trunc);
+    out << "stream,round,unfinished,assigned,speculative,idle_slots,newly_done\n";
+  }
+  void attach(BatchConfig& cfg) {
+    if (!out.is_open()) return;
+    cfg.trace = [this](const RoundTrace& t) {
+      out << t.stream << ',' << t.round << ',' << t.unfinished << ',' << t.assigned << ',' << t.speculative
+          << ',' << t.idle_slots << ',' << t.newly_done << '\n';
+    };
+  }
+};
 
 int cmd_batch_sign(const Args& a) {
   const bool hex = a.get("--out-format") == "hex";
@@ -339,9 +350,10 @@ int cmd_batch_sign(const Args& a) {
     for (const auto& m : msgs) jobs.push_back({&*pre, m});
     BatchConfig cfg;
     cfg.psi = psi;
+    TraceFile trace(a.get("--trace"));
+    trace.attach(cfg);
     BatchStats st;
     const auto sigs = batch_sign<P>(std::span<const SignJob<P>>(jobs), cfg, &st);
-    write_trace(a.get("--trace"), st, jobs.size());
     if (!st.failed_tasks.empty()) {
       std::cerr << "error: " << st.failed_tasks.size() << " task(s) exhausted the nonce space\n";
       return kBadInput;
@@ -426,6 +438,8 @@ int cmd_bench(const Args& a) {
     for (const auto& m : msgs) jobs.push_back({&*pre, m});
     BatchConfig cfg;
     cfg.psi = psi;
+    TraceFile trace(a.get("--trace"));  // rounds of every timed repetition are appended
+    trace.attach(cfg);
     BatchStats st;
     std::vector<SigBytes<P>> sigs;
     std::cout << "schema,mode,op,level,phi,psi,workers,streams,reps,throughput_ops_s,mean_latency_us,attempts_mean\n";
@@ -448,7 +462,6 @@ int cmd_bench(const Args& a) {
     char att[32];
     std::snprintf(att, sizeof att, "%.3f", double(st.accepted_attempt_sum) / phi);
     row("sign", ts, att);
-    write_trace(a.get("--trace"), st, phi);
     std::vector<VerifyJob<P>> vj(phi);
     for (size_t i = 0; i < phi; ++i) vj[i] = {pk, msgs[i], sigs[i]};
     std::vector<uint8_t> flags;
