@@ -29,6 +29,11 @@ for level in (2, 3, 5):
     pks, sks = eng.batch_keygen(level, zetas)
     rpk, rsk = ref.batch_keygen(level, zetas, workers=cores)
     assert np.array_equal(pks, rpk) and np.array_equal(sks, rsk), "keygen mismatch"
+    nk = min(n, 200000)  # key generation at scale
+    zk = rs.integers(0, 256, (nk, 32), dtype=np.uint8)
+    gpk, gsk = eng.batch_keygen(level, zk)
+    cpk, csk = ref.batch_keygen(level, zk, workers=cores)
+    assert np.array_equal(gpk, cpk) and np.array_equal(gsk, csk), "keygen mismatch (bulk)"
     lens = rs.integers(0, 301, n)
     off = np.zeros(n + 1, np.uint64)
     off[1:] = np.cumsum(lens)
@@ -48,7 +53,7 @@ for level in (2, 3, 5):
     assert np.array_equal(flags, rflags), "verify mismatch"
     assert flags.sum() == n - victims.size
     total += n
-    print("Dilithium%d: %d keys, %d signatures (mean attempts %.3f), %d verdicts (%d corrupted, all rejected) "
-          "identical to the reference; %.1f s" % (level, keys, n, att.mean(), n, victims.size, time.time() - t0),
+    print("Dilithium%d: %d + %d keys, %d signatures (mean attempts %.3f), %d verdicts (%d corrupted, all rejected) "
+          "identical to the reference; %.1f s" % (level, keys, nk, n, att.mean(), n, victims.size, time.time() - t0),
           flush=True)
 print("parity campaign: %d tasks per op, 0 mismatches (reference on %d host threads)" % (total, cores))
