@@ -103,7 +103,7 @@ def test_bench_work_model():
     assert bench.WORK[2]["bytes"]["sign"] == 32 + 2420
 
 
-def test_cli_argument_errors_need_no_gpu():
+def test_cli_argument_errors_need_no_gpu(lib):
     """tools/dilithium_b200 rejects bad command lines with exit code 2 before it ever creates an
     engine (proj/tests/test_cli.cpp:172-175: `keygen --pk a --sk b` without --level fails)."""
     import subprocess
