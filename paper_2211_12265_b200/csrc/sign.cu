@@ -189,9 +189,15 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 // one warp copies `bytes` (multiple of 16, 16-byte aligned) global -> shared, no commit
-__device__ __forceinline__ void warp_fetch(uint8_t* sdst, const void* gsrc, unsigned bytes, int lane) {
+template <unsigned BYTES>
+__device__ __forceinline__ void warp_fetch(uint8_t* sdst, const void* gsrc, int lane) {
+  static_assert(BYTES % 16 == 0, "whole 16-byte pieces");
   const uint8_t* g = static_cast<const uint8_t*>(gsrc);
-  for (unsigned o = lane * 16u; o < bytes; o += 512u) cp_async16(sdst + o, g + o);
+#pragma unroll
+  for (unsigned it = 0; it < (BYTES + 511) / 512; ++it) {  // compile-time trip count, last one predicated
+    const unsigned o = it * 512u + lane * 16u;
+    if ((it + 1) * 512u <= BYTES || o < BYTES) cp_async16(sdst + o, g + o);
+  }
 }
 
 // Raw BITS-wide fields of coefficients lane, lane + 32, ..., lane + 224 of a packed
@@ -221,8 +227,8 @@ __device__ __forceinline__ void stage_w(SignWarpScratch<P>& ws, SlotPipe& pp, co
 #pragma unroll 1
   for (int j = 0; j < P::L; ++j) {
     const uint8_t* cur = pp.ring(pp.k - 1);  // chunk y_j
-    if (j + 1 < P::L) warp_fetch(pp.ring(pp.k), ybytes + (j + 1) * S::Z_POLY, S::Z_POLY, lane);
-    else if (next_y) warp_fetch(pp.ring(pp.k), next_y, S::Z_POLY, lane);
+    if (j + 1 < P::L) warp_fetch<S::Z_POLY>(pp.ring(pp.k), ybytes + (j + 1) * S::Z_POLY, lane);
+    else if (next_y) warp_fetch<S::Z_POLY>(pp.ring(pp.k), next_y, lane);
     cp_async_commit();
     ++pp.k;
     cp_async_wait<1>();
@@ -286,7 +292,7 @@ __device__ __forceinline__ void mul_challenge(int32_t (&out)[8], const int32_t (
 
 // issue the head chunk (the challenge c, 256 bytes) of a slot into pp.head(par); caller commits
 __device__ __forceinline__ void fetch_head(SlotPipe& pp, int par, const int8_t* c8, int lane) {
-  warp_fetch(pp.head(par), c8, kN, lane);
+  warp_fetch<kN>(pp.head(par), c8, lane);
 }
 
 // S4: everything after the challenge (scheme.hpp:165-215) + signature packing into the
@@ -310,17 +316,16 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
   using S = Sizes<P>;
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int R = P::K + P::L;  // ring chunks of a slot: w_0..w_{K-1}, y_0..y_{L-1}
-  auto ring_src = [&](int r) -> const void* {
-    return r < P::K ? static_cast<const void*>(wrows + (size_t)r * kN)
-                    : static_cast<const void*>(ybytes + (r - P::K) * S::Z_POLY);
+  auto ring_fetch = [&](int r) {  // chunk r -> the ring buffer next in line
+    if (r < P::K) warp_fetch<kN * 4>(pp.ring(pp.k), wrows + (size_t)r * kN, lane);
+    else warp_fetch<S::Z_POLY>(pp.ring(pp.k), ybytes + (r - P::K) * S::Z_POLY, lane);
   };
-  auto ring_bytes = [&](int r) -> unsigned { return r < P::K ? kN * 4 : S::Z_POLY; };
 
   // ring chunk 0, then the next slot's head; then wait for everything older (our head).
   // (The buffer it lands in was read by the whole warp while finishing the previous slot;
   // that slot ended on a warp vote -- the explicit barrier states the ordering.)
   __syncwarp();
-  warp_fetch(pp.ring(pp.k), ring_src(0), ring_bytes(0), lane);
+  ring_fetch(0);
   cp_async_commit();
   ++pp.k;
   if (next_c8) fetch_head(pp, par ^ 1, next_c8, lane);
@@ -343,7 +348,7 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
     mul_challenge(t, ch, shat + (size_t)poly * kN, ws.tile, nzs, lane);
     // consume the oldest ring chunk; keep one more in flight behind it
     const uint8_t* cur = pp.ring(pp.k - 1);
-    if (p + 1 < R) warp_fetch(pp.ring(pp.k), ring_src(p + 1), ring_bytes(p + 1), lane);
+    if (p + 1 < R) ring_fetch(p + 1);
     cp_async_commit();
     ++pp.k;
     cp_async_wait<1>();
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
     {
       int s = grab(&sm.cursor2);
       if (s < kSignThreads) {  // prologue: first mask polynomial of the first slot
-        warp_fetch(pp.ring(pp.k), ybytes + (size_t)s * Z::Y_SLOT, S::Z_POLY, lane);
+        warp_fetch<S::Z_POLY>(pp.ring(pp.k), ybytes + (size_t)s * Z::Y_SLOT, lane);
         cp_async_commit();
         ++pp.k;
       }
