@@ -338,21 +338,33 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
   for (int e = 0; e < 8; ++e) ch[e] = reinterpret_cast<const int8_t*>(pp.head(par))[lane + 32 * e];
   ntt_fwd(ch, ws.tile, zs, lane);
 
-  // One loop over the K + L products c*s2_i, c*s1_j (one inverse-NTT instance in the
-  // instruction stream); iteration p consumes ring chunk p.  Every exit is warp-uniform.
+  // One loop over the K + L + K products c*s2_i, c*s1_j, c*t0_i: a single inverse-NTT
+  // instance in the instruction stream (the kernel is sensitive to code size: every extra
+  // copy of a transform costs instruction-cache misses in all stages).  Iterations p < R
+  // consume ring chunk p; the t0 rows read w - c s2 back from the slot's scratch.  Every
+  // exit is warp-uniform.
   //   r0 = LowBits(w - c s2), ||r0|| < gamma2 - beta            (scheme.hpp:177-190)
   //   z = y + c s1, ||z|| < gamma1 - beta                      (scheme.hpp:167-174)
+  //   ||c t0|| < gamma2, h = [HB(w - c s2 + c t0) != HB(w - c s2)]   (scheme.hpp:192-215)
+  unsigned weight = 0;
 #pragma unroll 1
-  for (int p = 0; p < R; ++p) {
-    const int poly = p < P::K ? P::L + p : p - P::K;  // shat order: s1 (L), s2 (K), t0 (K)
+  for (int p = 0; p < R + P::K; ++p) {
+    // shat order: s1 (L), s2 (K), t0 (K); visiting order: s2 rows, s1 rows, t0 rows
+    const int poly = p < P::K ? P::L + p : (p < R ? p - P::K : p - R + P::L + P::K);
+    int32_t wcs2[8];
+    if (p >= R) {  // issue the read-back before the transform hides its latency
+#pragma unroll
+      for (int e = 0; e < 8; ++e) wcs2[e] = wrows[(size_t)(p - R) * kN + lane + 32 * e];
+    }
     mul_challenge(t, ch, shat + (size_t)poly * kN, ws.tile, nzs, lane);
-    // consume the oldest ring chunk; keep one more in flight behind it
     const uint8_t* cur = pp.ring(pp.k - 1);
-    if (p + 1 < R) ring_fetch(p + 1);
-    cp_async_commit();
-    ++pp.k;
-    cp_async_wait<1>();
-    __syncwarp();
+    if (p < R) {  // consume the oldest ring chunk; keep one more in flight behind it
+      if (p + 1 < R) ring_fetch(p + 1);
+      cp_async_commit();
+      ++pp.k;
+      cp_async_wait<1>();
+      __syncwarp();
+    }
     // The exact product c*s1 has coefficients in [-beta, beta] (tau non-zero challenge
     // entries times eta) and c*t0 in (-2^22, 2^22), so the inverse NTT's output in (-q, q) is
     // that small value or the same +-q: reduce32 returns the centred value itself.
@@ -362,13 +374,13 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
       int32_t* wdst = wrows + (size_t)p * kN;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int32_t wcs2 = freeze(wrow[lane + 32 * e] - t[e]);
+        const int32_t d = freeze(wrow[lane + 32 * e] - t[e]);
         int32_t r0;
-        decompose<P::GAMMA2>(wcs2, r0);
+        decompose<P::GAMMA2>(d, r0);
         bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
-        wdst[lane + 32 * e] = wcs2;  // read back by this same lane in the hint phase
+        wdst[lane + 32 * e] = d;  // read back by this same lane in the hint phase
       }
-    } else {
+    } else if (p < R) {
       uint32_t raw[8];
       unpack_strided<P::Z_BITS>(cur, lane, raw);
 #pragma unroll
@@ -378,27 +390,16 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
         bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
         ws.vhat[p - P::K][e][lane] = z;
       }
-    }
-    if (__any_sync(FULL, bad)) return false;
-  }
-
-  //   ||c t0|| < gamma2, h = [HB(w - c s2 + c t0) != HB(w - c s2)]   (scheme.hpp:192-215)
-  unsigned weight = 0;
-#pragma unroll 1
-  for (int i = 0; i < P::K; ++i) {
-    int32_t wcs2[8];
+    } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) wcs2[e] = wrows[(size_t)i * kN + lane + 32 * e];
-    mul_challenge(t, ch, shat + (size_t)(P::L + P::K + i) * kN, ws.tile, nzs, lane);
-    bool bad = false;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int32_t vt = reduce32(t[e]);  // |c t0| <= tau * 2^12 < 2^22: already centred
-      bad = bad || abs(vt) >= P::GAMMA2;
-      const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != highbits<P::GAMMA2>(wcs2[e]);
-      const unsigned mask = __ballot_sync(FULL, h);
-      if (lane == 0) ws.hbits[i][e] = mask;
-      weight += __popc(mask);
+      for (int e = 0; e < 8; ++e) {
+        const int32_t vt = reduce32(t[e]);  // |c t0| <= tau * 2^12 < 2^22: already centred
+        bad = bad || abs(vt) >= P::GAMMA2;
+        const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != highbits<P::GAMMA2>(wcs2[e]);
+        const unsigned mask = __ballot_sync(FULL, h);
+        if (lane == 0) ws.hbits[p - R][e] = mask;
+        weight += __popc(mask);
+      }
     }
     if (__any_sync(FULL, bad)) return false;
   }
