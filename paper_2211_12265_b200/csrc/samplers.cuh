@@ -211,7 +211,9 @@ __device__ __forceinline__ void sample_in_ball_words(const uint64_t (&ct)[CTW],
       uint64_t v = s[0];
 #pragma unroll
       for (int k = 1; k < kWords256; ++k) v = (w == k) ? s[k] : v;  // register select, no local mem
-#pragma unroll
+      // (the byte walk is only two-way unrolled: it runs ~60 times per challenge, and the signing
+      // kernel gains more from the smaller code than it loses in loop overhead)
+#pragma unroll 2
       for (int e = 0; e < 8; ++e) {
         const unsigned b = (unsigned)(v >> (8 * e)) & 0xFF;
         if (i < (unsigned)kN && b <= i) {
