@@ -9,17 +9,20 @@
 // the 32 lanes onto 32 distinct banks).  No butterfly ever crosses lanes, so the last
 // levels need neither shuffles nor block barriers (only __syncwarp around the tile).
 //
-// Forward:  in  r[i] = a[lane + 32 i]      out r[m] = A[8 lane + m]   (|A| < |a|max + 8q)
+// Forward:  in  r[i] = a[lane + 32 i]      out r[m] = A[8 lane + m]   (|A| < |a|max + 10q)
 // Inverse:  in  r[m] = A[8 lane + m], |A| < q   out r[i] = a[lane + 32 i], |a| < q
-// The inverse's last level multiplies by n^-1 * R (kInvC*R variants), cancelling the
-// R^-1 left by a pointwise Montgomery product of two plain-domain operands, so no
-// operand is ever converted to Montgomery form.
+// Butterfly products use plain twiddles with a precomputed quotient (twiddle_mul: result in
+// (-q/4, 5q/4)); sums double per inverse level exactly as in the reference's lazy transform
+// (< 2^8 q < 2^31).  The inverse's last level is a Montgomery product by n^-1 * R^2
+// (DLB_INTT_C*R): it brings the result back into (-q, q) and cancels the R^-1 left by a
+// pointwise Montgomery product of two plain-domain operands, so no operand is ever
+// converted to Montgomery form.
 #pragma once
 #include "common.cuh"
 
 namespace dlb {
 
-static __device__ __constant__ int2 c_zeta[256] = DLB_ZETA_TABLE;    // (z*R mod q, that * q^-1)
+static __device__ __constant__ int2 c_zeta[256] = DLB_ZETA_TABLE;    // (z centred, round(z 2^32 / q))
 static __device__ __constant__ int2 c_nzeta[256] = DLB_NZETA_TABLE;  // (-z) likewise
 
 constexpr int kTileWords = 288;  // 256 + 4*7 padded, rounded up
@@ -34,8 +37,17 @@ __device__ __forceinline__ void load_twiddles(int2* zs, int2* nzs) {
   }
 }
 
+// a * z mod q for a twiddle pair (z, z' = round(z 2^32 / q)), |z| <= q/2, any |a| < 2^31:
+// h = floor(a z' / 2^32) is floor(a z / q + e) with |e| < 1/4, so a z - h q lies in
+// (-q/4, 5q/4) and fits a word.  One half-rate IMAD.HI and two 32-bit IMADs: on sm_100a the
+// 32-bit IMADs co-issue with the butterfly's add / sub, which the 64-bit-result IMADs of a
+// Montgomery product do not (profiles/r01_summary.md section 3: 8.7 against 10.7 clocks).
+__device__ __forceinline__ int32_t twiddle_mul(int32_t a, int2 z) {
+  return a * z.x - __mulhi(a, z.y) * kQ;
+}
+
 __device__ __forceinline__ void ct_bfly(int32_t& a, int32_t& b, int2 z) {
-  const int32_t t = mont_mul_pre(b, z.x, z.y);
+  const int32_t t = twiddle_mul(b, z);
   b = a - t;
   a = a + t;
 }
@@ -43,7 +55,7 @@ __device__ __forceinline__ void ct_bfly(int32_t& a, int32_t& b, int2 z) {
 __device__ __forceinline__ void gs_bfly(int32_t& a, int32_t& b, int2 z) {
   const int32_t t = a;
   a = t + b;
-  b = mont_mul_pre(t - b, z.x, z.y);
+  b = twiddle_mul(t - b, z);
 }
 
 __device__ __forceinline__ void ntt_fwd(int32_t (&r)[8], int32_t* tile, const int2* zs, int lane) {

@@ -1,7 +1,4 @@
 cd /root/repo
 export DLB_NO_PEAK=1
-SIZES=100000,1000000 VARIANTS="ku2 ku3" bash scripts/runs/ab.sh
-for v in "" ku2 ku3; do
-  if [ -z "$v" ]; then unset DLB_LIB; else export DLB_LIB=$PWD/paper_2211_12265_b200/libdilithium_b200_$v.so; fi
-  echo "== keygen/verify ${v:-default}"; timeout 300 python scripts/perf_probe.py 2 100000 keygen,verify 5 2>&1 | grep -E "keygen|verify" | cut -c1-80
-done
+timeout 1200 python -m pytest tests/test_gpu_primitives.py tests/test_gpu_sign.py tests/test_gpu_keygen_verify.py tests/test_gpu_edges.py tests/test_gpu_mldsa.py -m gpu -x -q 2>&1 | tail -3
+LEVELS=2,3,5 SIZES=100000,1000000 VARIANTS=prev bash scripts/runs/ab.sh
