@@ -138,7 +138,7 @@ __device__ __forceinline__ int32_t mont_reduce64(int64_t p) {
   return mont_fold(p, t);
 }
 
-// same with the constant operand's b*qinv supplied (twiddles): IMAD + 2 IMAD.WIDE
+// same with the constant operand's b*qinv supplied (last inverse-NTT level): IMAD + 2 IMAD.WIDE
 __device__ __forceinline__ int32_t mont_mul_pre(int32_t a, int32_t b, int32_t bq) {
   const int32_t t = a * bq;
   int64_t p;
