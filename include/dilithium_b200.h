@@ -194,7 +194,9 @@ int dlb_dbg_sample_in_ball(dlb_ctx* ctx, int level, size_t n, const uint8_t* c_t
  * Decompose high, low; UseHint with hint 0, hint 1. */
 int dlb_dbg_rounding(dlb_ctx* ctx, int gamma2_divisor, int32_t first, size_t n, int32_t* out6);
 /* forward NTT (output canonical [0,q)) and inverse NTT of canonical input (output
- * canonical): value-level parity with ntt.hpp:74-126 */
+ * canonical): value-level parity with ntt.hpp:74-126.  inverse = 2: the input is used as
+ * given, any signed representatives in (-q, q) -- the range the kernels feed the inverse
+ * transform with; exercises the lazy-reduction bound on its worst case. */
 int dlb_dbg_ntt(dlb_ctx* ctx, size_t n, int32_t* polys /* n*256 in place */, int inverse);
 /* sign_attempt<P> (scheme.hpp:225-230): one rejection-loop iteration per task at kappa[i].
  * accepted[i] 0/1; c_tilde n*32; z n*L*256 centered; hints n*K*256 -- the latter two

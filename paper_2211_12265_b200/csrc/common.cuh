@@ -96,25 +96,11 @@ static_assert(Sizes<Params<87>>::PK == 2592 && Sizes<Params<87>>::SK == 4896 &&
 
 // ---- Montgomery arithmetic, R = 2^32 (values as reduce.hpp:44-51) ---------------
 
-// a*b*R^-1 mod q in (-q, q); needs |a*b| < 2^31 q.  Written on 64-bit products so it
-// compiles to IMAD.WIDE / IMAD / IMAD.WIDE: on sm_100a IMAD.WIDE issues at the full
-// fma-pipe rate while IMAD.HI (mul.hi) runs at half rate (measured: 18.5 vs 9.25
-// Tlane-op/s, dlb_measure_imad_hi_peak), so the high word is taken from a wide
-// multiply-add whose low word cancels by construction.
-#ifndef DLB_MONT_WIDE
-#define DLB_MONT_WIDE 0
-#endif
+// a*b*R^-1 mod q in (-q, q); needs |a*b| < 2^31 q.  With t = lo(p) * q^-1 the low words of p
+// and t*q are equal, so (p - t*q) / 2^32 is exactly hi(p) - hi(t*q): one IMAD.HI and one
+// subtraction, no carry chain (a 64-bit `mad.wide` of -q onto p compiles to five instructions).
 __device__ __forceinline__ int32_t mont_fold(int64_t p, int32_t t) {
-  int64_t r;  // p - t*q as one wide multiply-add (kept opaque so it is not split into IMAD.HI)
-  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(t), "r"(-kQ), "l"(p));
-  // The low word is zero by construction; OR-ing it in keeps both halves live so the
-  // full-rate IMAD.WIDE is emitted instead of the half-rate IMAD.HI (one LOP3 on the
-  // otherwise idle alu pipe buys back one fma-pipe slot per product).
-#if DLB_MONT_WIDE
-  return (int32_t)(r >> 32) | (int32_t)r;
-#else
-  return (int32_t)(r >> 32);
-#endif
+  return (int32_t)(p >> 32) - __mulhi(t, kQ);
 }
 
 __device__ __forceinline__ int32_t mont_mul(int32_t a, int32_t b) {
@@ -128,9 +114,9 @@ __device__ __forceinline__ int32_t mont_mul(int32_t a, int32_t b) {
 // matrix-vector product costs L IMAD.WIDE + 2 instead of L full Montgomery products.
 // |acc| must stay below 2^31 q: L <= 7 terms of |a| < 2^23 times |b| < 2^27.
 __device__ __forceinline__ int64_t mac_wide(int64_t acc, int32_t a, int32_t b) {
-  int64_t r;
-  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(acc));
-  return r;
+  // plain C++: ptxas keeps this as one IMAD.WIDE with a 64-bit addend, while the same
+  // operation written as inline `mad.wide.s32` is split into IMAD.WIDE + IADD3 + IMAD.X
+  return acc + (int64_t)a * (int64_t)b;
 }
 
 __device__ __forceinline__ int32_t mont_reduce64(int64_t p) {

@@ -135,7 +135,7 @@ __global__ void k_dbg_ntt(unsigned n, int32_t* polys, int inverse) {
   } else {
     // the inverse carries an extra factor R (see ntt.cuh); undo it for the value test
 #pragma unroll
-    for (int m = 0; m < 8; ++m) r[m] = center(a[8 * lane + m]);
+    for (int m = 0; m < 8; ++m) r[m] = inverse == 2 ? a[8 * lane + m] : center(a[8 * lane + m]);
     ntt_inv(r, tiles[warp], nzs, lane);
 #pragma unroll
     for (int i = 0; i < 8; ++i) a[lane + 32 * i] = freeze(mont_mul(r[i], 1));

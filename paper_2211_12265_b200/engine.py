@@ -348,7 +348,7 @@ class Engine:
 
     def dbg_ntt(self, polys, inverse=False):
         p = np.ascontiguousarray(polys, np.int32).reshape(-1, 256).copy()
-        self._chk(self.lib.dlb_dbg_ntt(self.ctx, len(p), p.ctypes.data_as(_i32p), 1 if inverse else 0), "ntt")
+        self._chk(self.lib.dlb_dbg_ntt(self.ctx, len(p), p.ctypes.data_as(_i32p), int(inverse)), "ntt")
         return p
 
     def dbg_sign_attempt(self, level, sks, mus, rho_primes, kappas):

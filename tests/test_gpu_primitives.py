@@ -124,6 +124,30 @@ def test_ntt_values(eng, oracle):
         assert np.array_equal(b[i], oracle.intt(a[i])), i
 
 
+def test_inverse_ntt_lazy_bound_worst_case(eng, oracle):
+    """The inverse transform reduces nothing between levels: sums double eight times, so inputs
+    in (-q, q) reach 2^8 * q < 2^31 on the all-sums path (ntt.hpp:92-110 relies on the same
+    bound).  Feed the representatives that maximise every partial sum -- all +(q-1), all
+    -(q-1), sign patterns of each butterfly stride, random signed -- and compare values."""
+    rng = np.random.default_rng(11)
+    rows = [np.full(256, Q - 1), np.full(256, -(Q - 1))]
+    idx = np.arange(256)
+    for stride in (1, 2, 4, 8, 16, 32, 64, 128):
+        sign = np.where((idx // stride) % 2 == 0, 1, -1)
+        rows += [sign * (Q - 1), -sign * (Q - 1)]
+    rows += [rng.integers(-(Q - 1), Q, 256) for _ in range(40)]
+    rows += [rng.choice([-(Q - 1), Q - 1], 256) for _ in range(40)]
+    a = np.array(rows, dtype=np.int32)
+    got = eng.dbg_ntt(a, inverse=2)
+    for i in range(len(a)):
+        assert np.array_equal(got[i], oracle.intt((a[i].astype(np.int64) % Q).astype(np.int32))), i
+    # forward transform of the largest inputs the kernels feed it: t1 * 2^13 (up to 1023 << 13)
+    big = np.array([np.full(256, 1023 << 13), rng.integers(0, 1024, 256) << 13], dtype=np.int32)
+    f = eng.dbg_ntt(big)
+    for i in range(len(big)):
+        assert np.array_equal(f[i], oracle.ntt((big[i].astype(np.int64) % Q).astype(np.int32))), i
+
+
 @pytest.mark.parametrize("divisor", [88, 32])
 def test_rounding_exhaustive(eng, oracle, divisor):
     """Power2Round, Decompose and UseHint on the device for EVERY r in [0, q)
