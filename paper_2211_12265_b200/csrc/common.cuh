@@ -139,8 +139,16 @@ __device__ __forceinline__ int32_t reduce32(int32_t a) {
   return a - t * kQ;
 }
 
-// (-q, q) -> [0, q)
-__device__ __forceinline__ int32_t caddq(int32_t a) { return a + ((a >> 31) & kQ); }
+// [-q, 2^31 - q) -> a + q if negative: as unsigned numbers the wrong candidate is the huge
+// one, so an unsigned minimum picks the representative (two instructions, no mask)
+__device__ __forceinline__ int32_t caddq(int32_t a) {
+  return (int32_t)min((uint32_t)a, (uint32_t)(a + kQ));
+}
+
+// (-q, 2q) -> [0, q): the one candidate of a - q, a, a + q that is not negative or too large
+__device__ __forceinline__ int32_t freeze_near(int32_t a) {
+  return (int32_t)min(min((uint32_t)a, (uint32_t)(a + kQ)), (uint32_t)(a - kQ));
+}
 
 // any int32 -> canonical [0, q)
 __device__ __forceinline__ int32_t freeze(int32_t a) { return caddq(reduce32(a)); }

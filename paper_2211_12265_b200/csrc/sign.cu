@@ -370,7 +370,7 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
       int32_t* wdst = wrows + (size_t)p * kN;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int32_t d = freeze(wrow[lane + 32 * e] - t[e]);
+        const int32_t d = freeze_near(wrow[lane + 32 * e] - t[e]);  // [0, q) - (-q, q)
         int32_t r0;
         decompose<P::GAMMA2>(d, r0);
         bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
@@ -391,7 +391,7 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
       for (int e = 0; e < 8; ++e) {
         const int32_t vt = reduce32(t[e]);  // |c t0| <= tau * 2^12 < 2^22: already centred
         bad = bad || abs(vt) >= P::GAMMA2;
-        const int h = highbits<P::GAMMA2>(freeze(wcs2[e] + vt)) != highbits<P::GAMMA2>(wcs2[e]);
+        const int h = highbits<P::GAMMA2>(freeze_near(wcs2[e] + vt)) != highbits<P::GAMMA2>(wcs2[e]);
         const unsigned mask = __ballot_sync(FULL, h);
         if (lane == 0) ws.hbits[p - R][e] = mask;
         weight += __popc(mask);
