@@ -173,7 +173,7 @@ __device__ __forceinline__ int32_t decompose(int32_t a, int32_t& a0) {
     a1 &= 15;
   } else {
     a1 = (a1 * 11275 + (1 << 23)) >> 24;
-    a1 ^= ((43 - a1) >> 31) & a1;
+    a1 = (int32_t)min((uint32_t)a1, (uint32_t)(a1 - 44));  // a1 in [0, 44]: 44 -> 0
   }
   a0 = a - a1 * 2 * GAMMA2;
   a0 -= (((kQ - 1) / 2 - a0) >> 31) & kQ;
