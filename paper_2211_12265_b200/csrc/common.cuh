@@ -142,12 +142,14 @@ __device__ __forceinline__ int32_t reduce32(int32_t a) {
 // [-q, 2^31 - q) -> a + q if negative: as unsigned numbers the wrong candidate is the huge
 // one, so an unsigned minimum picks the representative (two instructions, no mask)
 __device__ __forceinline__ int32_t caddq(int32_t a) {
-  return (int32_t)min((uint32_t)a, (uint32_t)(a + kQ));
+  const uint32_t u = (uint32_t)a;
+  return (int32_t)min(u, u + (uint32_t)kQ);
 }
 
 // (-q, 2q) -> [0, q): the one candidate of a - q, a, a + q that is not negative or too large
 __device__ __forceinline__ int32_t freeze_near(int32_t a) {
-  return (int32_t)min(min((uint32_t)a, (uint32_t)(a + kQ)), (uint32_t)(a - kQ));
+  const uint32_t u = (uint32_t)a;
+  return (int32_t)min(min(u, u + (uint32_t)kQ), u - (uint32_t)kQ);
 }
 
 // any int32 -> canonical [0, q)
@@ -173,7 +175,7 @@ __device__ __forceinline__ int32_t decompose(int32_t a, int32_t& a0) {
     a1 &= 15;
   } else {
     a1 = (a1 * 11275 + (1 << 23)) >> 24;
-    a1 = (int32_t)min((uint32_t)a1, (uint32_t)(a1 - 44));  // a1 in [0, 44]: 44 -> 0
+    a1 = (int32_t)min((uint32_t)a1, (uint32_t)a1 - 44u);  // a1 in [0, 44]: 44 -> 0
   }
   a0 = a - a1 * 2 * GAMMA2;
   a0 -= (((kQ - 1) / 2 - a0) >> 31) & kQ;
