@@ -27,6 +27,9 @@
 #include "samplers.cuh"
 #include "verify_keygen.cuh"
 
+#ifndef DLB_R0_MIN
+#define DLB_R0_MIN 0
+#endif
 namespace dlb {
 
 #ifndef DLB_SIGN_MINB
@@ -368,14 +371,29 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
     if (p < P::K) {
       const int32_t* wrow = reinterpret_cast<const int32_t*>(cur);
       int32_t* wdst = wrows + (size_t)p * kN;
+#if DLB_R0_MIN
+      uint32_t worst = 0;
+#endif
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int32_t d = freeze_near(wrow[lane + 32 * e] - t[e]);  // [0, q) - (-q, q)
+#if DLB_R0_MIN
+        // |r0| < B without materialising the centred r0: a0 = d - r1 * 2 gamma2 is r0 or, when
+        // HighBits wrapped to 0, r0 + q; shifted by B - 1 the valid one lands in [0, 2B - 1)
+        constexpr int32_t B = P::GAMMA2 - P::BETA;
+        const int32_t a0 = d - highbits<P::GAMMA2>(d) * 2 * P::GAMMA2;
+        const uint32_t u = (uint32_t)(a0 + B - 1);
+        worst = max(worst, min(u, u - (uint32_t)kQ));
+#else
         int32_t r0;
         decompose<P::GAMMA2>(d, r0);
         bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
+#endif
         wdst[lane + 32 * e] = d;  // read back by this same lane in the hint phase
       }
+#if DLB_R0_MIN
+      bad = worst >= 2u * (P::GAMMA2 - P::BETA) - 1u;
+#endif
     } else if (p < R) {
       uint32_t raw[8];
       unpack_strided<P::Z_BITS>(cur, lane, raw);
