@@ -38,6 +38,8 @@ extern "C" {
 #define DLB_E_LEVEL (-2)
 #define DLB_E_KEY (-3)
 #define DLB_E_NOMEM (-4)
+#define DLB_E_BUSY (-5)     /* 16 signing batches already in flight: wait for the oldest first */
+#define DLB_E_INTERNAL (-6) /* a submitted batch was never completed (device fault) */
 
 typedef struct dlb_ctx dlb_ctx;
 
@@ -91,6 +93,19 @@ typedef struct dlb_round_trace {
 } dlb_round_trace;
 int dlb_set_trace(dlb_ctx* ctx, size_t cap);
 long long dlb_get_trace(dlb_ctx* ctx, dlb_round_trace* out, size_t max_records);
+
+/* Per-attempt execution log (BatchConfig::assignment_hook, batch.hpp:28,87-88; Assignment
+ * scheduler.hpp:14-19): one record per (task, attempt) the device scheduler actually ran,
+ * speculative ones included.  `slot` is the global attempt slot (CTA * 128 + slot in the CTA),
+ * `kappa` the first mask nonce of the attempt (attempt * l).  dlb_set_assignment_log(ctx, cap):
+ * the next synchronous sign calls log up to cap records (0 = off, the default; logging costs
+ * one atomic and one 16-byte store per executed attempt).  dlb_get_assignment_log copies the
+ * records of the last sign call, in no particular order, and returns how many it produced. */
+typedef struct dlb_assignment {
+  uint32_t slot, task, attempt, kappa;
+} dlb_assignment;
+int dlb_set_assignment_log(dlb_ctx* ctx, size_t cap);
+long long dlb_get_assignment_log(dlb_ctx* ctx, dlb_assignment* out, size_t max_records);
 
 /* FIPS 204 context string for the ML-DSA levels (44 / 65 / 87): signing and verification
  * hash M' = 0 || len || ctx || M.  len <= 255; the default is the empty string.  Sticky per
@@ -153,6 +168,32 @@ int dlb_verify_batch_keyed(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t
                            const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
                            const uint8_t* sigs, uint8_t* flags);
 
+/* Batches in flight --------------------------------------------------------------------
+ * The paper keeps several batches in flight per GPU (the reference
+ * tool's engines, tools/dilithium_cli.cpp:309-345).  dlb_sign_submit enqueues a batch and
+ * returns at once with a ticket; dlb_sign_wait blocks until that batch is complete and fills
+ * the outputs.  Up to 16 batches may be in flight per context (DLB_E_BUSY beyond).  The device
+ * scheduler is shared: CTAs that run out of tasks of one batch claim tasks of the next
+ * submitted batches (of the same level) before they speculate, so the rejection-loop tail of a
+ * batch overlaps the body of its successors.  Output bytes never depend on what else is in
+ * flight.  Arguments as dlb_sign_batch / dlb_sign_batch_keyed (key_idx == NULL: sk_stride 0 =
+ * one shared key, else one key per task; key_idx != NULL: a table of n_keys keys, sk_stride
+ * = sk_bytes).  All input and output buffers must stay valid until the wait returns; a
+ * signature buffer in pinned memory (dlb_host_alloc) is written in place by the device.
+ * *ticket == 0 means the batch was empty (waiting on it returns at once).  Tickets may be
+ * waited in any order.  The synchronous calls above are submit + wait. */
+int dlb_sign_submit(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t* sks, size_t sk_stride,
+                    size_t n, const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+                    const uint8_t* rho_prime_override, size_t psi, int speculate, uint8_t* sigs,
+                    uint32_t* attempts, uint8_t* failed, uint64_t* ticket);
+int dlb_sign_wait(dlb_ctx* ctx, uint64_t ticket, dlb_sign_stats* stats);
+/* The same with every buffer in device memory. */
+int dlb_sign_submit_dev(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t* d_sks, size_t sk_stride,
+                        size_t n, const uint32_t* d_key_idx, const uint8_t* d_msgs,
+                        const uint64_t* d_msg_off, const uint8_t* d_rho_prime_override, size_t psi,
+                        int speculate, uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed,
+                        uint64_t* ticket);
+
 /* Device-resident variants -------------------------------------------------------------
  * Same contracts with every buffer already in device memory (HBM); no copies are made.
  * Used for kernel-only timing and by callers that keep keys/messages on the GPU. */
@@ -205,6 +246,20 @@ int dlb_dbg_sign_attempt(dlb_ctx* ctx, int level, size_t n, const uint8_t* sks, 
                          const uint8_t* mus /* n*64 */, const uint8_t* rho_primes /* n*64 */,
                          const uint32_t* kappas, uint8_t* accepted, uint8_t* c_tilde, int32_t* z,
                          int32_t* hints);
+
+/* detail::sign_attempt_bounded<P> (scheme.hpp:133-219): the same with the three norm bounds
+ * injected (tests force individual reject stages through them; each must be in [0, (q-1)/8],
+ * rounding.hpp:65).  stage[i]: 255 accepted, else the RejectStage (scheme.hpp:34) the reference
+ * reports -- the first failing check in its order: 0 ZNorm, 1 R0Norm, 2 VtNorm, 3 HintWeight. */
+int dlb_dbg_sign_attempt_bounded(dlb_ctx* ctx, int level, size_t n, const uint8_t* sks,
+                                 size_t sk_stride, const uint8_t* mus, const uint8_t* rho_primes,
+                                 const uint32_t* kappas, int32_t z_bound, int32_t r0_bound,
+                                 int32_t vt_bound, uint8_t* accepted, uint8_t* stage, uint8_t* c_tilde,
+                                 int32_t* z, int32_t* hints);
+/* Shrinks the nonce space of the following sign calls: a task whose attempts 0 .. max_attempt
+ * all fail is reported failed (scheduler.hpp:52,122-128 -- the real limit, (65535 - (l-1)) / l,
+ * is never reached by honest inputs).  0 restores the scheme's limit. */
+int dlb_dbg_set_max_attempt(dlb_ctx* ctx, unsigned max_attempt);
 
 #ifdef __cplusplus
 }

@@ -201,14 +201,56 @@ __device__ __forceinline__ int32_t use_hint(int h, int32_t r) {
 
 // ---- small utilities -----------------------------------------------------------
 
+// Coherent ("weak", L1-cacheable) global loads that the compiler may not turn into the
+// read-only ld.global.nc form.  The signing scheduler reads data of batches that were
+// published after its kernel started; each CTA orders those reads behind an acquire load of the
+// batch's gate word (which also drops stale L1 lines), a guarantee the non-coherent path is
+// outside of.  Not volatile: the loads may be scheduled freely behind their address.
+__device__ __forceinline__ uint64_t ld_weak(const uint64_t* p) {
+  uint64_t v;
+  asm("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_weak(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ld_weak(const int4* p) {
+#ifdef DLB_AB_LDG
+  return __ldg(p);  // A/B measurement only: the non-coherent path is not safe here
+#endif
+  int4 v;
+  asm("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint8_t ld_weak(const uint8_t* p) {
+  uint32_t v;
+  asm("ld.global.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return (uint8_t)v;
+}
+
 // unaligned little-endian loads from global memory (byte-granular key/sig/msg offsets)
+// (NC = false: coherent loads, see ld_weak)
+template <bool NC = true>
 __device__ __forceinline__ uint32_t load_u32_unaligned(const uint8_t* p) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
   const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
   const unsigned sh = (a & 3) * 8;
-  const uint32_t lo = __ldg(w);
+  const uint32_t lo = NC ? __ldg(w) : ld_weak(w);
   if (sh == 0) return lo;
-  return __funnelshift_r(lo, __ldg(w + 1), sh);
+  return __funnelshift_r(lo, NC ? __ldg(w + 1) : ld_weak(w + 1), sh);
 }
 
 // bits [bit, bit+width) of an LSB-first little-endian stream, width <= 24.

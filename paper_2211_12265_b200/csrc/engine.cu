@@ -162,16 +162,7 @@ extern "C" {
 
 const char* dlb_version(void) { return "dilithium-b200 0.1 (sm_100a)"; }
 
-int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
-  (void)max_batch;
-  if (!out) return DLB_E_ARG;
-  int count = 0;
-  cudaError_t e = cudaGetDeviceCount(&count);
-  if (e != cudaSuccess) return -1000 - (int)e;
-  if (device < 0 || device >= count) return DLB_E_ARG;
-  DLB_CUDA_CHECK(cudaSetDevice(device));
-  dlb_ctx* c = new dlb_ctx();
-  c->device = device;
+static int create_resources(dlb_ctx* c) {
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
@@ -182,12 +173,37 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
   DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev0));
   DLB_CUDA_CHECK(cudaEventCreate(&c->ev1));
-  DLB_CUDA_CHECK(cudaEventCreate(&c->ev2));
-  DLB_CUDA_CHECK(cudaEventCreate(&c->ev3));
   for (int b = 0; b < 2; ++b) {
     DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in[b], cudaEventDisableTiming));
     DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_comp[b], cudaEventDisableTiming));
     DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_out[b], cudaEventDisableTiming));
+  }
+  return 0;
+}
+
+int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
+  if (!out) return DLB_E_ARG;
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess) return -1000 - (int)e;
+  if (device < 0 || device >= count) return DLB_E_ARG;
+  DLB_CUDA_CHECK(cudaSetDevice(device));
+  dlb_ctx* c = new dlb_ctx();
+  c->device = device;
+  c->max_batch_hint = max_batch;
+  // tuning knobs for the sweeps recorded in profiles/: read once, here
+  if (const char* v = getenv("DLB_SPEC_DEPTH")) c->knob_spec_depth = (unsigned)atoi(v);
+  if (const char* v = getenv("DLB_CHUNK")) c->knob_chunk = (size_t)atol(v);
+  if (const char* v = getenv("DLB_PIPE_CHUNK")) c->knob_pipe_chunk = (size_t)atol(v);
+  if (const char* v = getenv("DLB_SIGN_PAD_SMEM")) c->knob_sign_pad_smem = (size_t)atol(v);
+  if (const char* v = getenv("DLB_CARVEOUT")) c->knob_carveout = atoi(v);
+  if (const char* v = getenv("DLB_SIGN_OCC")) c->knob_sign_occ = (unsigned)atoi(v);
+  if (const char* v = getenv("DLB_KEY_CACHE")) c->knob_key_cache = (size_t)atol(v);
+  const int rc = create_resources(c);
+  if (rc != 0) {
+    dlb_destroy(c);  // tolerates the handles that were never created
+    return rc;
   }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   *out = c;
@@ -198,27 +214,66 @@ void dlb_destroy(dlb_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  // secret material (keys, their transforms, rho', masks) lives in these arenas: wipe before release
   for (auto& kv : c->dev)
-    if (kv.second.p) cudaFree(kv.second.p);
+    if (kv.second.p) {
+      cudaMemset(kv.second.p, 0, kv.second.cap);
+      cudaFree(kv.second.p);
+    }
   for (auto& kv : c->pinned)
-    if (kv.second.p) cudaFreeHost(kv.second.p);
-  cudaEventDestroy(c->ev0);
-  cudaEventDestroy(c->ev1);
-  cudaEventDestroy(c->ev2);
-  cudaEventDestroy(c->ev3);
-  for (int b = 0; b < 2; ++b) {
-    cudaEventDestroy(c->ev_in[b]);
-    cudaEventDestroy(c->ev_comp[b]);
-    cudaEventDestroy(c->ev_out[b]);
+    if (kv.second.p) {
+      memset(kv.second.p, 0, kv.second.cap);
+      cudaFreeHost(kv.second.p);
+    }
+  for (auto& e : c->key_cache) {
+    if (e.A) {
+      cudaMemset(e.A, 0, 8 * 7 * kN * 4);
+      cudaFree(e.A);
+    }
+    if (e.shat) {
+      cudaMemset(e.shat, 0, (7 + 2 * 8) * kN * 4);
+      cudaFree(e.shat);
+    }
+    if (e.ready) cudaEventDestroy(e.ready);
+    if (!e.sk.empty()) memset(e.sk.data(), 0, e.sk.size());
   }
-  for (int b = 0; b < 2; ++b) {
-    cudaStreamDestroy(c->lane_s[b]);
-    cudaEventDestroy(c->ev_join[b]);
+  if (c->sign_ready) {
+    cudaFree(c->d_ring);
+    cudaFree(c->d_log);
+    cudaFreeHost(c->h_ring);
+    cudaFreeHost((void*)c->h_flags);
+    for (int l = 0; l < kLanes; ++l) {
+      if (c->sign_lane[l]) cudaStreamDestroy(c->sign_lane[l]);
+      if (c->lane_done[l]) cudaEventDestroy(c->lane_done[l]);
+    }
+    for (int r = 0; r < kRing; ++r) {
+      if (c->sign_evs[r]) cudaEventDestroy(c->sign_evs[r]);
+      if (c->sign_ev0[r]) cudaEventDestroy(c->sign_ev0[r]);
+      if (c->sign_ev1[r]) cudaEventDestroy(c->sign_ev1[r]);
+    }
+    if (c->sign_dep) cudaEventDestroy(c->sign_dep);
+    if (c->sign_pubd) cudaEventDestroy(c->sign_pubd);
+    if (c->sign_pub) cudaStreamDestroy(c->sign_pub);
   }
-  cudaEventDestroy(c->ev_fork);
-  cudaStreamDestroy(c->stream);
-  cudaStreamDestroy(c->copy_in);
-  cudaStreamDestroy(c->copy_out);
+  auto ev = [](cudaEvent_t e) {
+    if (e) cudaEventDestroy(e);
+  };
+  auto st = [](cudaStream_t s) {
+    if (s) cudaStreamDestroy(s);
+  };
+  ev(c->ev0);
+  ev(c->ev1);
+  for (int b = 0; b < 2; ++b) {
+    ev(c->ev_in[b]);
+    ev(c->ev_comp[b]);
+    ev(c->ev_out[b]);
+    ev(c->ev_join[b]);
+    st(c->lane_s[b]);
+  }
+  ev(c->ev_fork);
+  st(c->stream);
+  st(c->copy_in);
+  st(c->copy_out);
   delete c;
 }
 
@@ -317,35 +372,90 @@ int dlb_verify_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_pks, 
   return tm.finish();
 }
 
+namespace {
+
+// ticket handed to callers: internal ticket + 1; 0 = an empty batch (nothing to wait for)
+int sign_submit_dev(dlb_ctx* c, int level, size_t n_keys, const uint8_t* d_sks, size_t sk_stride, size_t n,
+                    const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
+                    const uint8_t* d_rho_prime, size_t psi, int speculate, uint8_t* d_sigs,
+                    uint32_t* d_attempts, uint8_t* d_failed, uint64_t* ticket_out) {
+  LevelSizes ls;
+  if (!c || !ticket_out) return DLB_E_ARG;
+  if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
+  *ticket_out = 0;
+  if (n == 0) return 0;
+  if (!d_sks || !d_msg_off || !d_sigs) return DLB_E_ARG;
+  if (sk_stride != 0 && sk_stride != ls.sk) return DLB_E_ARG;
+  cudaSetDevice(c->device);
+  unsigned t;
+  cudaStream_t st;
+  DLB_TRY(sign_reserve(c, &t, &st));
+  SignIo io;
+  io.n = n;
+  io.d_sks = d_sks;
+  io.sk_stride = sk_stride;
+  io.n_keys = n_keys;
+  io.d_key_idx = d_key_idx;
+  io.d_msgs = d_msgs;
+  io.d_msg_off = d_msg_off;
+  io.d_rho_prime = d_rho_prime;
+  io.psi = psi;
+  io.speculate = speculate;
+  io.d_sigs = d_sigs;
+  io.d_attempts = d_attempts;
+  io.d_failed = d_failed;
+  c->launches = 0;
+  DLB_TRY(with_level(level, [&](auto p) { return sign_submit<decltype(p)>(c, t, io); }));
+  c->tickets[t % kRing].zero_dev = d_sigs;
+  *ticket_out = (uint64_t)t + 1;
+  return 0;
+}
+
+int sign_wait_ticket(dlb_ctx* c, uint64_t ticket, dlb_sign_stats* stats, bool drain) {
+  if (!c) return DLB_E_ARG;
+  if (stats) memset(stats, 0, sizeof *stats);
+  if (ticket == 0) return 0;
+  cudaSetDevice(c->device);
+  return sign_wait(c, (unsigned)(ticket - 1), stats, drain);
+}
+
+}  // namespace
+
+int dlb_sign_submit_dev(dlb_ctx* c, int level, size_t n_keys, const uint8_t* d_sks, size_t sk_stride,
+                        size_t n, const uint32_t* d_key_idx, const uint8_t* d_msgs,
+                        const uint64_t* d_msg_off, const uint8_t* d_rho_prime, size_t psi, int speculate,
+                        uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed, uint64_t* ticket) {
+  if (n && d_key_idx && !n_keys) return DLB_E_ARG;
+  return sign_submit_dev(c, level, n_keys, d_sks, sk_stride, n, d_key_idx, d_msgs, d_msg_off, d_rho_prime,
+                         psi, speculate, d_sigs, d_attempts, d_failed, ticket);
+}
+
+int dlb_sign_wait(dlb_ctx* c, uint64_t ticket, dlb_sign_stats* stats) {
+  return sign_wait_ticket(c, ticket, stats, false);
+}
+
 int dlb_sign_batch_keyed_dev(dlb_ctx* c, int level, size_t n_keys, const uint8_t* d_sks, size_t n,
                              const uint32_t* d_key_idx, const uint8_t* d_msgs,
                              const uint64_t* d_msg_off, const uint8_t* d_rho_prime, size_t psi,
                              int speculate, uint8_t* d_sigs, uint32_t* d_attempts, uint8_t* d_failed,
                              dlb_sign_stats* stats) {
   LevelSizes ls;
-  if (!c || (n && (!d_sks || !d_msg_off || !d_sigs || !d_key_idx || !n_keys))) return DLB_E_ARG;
+  if (!c || (n && (!d_key_idx || !n_keys))) return DLB_E_ARG;
   if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
-  cudaSetDevice(c->device);
-  Timed tm(c);
-  DLB_TRY(with_level(level, [&](auto p) {
-    return sign_dev<decltype(p)>(c, n, d_sks, ls.sk, n_keys, d_key_idx, d_msgs, d_msg_off, d_rho_prime,
-                                 psi, speculate, d_sigs, d_attempts, d_failed, stats);
-  }));
-  return tm.finish();
+  uint64_t t = 0;
+  DLB_TRY(sign_submit_dev(c, level, n_keys, d_sks, ls.sk, n, d_key_idx, d_msgs, d_msg_off, d_rho_prime, psi,
+                          speculate, d_sigs, d_attempts, d_failed, &t));
+  return sign_wait_ticket(c, t, stats, true);
 }
 
 int dlb_sign_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_sks, size_t sk_stride,
                        const uint8_t* d_msgs, const uint64_t* d_msg_off,
                        const uint8_t* d_rho_prime, size_t psi, int speculate, uint8_t* d_sigs,
                        uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats) {
-  if (!c || (n && (!d_sks || !d_msg_off || !d_sigs))) return DLB_E_ARG;
-  cudaSetDevice(c->device);
-  Timed tm(c);
-  DLB_TRY(with_level(level, [&](auto p) {
-    return sign_dev<decltype(p)>(c, n, d_sks, sk_stride, 0, nullptr, d_msgs, d_msg_off, d_rho_prime,
-                                 psi, speculate, d_sigs, d_attempts, d_failed, stats);
-  }));
-  return tm.finish();
+  uint64_t t = 0;
+  DLB_TRY(sign_submit_dev(c, level, 0, d_sks, sk_stride, n, nullptr, d_msgs, d_msg_off, d_rho_prime, psi,
+                          speculate, d_sigs, d_attempts, d_failed, &t));
+  return sign_wait_ticket(c, t, stats, true);
 }
 
 // ---- host-buffer API -----------------------------------------------------------------
@@ -363,15 +473,14 @@ int dlb_sign_batch_dev(dlb_ctx* c, int level, size_t n, const uint8_t* d_sks, si
 
 namespace {
 
-constexpr size_t kPipeChunkMax = 8192;  // measured: finer chunks hide more of the PCIe time (+3 % at 100k)
+// (pipeline chunk cap: dlb_ctx::knob_pipe_chunk, 8192 tasks -- measured: finer chunks hide more of the PCIe time, +3 % at 100k)
 
 // transfer/compute pipeline granularity: at least four chunks per batch so small batches
 // (the batch-10k latency case) overlap their copies too
-inline size_t pipe_chunk(size_t n) {
+inline size_t pipe_chunk(const dlb_ctx* ctx, size_t n) {
   size_t c = (n + 3) / 4;
   if (c < 2048) c = 2048;
-  size_t cmax = kPipeChunkMax;
-  if (const char* e = getenv("DLB_PIPE_CHUNK")) cmax = (size_t)atol(e);  // experiments
+  const size_t cmax = ctx->knob_pipe_chunk;  // DLB_PIPE_CHUNK at dlb_create
   if (c > cmax) c = cmax;
   return c < n ? c : n;
 }
@@ -412,7 +521,7 @@ int dlb_keygen_batch(dlb_ctx* c, int level, size_t n, const uint8_t* zetas, uint
   cudaSetDevice(c->device);
   OwnStream own(c);
   cudaStream_t S = c->stream, CO = c->copy_out;
-  const size_t chunk = pipe_chunk(n);
+  const size_t chunk = pipe_chunk(c, n);
   uint8_t *dz, *dpk[2], *dsk[2];
   DLB_TRY(dalloc(c, "io.zeta", n * 32, &dz));
   DLB_TRY(dalloc(c, "io.pk0", chunk * ls.pk, &dpk[0]));
@@ -466,7 +575,7 @@ int verify_host(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_s
   OwnStream own(c);
   cudaStream_t S = c->stream, CI = c->copy_in;
   const size_t mbytes = msg_off[n];
-  const size_t chunk = pipe_chunk(n);
+  const size_t chunk = pipe_chunk(c, n);
   const bool keyed = key_idx != nullptr;
   const size_t pk_cap = keyed ? n_keys : (pk_stride ? chunk : 1);
   uint8_t *dpk[2], *dm, *dsig[2], *dfl;
@@ -532,70 +641,131 @@ int dlb_verify_batch_keyed(dlb_ctx* c, int level, size_t n_keys, const uint8_t* 
 
 namespace {
 
-int sign_host(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride, size_t n_keys,
-              const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
-              const uint8_t* rho_prime, size_t psi, int speculate, uint8_t* sigs, uint32_t* attempts,
-              uint8_t* failed, dlb_sign_stats* stats) {
+// offsets must be non-decreasing (task i signs msgs[off[i] .. off[i+1])) and msgs non-null when any byte is used
+bool msg_off_ok(const uint8_t* msgs, const uint64_t* msg_off, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (msg_off[i + 1] < msg_off[i]) return false;
+  return msg_off[n] == msg_off[0] || msgs != nullptr;
+}
+
+int sign_host_submit(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride, size_t n_keys,
+                     const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+                     const uint8_t* rho_prime, size_t psi, int speculate, uint8_t* sigs,
+                     uint32_t* attempts, uint8_t* failed, uint64_t* ticket_out) {
   LevelSizes ls;
-  if (!c) return DLB_E_ARG;
+  if (!c || !ticket_out) return DLB_E_ARG;
   if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
-  if (stats) memset(stats, 0, sizeof *stats);
+  *ticket_out = 0;
   if (n == 0) return 0;
   if (!sks || !msg_off || !sigs) return DLB_E_ARG;
   if (sk_stride != 0 && sk_stride != ls.sk) return DLB_E_ARG;
   if (key_idx && (n_keys == 0 || sk_stride == 0 || !key_idx_ok(key_idx, n, n_keys))) return DLB_E_ARG;
+  if (msg_off[0] != 0 || !msg_off_ok(msgs, msg_off, n)) return DLB_E_ARG;
   cudaSetDevice(c->device);
   OwnStream own(c);
-  cudaStream_t S = c->stream;
+  PhaseProf prof;
+  unsigned t;
+  cudaStream_t S;
+  DLB_TRY(sign_reserve(c, &t, &S));
+  prof.mark("reserve");
+  const int slot = (int)(t % kRing);
   const size_t mbytes = msg_off[n];
   const size_t nk = key_idx ? n_keys : (sk_stride ? n : 1);
   uint8_t *dsk, *dm, *dsig, *dfail, *drp = nullptr;
   uint64_t* doff;
   uint32_t *datt, *dkidx = nullptr;
-  if (key_idx) DLB_TRY(dalloc(c, "io.kidx", n, &dkidx));
+  if (key_idx) DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.kidx"), n, &dkidx));
   uint8_t* zero_copy = static_cast<uint8_t*>(pinned_alias(sigs));  // pinned: write in place
-  DLB_TRY(dalloc(c, "io.sk", nk * ls.sk, &dsk));
-  DLB_TRY(dalloc(c, "io.msg", mbytes + 8, &dm));
-  DLB_TRY(dalloc(c, "io.off", n + 1, &doff));
-  if (!zero_copy) DLB_TRY(dalloc(c, "io.sig", n * ls.sig + 8, &dsig));
+  DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.sk"), nk * ls.sk, &dsk));
+  DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.msg"), mbytes + 8, &dm));
+  DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.off"), n + 1, &doff));
+  if (!zero_copy) DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.sig"), n * ls.sig + 8, &dsig));
   else dsig = zero_copy;
-  DLB_TRY(dalloc(c, "io.att", n, &datt));
-  DLB_TRY(dalloc(c, "io.fail", n, &dfail));
-  DLB_CU(cudaMemcpyAsync(dsk, sks, nk * ls.sk, cudaMemcpyHostToDevice, S));
-  if (mbytes) DLB_CU(cudaMemcpyAsync(dm, msgs, mbytes, cudaMemcpyHostToDevice, S));
-  DLB_CU(cudaMemcpyAsync(doff, msg_off, (n + 1) * 8, cudaMemcpyHostToDevice, S));
-  if (key_idx) DLB_CU(cudaMemcpyAsync(dkidx, key_idx, n * 4, cudaMemcpyHostToDevice, S));
+  DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.att"), n, &datt));
+  DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.fail"), n, &dfail));
+  // Inputs go up with truly asynchronous copies: pageable memory is first copied into this ring
+  // slot's pinned staging (a pageable cudaMemcpyAsync would wait for the lane's previous kernel
+  // and stall the submitting thread); pinned caller buffers are used where they lie.
+  auto upload = [&](const char* what, void* dst, const void* src, size_t bytes) -> int {
+    if (!bytes) return 0;
+    if (!pinned_alias(src)) {
+      void* stage = nullptr;
+      DLB_TRY(c->hbuf(c->slot_name(c->cur_set, what), bytes, &stage));
+      memcpy(stage, src, bytes);
+      src = stage;
+    }
+    DLB_CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S));
+    return 0;
+  };
+  prof.mark("arenas");
+  DLB_TRY(upload("h.sk", dsk, sks, nk * ls.sk));
+  DLB_TRY(upload("h.msg", dm, msgs, mbytes));
+  DLB_TRY(upload("h.off", doff, msg_off, (n + 1) * 8));
+  if (key_idx) DLB_TRY(upload("h.kidx", dkidx, key_idx, n * 4));
   if (rho_prime) {
-    DLB_TRY(dalloc(c, "io.rp", n * 64, &drp));
-    DLB_CU(cudaMemcpyAsync(drp, rho_prime, n * 64, cudaMemcpyHostToDevice, S));
+    DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.rp"), n * 64, &drp));
+    DLB_TRY(upload("h.rp", drp, rho_prime, n * 64));
   }
+  prof.mark("uploads");
+  SignIo io;
+  io.n = n;
+  io.d_sks = dsk;
+  io.h_sks = sks;
+  io.sk_stride = sk_stride;
+  io.n_keys = n_keys;
+  io.d_key_idx = dkidx;
+  io.d_msgs = dm;
+  io.d_msg_off = doff;
+  io.d_rho_prime = drp;
+  io.psi = psi;
+  io.speculate = speculate;
+  io.d_sigs = dsig;
+  io.d_attempts = datt;
+  io.d_failed = dfail;
   c->launches = 0;
-  DLB_CU(cudaEventRecord(c->ev0, S));
-  const int rc = with_level(level, [&](auto p) {
-    return sign_dev<decltype(p)>(c, n, dsk, sk_stride, n_keys, dkidx, dm, doff, drp, psi, speculate,
-                                 dsig, datt, dfail, stats);
-  });
-  DLB_CU(cudaEventRecord(c->ev1, S));
+  const int rc = with_level(level, [&](auto p) { return sign_submit<decltype(p)>(c, t, io); });
+  prof.mark("sign_submit");
   if (rc != 0) {
-    cudaStreamSynchronize(S);
+    cudaStreamSynchronize(S);  // copies in flight read the caller's buffers
     return rc;
   }
-  if (!zero_copy) DLB_CU(cudaMemcpyAsync(sigs, dsig, n * ls.sig, cudaMemcpyDeviceToHost, S));
-  if (attempts) DLB_CU(cudaMemcpyAsync(attempts, datt, n * 4, cudaMemcpyDeviceToHost, S));
-  if (failed) DLB_CU(cudaMemcpyAsync(failed, dfail, n, cudaMemcpyDeviceToHost, S));
-  DLB_CU(cudaStreamSynchronize(S));
-  cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  SignTicket& tk = c->tickets[slot];
+  if (!zero_copy) {
+    tk.h_sigs = sigs;
+    tk.d_sigs = dsig;
+  }
+  if (attempts) {
+    tk.h_att = attempts;
+    tk.d_att = datt;
+  }
+  if (failed) {
+    tk.h_failed = failed;
+    tk.d_failed = dfail;
+  }
+  tk.zero_host = sigs;
+  *ticket_out = (uint64_t)t + 1;
   return 0;
 }
 
 }  // namespace
 
+int dlb_sign_submit(dlb_ctx* c, int level, size_t n_keys, const uint8_t* sks, size_t sk_stride, size_t n,
+                    const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
+                    const uint8_t* rho_prime, size_t psi, int speculate, uint8_t* sigs,
+                    uint32_t* attempts, uint8_t* failed, uint64_t* ticket) {
+  return sign_host_submit(c, level, n, sks, sk_stride, n_keys, key_idx, msgs, msg_off, rho_prime, psi,
+                          speculate, sigs, attempts, failed, ticket);
+}
+
 int dlb_sign_batch(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride,
                    const uint8_t* msgs, const uint64_t* msg_off, const uint8_t* rho_prime,
                    size_t psi, int speculate, uint8_t* sigs, uint32_t* attempts, uint8_t* failed,
                    dlb_sign_stats* stats) {
-  return sign_host(c, level, n, sks, sk_stride, 0, nullptr, msgs, msg_off, rho_prime, psi, speculate,
-                   sigs, attempts, failed, stats);
+  if (stats) memset(stats, 0, sizeof *stats);
+  uint64_t t = 0;
+  DLB_TRY(sign_host_submit(c, level, n, sks, sk_stride, 0, nullptr, msgs, msg_off, rho_prime, psi, speculate,
+                           sigs, attempts, failed, &t));
+  return sign_wait_ticket(c, t, stats, true);
 }
 
 int dlb_sign_batch_keyed(dlb_ctx* c, int level, size_t n_keys, const uint8_t* sks, size_t n,
@@ -605,8 +775,38 @@ int dlb_sign_batch_keyed(dlb_ctx* c, int level, size_t n_keys, const uint8_t* sk
   LevelSizes ls;
   if (!level_sizes(level, &ls)) return DLB_E_LEVEL;
   if (n && !key_idx) return DLB_E_ARG;
-  return sign_host(c, level, n, sks, ls.sk, n_keys, key_idx, msgs, msg_off, rho_prime, psi, speculate,
-                   sigs, attempts, failed, stats);
+  if (stats) memset(stats, 0, sizeof *stats);
+  uint64_t t = 0;
+  DLB_TRY(sign_host_submit(c, level, n, sks, ls.sk, n_keys, key_idx, msgs, msg_off, rho_prime, psi, speculate,
+                           sigs, attempts, failed, &t));
+  return sign_wait_ticket(c, t, stats, true);
+}
+
+int dlb_set_assignment_log(dlb_ctx* c, size_t cap) {
+  if (!c || cap > (1u << 26)) return DLB_E_ARG;
+  c->alog_cap = cap;
+  c->alog_count = 0;
+  return 0;
+}
+
+long long dlb_get_assignment_log(dlb_ctx* c, dlb_assignment* out, size_t max_records) {
+  if (!c) return DLB_E_ARG;
+  const unsigned long long have = c->alog_count < c->alog_cap ? c->alog_count : c->alog_cap;
+  const size_t ncopy = have < max_records ? (size_t)have : max_records;
+  if (ncopy && out) {
+    auto it = c->dev.find("s.alog");
+    if (it == c->dev.end() || !it->second.p) return DLB_E_ARG;
+    cudaSetDevice(c->device);
+    const cudaError_t e = cudaMemcpy(out, it->second.p, ncopy * sizeof(dlb_assignment), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return -1000 - (int)e;
+  }
+  return (long long)c->alog_count;
+}
+
+int dlb_dbg_set_max_attempt(dlb_ctx* c, unsigned max_attempt) {
+  if (!c) return DLB_E_ARG;
+  c->dbg_max_attempt = max_attempt;
+  return 0;
 }
 
 // ---- stage-level entry points -----------------------------------------------------------

@@ -10,11 +10,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <map>
 #include <string>
+#include <vector>
 
 #include "../../include/dilithium_b200.h"
 #include "common.cuh"
+#include "sign_queue.cuh"
 
 namespace dlb {
 
@@ -28,6 +31,73 @@ struct HostBuf {
   size_t cap = 0;
 };
 
+// host-side record of a submitted signing batch (ring slot = ticket % kRing)
+struct SignTicket {
+  bool active = false;
+  unsigned ticket = 0;
+  int level = 0;
+  size_t n = 0, sig_bytes = 0;
+  bool had_trace = false, had_alog = false;
+  int set = 0;  // arena set held until the wait
+  // results still to be copied to the caller at wait time (null = already in place)
+  uint8_t* h_sigs = nullptr;
+  const uint8_t* d_sigs = nullptr;
+  uint32_t* h_att = nullptr;
+  const uint32_t* d_att = nullptr;
+  uint8_t* h_failed = nullptr;
+  const uint8_t* d_failed = nullptr;
+  // the caller's signature buffer, cleared when the key turns out malformed
+  uint8_t* zero_host = nullptr;
+  uint8_t* zero_dev = nullptr;
+};
+
+// Per-key signing state kept across calls (SignPrecomp, scheme.hpp:26-32,106-125): the expanded
+// matrix and the transformed secret vectors of a shared key, in device allocations that are never
+// rewritten while the entry lives.  A batch signed under a cached key needs no per-key kernels.
+struct KeyCacheEntry {
+  int level = 0;
+  uint64_t hash = 0;
+  std::vector<uint8_t> sk;   // the packed key the entry was built from (compared on a hit)
+  int32_t* A = nullptr;
+  int32_t* shat = nullptr;
+  cudaEvent_t ready = nullptr;  // precomputation finished (recorded on the lane that built it)
+  unsigned long long last_use = 0;
+};
+
+// what a signing submission passes down; device pointers unless noted
+struct SignIo {
+  size_t n = 0;
+  const uint8_t* d_sks = nullptr;
+  const uint8_t* h_sks = nullptr;         // nullable: host copy of the keys (shared key: cache lookup)
+  size_t sk_stride = 0, n_keys = 0;
+  const uint32_t* d_key_idx = nullptr;
+  const uint8_t* d_msgs = nullptr;
+  const uint64_t* d_msg_off = nullptr;
+  const uint64_t* d_mu_in = nullptr;      // stage tests: mu supplied (then d_rho_prime is rho' itself)
+  const uint8_t* d_rho_prime = nullptr;   // nullable: n * 64 override
+  const uint32_t* d_kappa0 = nullptr;     // stage tests: first nonce per task
+  size_t psi = 0;
+  int speculate = 1, single_round = 0;
+  uint8_t* d_sigs = nullptr;
+  uint32_t* d_attempts = nullptr;
+  uint8_t* d_failed = nullptr;
+  uint8_t* d_dbg_ct = nullptr;
+  uint8_t* d_dbg_stage = nullptr;
+  bool dbg_bounds = false;                // run the DBG kernel with the bounds below
+  int32_t bounds[3] = {0, 0, 0};
+};
+
+inline int level_index(int level) {
+  switch (level) {
+    case 2: return 0;
+    case 3: return 1;
+    case 5: return 2;
+    case 44: return 3;
+    case 65: return 4;
+    default: return 5;
+  }
+}
+
 }  // namespace dlb
 
 struct dlb_ctx {
@@ -38,11 +108,12 @@ struct dlb_ctx {
   cudaStream_t ext = nullptr;         // caller's stream for *_dev calls (optional)
   cudaStream_t lane_s[2] = {};        // two compute lanes: consecutive chunks overlap
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {};
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};  // chunk pipeline hand-offs
   float last_ms = 0.f, last_main_ms = 0.f;  // whole call / dominant kernel only
   unsigned launches = 0;
   int sm_count = 148;
+  size_t max_batch_hint = 0;     // dlb_create's sizing hint: arenas of the first call are sized for it
   size_t trace_cap = 0;          // per-round scheduler trace (dlb_set_trace); 0 = off
   unsigned long long trace_count = 0;  // records the last sign call produced
   // FIPS 204 message prefix 0 || |ctx| || ctx (2..257 bytes) for the ML-DSA levels: host copy
@@ -54,7 +125,53 @@ struct dlb_ctx {
   std::map<std::string, dlb::DevBuf> dev;
   std::map<std::string, dlb::HostBuf> pinned;
 
+  // ---- signing scheduler: batches in flight (sign.cu) --------------------------------
+  bool sign_ready = false;
+  dlb::SignBatch* d_ring = nullptr;      // kRing descriptors in device memory
+  dlb::SignBatch* h_ring = nullptr;      // pinned staging of the same
+  volatile unsigned* h_flags = nullptr;  // mapped pinned completion flags, one per ring slot
+  unsigned* d_flags = nullptr;           // their device alias
+  dlb::SignLog* d_log = nullptr;
+  cudaStream_t sign_lane[dlb::kLanes] = {};
+  cudaEvent_t lane_done[dlb::kLanes] = {};  // last scheduler kernel of the lane finished
+  bool lane_used[dlb::kLanes] = {};
+  cudaStream_t sign_pub = nullptr;       // publication stream: copies and per-key kernels, never a scheduler kernel
+  cudaEvent_t sign_pubd = nullptr;       // batch published (the lane's kernel launch waits for it)
+  // per ring slot: start of the batch's device work, start / end of its scheduler kernel
+  cudaEvent_t sign_evs[dlb::kRing] = {}, sign_ev0[dlb::kRing] = {}, sign_ev1[dlb::kRing] = {}, sign_dep = nullptr;
+  dlb::SignTicket tickets[dlb::kRing];
+  unsigned next_ticket = 0;
+  // input / output / per-batch arenas come in sets; a ticket holds the lowest free set from
+  // submission to wait, so a pipeline of depth d only ever touches (and warms) d sets
+  bool set_busy[dlb::kRing] = {};
+  int cur_set = 0;                       // set reserved for the submission in progress
+  int sign_occ[12] = {};                 // resident CTAs per SM of k_sign_persistent<level, DBG>
+  size_t sign_smem[12] = {};
+  int sign_carveout[12] = {};            // their L1 / shared split (percent of 228 KB)
+  size_t alog_cap = 0;                   // executed-attempt log (dlb_set_assignment_log); 0 = off
+  unsigned long long alog_count = 0;
+  std::vector<dlb::KeyCacheEntry> key_cache;
+  unsigned long long key_cache_clock = 0, key_cache_hits = 0, key_cache_misses = 0;
+  size_t knob_key_cache = 32;            // entries; 0 disables (DLB_KEY_CACHE)
+  unsigned dbg_max_attempt = 0;          // stage tests: smaller nonce space (0 = the scheme's)
+  // tuning knobs, read from the environment once at dlb_create (profiles/: the sweeps)
+  unsigned knob_spec_depth = 8;
+  size_t knob_chunk = 65536;      // keygen / verify device chunk (tasks)
+  size_t knob_pipe_chunk = 8192;  // host transfer pipeline chunk (tasks)
+  size_t knob_sign_pad_smem = 0;  // occupancy experiments
+  int knob_carveout = -1;
+  unsigned knob_sign_occ = 0;     // resident scheduler CTAs per SM (DLB_SIGN_OCC; 0 = what fits)
+
   cudaStream_t s() const { return ext ? ext : stream; }
+  const char* slot_name(int slot, const char* what) {
+    snprintf(name_buf, sizeof name_buf, "r%02d.%s", slot, what);
+    return name_buf;
+  }
+  const char* lane_name(int lane, const char* what) {
+    snprintf(name_buf, sizeof name_buf, "l%d.%s", lane, what);
+    return name_buf;
+  }
+  char name_buf[48] = {};
 
   // 256-byte aligned device arena slot (memory_pool.hpp:27 kArenaAlign), grown geometrically
   int dbuf(const char* name, size_t bytes, void** out) {
@@ -103,6 +220,24 @@ struct dlb_ctx {
 
 namespace dlb {
 
+// host-side phase timer for the submission path (DLB_SUBMIT_PROF=1 prints to stderr)
+struct PhaseProf {
+  bool on;
+  double t0;
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
+  PhaseProf() : on(getenv("DLB_SUBMIT_PROF") != nullptr), t0(on ? now() : 0) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const double t = now();
+    fprintf(stderr, "[submit] %-16s %.3f ms\n", what, t - t0);
+    t0 = t;
+  }
+};
+
 template <class T>
 inline int dalloc(dlb_ctx* c, const char* name, size_t count, T** out) {
   void* p = nullptr;
@@ -142,13 +277,7 @@ template <class K>
 inline void prefer_carveout(K kernel, int percent) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, percent);
 }
-inline int pipeline_carveout() {
-  static const int v = [] {
-    const char* e = getenv("DLB_CARVEOUT");  // experiments: -1 leaves the driver's per-kernel choice
-    return e ? atoi(e) : -1;
-  }();
-  return v;
-}
+inline int pipeline_carveout(const dlb_ctx* c) { return c->knob_carveout; }  // -1: the driver's per-kernel choice
 
 #define DLB_TRY(x)            \
   do {                        \
@@ -171,10 +300,11 @@ template <class P>
 int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, size_t n_keys,
                const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
                const uint8_t* d_sigs, uint8_t* d_flags);
+// signing: reserve a ticket (and learn its stream lane, for the caller's input copies), enqueue
+// the batch, later wait for it (sign.cu)
+int sign_reserve(dlb_ctx* c, unsigned* ticket, cudaStream_t* lane);
 template <class P>
-int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, size_t n_keys,
-             const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
-             const uint8_t* d_rho_prime, size_t psi, int speculate, uint8_t* d_sigs,
-             uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats);
+int sign_submit(dlb_ctx* c, unsigned ticket, const SignIo& io);
+int sign_wait(dlb_ctx* c, unsigned ticket, dlb_sign_stats* stats, bool drain);
 
 }  // namespace dlb

@@ -102,13 +102,14 @@ constexpr int kWords128 = 21, kWords256 = 17;
 // `p` (global, any alignment), zero beyond the end, with the SHAKE suffix 0x1F at
 // byte `len` -- i.e. the word to XOR into the state for a padded message.  The final
 // 0x80 is XORed by the caller into the last word of the block that holds byte `len`.
+template <bool NC = true>
 __device__ __forceinline__ uint64_t padded_word(const uint8_t* p, size_t len, size_t off) {
   uint64_t w = 0;
   if (off + 8 <= len) {
-    w = (uint64_t)load_u32_unaligned(p + off) | ((uint64_t)load_u32_unaligned(p + off + 4) << 32);
+    w = (uint64_t)load_u32_unaligned<NC>(p + off) | ((uint64_t)load_u32_unaligned<NC>(p + off + 4) << 32);
   } else if (off <= len) {
     const int n = (int)(len - off);  // 0..7 valid bytes
-    for (int i = 0; i < n; ++i) w |= (uint64_t)__ldg(p + off + i) << (8 * i);
+    for (int i = 0; i < n; ++i) w |= (uint64_t)(NC ? __ldg(p + off + i) : ld_weak(p + off + i)) << (8 * i);
     w |= (uint64_t)0x1F << (8 * n);
   }
   return w;
@@ -118,7 +119,7 @@ __device__ __forceinline__ uint64_t padded_word(const uint8_t* p, size_t len, si
 // (`pre`), then `plen` bytes from `pfx` (global memory; FIPS 204's 0 || |ctx| || ctx in front
 // of the message, plen = 0 for round 3), then msg[0..msg_len) from global memory.
 // Leaves the sponge finalized and permuted once: s holds the first squeeze block.
-template <int RATE_WORDS, int PRE_WORDS>
+template <int RATE_WORDS, int PRE_WORDS, bool NC = true>
 __device__ __forceinline__ void shake_absorb_pre(uint64_t (&s)[25], const uint64_t (&pre)[PRE_WORDS],
                                                  const uint8_t* pfx, unsigned plen,
                                                  const uint8_t* msg, size_t msg_len) {
@@ -128,14 +129,14 @@ __device__ __forceinline__ void shake_absorb_pre(uint64_t (&s)[25], const uint64
   const size_t total = (size_t)PRE_WORDS * 8 + plen + msg_len;
   const size_t nblocks = total / (RATE_WORDS * 8) + 1;  // padding always adds a byte
   auto tail_word = [&](size_t off) -> uint64_t {  // 8 bytes of the padded tail at `off`
-    if (plen == 0) return padded_word(msg, msg_len, off);
-    if (off >= plen) return padded_word(msg, msg_len, off - plen);
+    if (plen == 0) return padded_word<NC>(msg, msg_len, off);
+    if (off >= plen) return padded_word<NC>(msg, msg_len, off - plen);
     const unsigned nb = plen - (unsigned)off;  // prefix bytes from this word on
     if (nb >= 8)
-      return (uint64_t)load_u32_unaligned(pfx + off) | ((uint64_t)load_u32_unaligned(pfx + off + 4) << 32);
+      return (uint64_t)load_u32_unaligned<NC>(pfx + off) | ((uint64_t)load_u32_unaligned<NC>(pfx + off + 4) << 32);
     uint64_t w = 0;
-    for (unsigned i = 0; i < nb; ++i) w |= (uint64_t)__ldg(pfx + off + i) << (8 * i);
-    return w | (padded_word(msg, msg_len, 0) << (8 * nb));  // the bytes shifted out lead the next word
+    for (unsigned i = 0; i < nb; ++i) w |= (uint64_t)(NC ? __ldg(pfx + off + i) : ld_weak(pfx + off + i)) << (8 * i);
+    return w | (padded_word<NC>(msg, msg_len, 0) << (8 * nb));  // the bytes shifted out lead the next word
   };
 #pragma unroll 1
   for (size_t blk = 0; blk < nblocks; ++blk) {

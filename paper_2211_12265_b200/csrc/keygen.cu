@@ -11,7 +11,7 @@
 
 namespace dlb {
 
-constexpr size_t kKeygenChunk = 65536;  // measured: 16k -> 64k tasks per chunk = +7 % (one-sponge-per-task kernels fill more SMs)
+// device chunk: dlb_ctx::knob_chunk = 65536 tasks -- measured: 16k -> 64k tasks per chunk = +7 % (one-sponge-per-task kernels fill more SMs)
 
 // Chunks alternate between two compute lanes so the one-thread-per-task hashes of one
 // chunk overlap the wide sampler / arithmetic kernels of the next (see verify.cu).
@@ -24,8 +24,7 @@ int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uin
   cudaStream_t main = c->s();
   size_t chunk = (n + 1) / 2;
   if (chunk < 2048) chunk = 2048;
-  size_t cmax = kKeygenChunk;
-  if (const char* e = getenv("DLB_CHUNK")) cmax = (size_t)atol(e);  // experiments
+  const size_t cmax = c->knob_chunk;  // DLB_CHUNK at dlb_create for experiments
   if (chunk > cmax) chunk = cmax;
   if (chunk > n) chunk = n;
   uint64_t* seeds[2];
@@ -37,7 +36,7 @@ int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uin
     DLB_TRY(dalloc(c, nm[b][1], chunk * PV * kN, &s8[b]));
     DLB_TRY(dalloc(c, nm[b][2], chunk * KL * kN, &A[b]));
   }
-  if (const int co = pipeline_carveout(); co >= 0) {
+  if (const int co = pipeline_carveout(c); co >= 0) {
     prefer_carveout(k_keygen_seed, co);
     prefer_carveout(k_expand_s<P, HW>, co);
     prefer_carveout(k_expand_a<P, HW>, co);

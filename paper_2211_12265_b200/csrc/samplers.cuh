@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(WARPS * 32)
 // consumers decode gamma1 - raw with the same bit reader as the signature's z field,
 // which is exactly how the reference defines the mask (sampling.hpp:86-90).
 // Works on one sponge already positioned by the caller; used by the sign kernel.
-template <class P>
+// NC = false: rho' is read with coherent loads -- the signing scheduler serves batches that
+// were published after its kernel started, which the read-only (ld.global.nc) path must not touch.
+template <class P, bool NC = true>
 __device__ __forceinline__ void expand_mask_stream(const uint64_t* __restrict__ rho_prime,
                                                    unsigned nonce, uint8_t* __restrict__ dst) {
   constexpr int BYTES = 32 * P::Z_BITS;              // 576 / 640
@@ -163,7 +165,7 @@ __device__ __forceinline__ void expand_mask_stream(const uint64_t* __restrict__ 
   uint64_t s[25];
   keccak_clear(s);
 #pragma unroll
-  for (int w = 0; w < 8; ++w) s[w] = __ldg(rho_prime + w);
+  for (int w = 0; w < 8; ++w) s[w] = NC ? __ldg(rho_prime + w) : ld_weak(rho_prime + w);
   s[8] = (uint64_t)(nonce & 0xFFFF) | ((uint64_t)0x1F << 16);
   s[16] = 0x8000000000000000ull;
   uint64_t* out = reinterpret_cast<uint64_t*>(dst);
@@ -307,11 +309,46 @@ static __global__ void k_hash_tr(const uint8_t* __restrict__ pk, size_t pk_strid
 }
 
 // mu = SHAKE256(tr || M, 64) and optionally rho' = SHAKE256(K || mu, 64)
-// (scheme.hpp:240-248).  tr and K (32 B) per key, 8-byte aligned; task t uses key
-// key_idx[t] (key_idx == nullptr: key t), strides 0 = one shared key.
+// (scheme.hpp:240-248) of one task.  tr and K (32 B) of the task's key, 8-byte aligned.
 // MLDSA (FIPS 204 Alg. 2 / 7, deterministic variant): tr is 64 bytes,
 // mu = H(tr || 0 || |ctx| || ctx || M, 64) with the 2 + |ctx| prefix bytes at `pfx`
 // (plen of them), and rho'' = H(K || 0^32 || mu, 64).  Round 3: pfx unused, plen = 0.
+// NC = false reads every input with coherent loads (the signing scheduler hashes tasks of
+// batches that were published after its kernel started).
+template <bool MLDSA, bool NC>
+__device__ __forceinline__ void hash_mu_task(const uint64_t* tr, const uint64_t* key,
+                                             const uint8_t* pfx, unsigned plen, const uint8_t* msg,
+                                             size_t msg_len, uint64_t* mu_out,
+                                             uint64_t* rho_prime_out) {
+  constexpr int TRW = MLDSA ? 8 : 4;
+  uint64_t s[25];
+  uint64_t pre[TRW];
+#pragma unroll
+  for (int w = 0; w < TRW; ++w) pre[w] = NC ? __ldg(tr + w) : ld_weak(tr + w);
+  shake_absorb_pre<kWords256, TRW, NC>(s, pre, pfx, MLDSA ? plen : 0u, msg, msg_len);
+  uint64_t mu[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    mu[w] = s[w];
+    mu_out[w] = s[w];
+  }
+  if (rho_prime_out != nullptr) {
+    keccak_clear(s);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) s[w] = NC ? __ldg(key + w) : ld_weak(key + w);
+    constexpr int MU0 = MLDSA ? 8 : 4;  // rnd = 0^32 sits between K and mu
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s[MU0 + w] = mu[w];
+    s[MU0 + 8] = 0x1F;
+    s[16] ^= 0x8000000000000000ull;
+    keccak_f1600(s);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) rho_prime_out[w] = s[w];
+  }
+}
+
+// One thread per task; task t uses key key_idx[t] (key_idx == nullptr: key t), strides 0 = one
+// shared key.
 template <bool MLDSA>
 static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_stride,
                           const uint8_t* __restrict__ key_base, size_t key_stride,
@@ -320,37 +357,14 @@ static __global__ void k_hash_mu(const uint8_t* __restrict__ tr_base, size_t tr_
                           const uint8_t* __restrict__ msgs, const uint64_t* __restrict__ msg_off,
                           unsigned n, uint64_t* __restrict__ mu_out,
                           uint64_t* __restrict__ rho_prime_out) {
-  constexpr int TRW = MLDSA ? 8 : 4;
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  uint64_t s[25];
-  uint64_t pre[TRW];
   const size_t kt = key_idx ? (size_t)__ldg(key_idx + t) : (size_t)t;
-  const uint64_t* tr = reinterpret_cast<const uint64_t*>(tr_base + kt * tr_stride);
-#pragma unroll
-  for (int w = 0; w < TRW; ++w) pre[w] = __ldg(tr + w);
   const uint64_t m0 = msg_off[t], m1 = msg_off[t + 1];
-  shake_absorb_pre<kWords256, TRW>(s, pre, pfx, MLDSA ? plen : 0u, msgs + m0, (size_t)(m1 - m0));
-  uint64_t mu[8];
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    mu[w] = s[w];
-    mu_out[(size_t)t * 8 + w] = s[w];
-  }
-  if (rho_prime_out != nullptr) {
-    const uint64_t* key = reinterpret_cast<const uint64_t*>(key_base + kt * key_stride);
-    keccak_clear(s);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) s[w] = __ldg(key + w);
-    constexpr int MU0 = MLDSA ? 8 : 4;  // rnd = 0^32 sits between K and mu
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s[MU0 + w] = mu[w];
-    s[MU0 + 8] = 0x1F;
-    s[16] ^= 0x8000000000000000ull;
-    keccak_f1600(s);
-#pragma unroll
-    for (int w = 0; w < 8; ++w) rho_prime_out[(size_t)t * 8 + w] = s[w];
-  }
+  hash_mu_task<MLDSA, true>(reinterpret_cast<const uint64_t*>(tr_base + kt * tr_stride),
+                            reinterpret_cast<const uint64_t*>(key_base + kt * key_stride), pfx, plen,
+                            msgs + m0, (size_t)(m1 - m0), mu_out + (size_t)t * 8,
+                            rho_prime_out ? rho_prime_out + (size_t)t * 8 : nullptr);
 }
 
 // c~ = SHAKE256(mu || w1_packed, 32)  (scheme.hpp:158-163,311-317) for one stream:
@@ -369,7 +383,7 @@ __device__ __forceinline__ void hash_ctilde_stream(const uint64_t* __restrict__ 
     for (int w = 0; w < kWords256; ++w) {
       const int idx = blk * kWords256 + w;  // message word index
       uint64_t v = 0;
-      if (idx < 8) v = __ldg(mu + idx);
+      if (idx < 8) v = NC ? __ldg(mu + idx) : ld_weak(mu + idx);
       else if (idx < TOTALW) v = NC ? __ldg(w1 + (idx - 8)) : w1[idx - 8];
       else if (idx == TOTALW) v = 0x1F;
       s[w] ^= v;

@@ -28,7 +28,7 @@
 #include "verify_keygen.cuh"
 
 #ifndef DLB_R0_MIN
-#define DLB_R0_MIN 0
+#define DLB_R0_MIN 1  // S4's r0 norm check as an unsigned minimum (+0.5 %, parity campaign green)
 #endif
 namespace dlb {
 
@@ -82,46 +82,62 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 
 // ---- device-side scheduler state -----------------------------------------------------
+//
+// Batches in flight.  A submitted batch is described by one SignBatch in a device ring
+// (slot = ticket % kRing).  The scheduler kernel launched for ticket T serves tickets
+// T .. T + window - 1: its CTAs refill their open-task tables from ANY published batch of
+// that window before they speculate (the reference's pass 1 before pass 2,
+// scheduler.hpp:58-92, extended across batches -- the paper's in-flight batches,
+// PAPER.md:710-721), so the tail of one batch overlaps the body of the next ones.  Kernels of
+// consecutive tickets run on kLanes stream lanes with one scratch set each; a CTA never
+// waits for anything, it exits when its table is empty and no batch of its window has
+// unclaimed tasks.  Completion is per batch (SignBatch::done reaching n raises a flag in
+// mapped host memory), not per kernel.
 
-struct SignQueue {
-  unsigned head;          // next unclaimed task of the batch (the device work queue)
-  unsigned key_bad;       // some secret key failed the eta range check
-  unsigned long long rounds, attempts, speculative, idle_slots, accepted_sum, failed;
-  unsigned long long t_first_start, t_last_start, t_first_exit, t_last_exit;  // %globaltimer, ns
-  unsigned long long trace_count;  // per-round trace records produced (may exceed the capacity)
+// what a CTA keeps of a batch it serves (window position i <-> ticket own + i)
+struct BatchView {
+  unsigned n, tcap, max_attempt, spec_depth, key_stride, pad;
+  const uint64_t* mu;
+  const uint64_t* rho_prime;
+  const uint32_t* kappa0;
+  const int32_t* A;
+  const int32_t* shat;
+  const uint32_t* key_idx;
+  uint8_t* sigs;
+  uint32_t* attempts_out;
+  uint8_t* failed_out;
+  uint8_t* dbg_ctilde;
+  uint8_t* dbg_stage;
+  int32_t bounds[3];
+  unsigned plen;
+  const uint8_t* sk_base;
+  const uint8_t* msgs;
+  const uint64_t* msg_off;
+  const uint8_t* pfx;
+  uint64_t* mu_w;
+  uint64_t* rp_w;
+  SignBatch* g;  // the descriptor in the ring (mutable counters)
 };
 
-struct SignArgs {
-  unsigned n;                 // tasks
-  unsigned tcap;              // max open tasks per CTA (<= slots)
-  unsigned slots;             // attempt slots a CTA uses (<= 128): small batches are spread
-                              // over more CTAs with fewer slots each to cut round latency
-  unsigned max_attempt;       // (65535 - (L-1)) / L   (scheduler.hpp:52)
-  int speculate;
-  unsigned spec_depth;        // deepest speculative attempt per task and round (pass-2 cap)
+struct SignArgs {             // one scheduler-kernel instance
+  SignBatch* ring;            // kRing descriptors
+  unsigned ticket;            // own ticket
+  unsigned window;            // tickets served: ticket .. ticket + window - 1
+  unsigned slots;             // attempt slots a CTA fills with speculation (<= 128): small batches are
+                              // spread over more CTAs with fewer slots each to cut round latency
   int single_round;           // stage-test mode: exactly one round, then fail open tasks
-  const uint64_t* mu;         // n * 8
-  const uint64_t* rho_prime;  // n * 8
-  const uint32_t* kappa0;     // nullable: first nonce per task (stage tests)
-  const int32_t* A;           // keys * K*L*256
-  const int32_t* shat;        // keys * (L+2K)*256
-  unsigned key_stride;        // 0 shared key, 1 per-task keys (when key_idx == nullptr)
-  const uint32_t* key_idx;    // nullable: key table index of each task
   uint32_t* trace;            // nullable: per-round records of 8 words (dlb_round_trace)
   unsigned trace_cap;
-  // per-CTA scratch in HBM/L2, indexed [cta][slot]
+  uint32_t* alog;             // nullable: per executed attempt 4 words (dlb_assignment)
+  unsigned alog_cap;
+  SignLog* log;
+  // per-CTA scratch in HBM/L2, indexed [cta][slot] (one set per stream lane)
   uint8_t* ybytes;
   int32_t* wbuf;
   uint8_t* w1buf;
   uint64_t* ctbuf;
   int8_t* c8buf;
   uint8_t* staging;
-  // outputs
-  uint8_t* sigs;
-  uint32_t* attempts_out;     // nullable
-  uint8_t* failed_out;        // nullable
-  uint8_t* dbg_ctilde;        // nullable: n*32, c~ of each task's first executed attempt
-  SignQueue* q;
 };
 
 template <class P>
@@ -153,17 +169,23 @@ struct SignSmem {
     } a;
     int8_t rows[kSignThreads][kByteRowStride];
   } u;
-  uint32_t utask[kSignThreads];    // open tasks of this CTA (compact)
+  uint32_t utask[kSignThreads];    // open tasks of this CTA (compact): task id within its batch
   uint32_t unext[kSignThreads];    // their next unresolved attempt ordinal
-  uint32_t slot_task[kSignThreads];     // global task id or kNoSlot
+  uint8_t ubatch[kSignThreads];    // their batch: window position (ticket - own ticket)
+  uint32_t slot_task[kSignThreads];     // task id or kNoSlot
   uint32_t slot_attempt[kSignThreads];
+  uint8_t slot_batch[kSignThreads];
   uint8_t slot_valid[kSignThreads];
   int32_t winner[kSignThreads];    // per open task: winning slot, -1 none, -2 failed
   uint32_t warp_sums[kSignWarps];
-  unsigned U, newU, got, base;
+  BatchView bv[kWindow];           // descriptors of the batches this CTA has seen published
+  unsigned bcnt[kWindow];          // open tasks held per batch
+  unsigned bfin[kWindow];          // tasks of each batch finished in the current round
+  unsigned seen;                   // bit i: bv[i] loaded
+  unsigned U, Uold, span, need_hash;
   unsigned cursor2, cursor4;  // next unclaimed slot of stages S2 / S4 (warps pull slots)
   unsigned r_on, r_spec;      // this round's assigned / speculative slots (trace)
-  unsigned long long st_rounds, st_attempts, st_spec, st_idle;  // per-CTA counters
+  unsigned rounds;            // rounds this CTA has run
 };
 
 // ---- asynchronous scratch prefetch ----------------------------------------------------
@@ -256,7 +278,7 @@ __device__ __forceinline__ void stage_w(SignWarpScratch<P>& ws, SlotPipe& pp, co
     const int4* ap = reinterpret_cast<const int4*>(A + (size_t)(i * P::L) * kN) + 2 * lane;
 #pragma unroll 1
     for (int j = 0; j < P::L; ++j) {
-      const int4 a0 = __ldg(ap + j * (kN / 4)), a1 = __ldg(ap + j * (kN / 4) + 1);
+      const int4 a0 = ld_weak(ap + j * (kN / 4)), a1 = ld_weak(ap + j * (kN / 4) + 1);
       const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
       for (int m = 0; m < 8; ++m) acc64[m] = mac_wide(acc64[m], a[m], ws.vhat[j][m][lane]);
@@ -282,7 +304,7 @@ __device__ __forceinline__ void mul_challenge(int32_t (&out)[8], const int32_t (
                                               const int32_t* shat_poly, int32_t* tile,
                                               const int2* nzs, int lane) {
   const int4* sp = reinterpret_cast<const int4*>(shat_poly) + 2 * lane;
-  const int4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
+  const int4 s0 = ld_weak(sp), s1 = ld_weak(sp + 1);
   const int32_t s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
   for (int m = 0; m < 8; ++m) out[m] = mont_mul(ch[m], s[m]);
@@ -306,12 +328,22 @@ __device__ __forceinline__ void fetch_head(SlotPipe& pp, int par, const int8_t* 
 //
 // Precondition: head[par] (c) of this slot issued (possibly still in flight).  next_c8 is
 // the challenge of the warp's next active slot (nullptr if none); it goes to head[par ^ 1].
-template <class P>
-__device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp, int par,
-                                             const int2* zs, const int2* nzs, int lane,
-                                             const uint8_t* ybytes, int32_t* wrows,
-                                             const int8_t* next_c8, const uint64_t* ct,
-                                             const int32_t* shat, uint8_t* stage_sig) {
+//
+// Returns 0 when the attempt is accepted.  DBG = false: any other value means rejected (the
+// first failing check ends the attempt).  DBG = true (stage tests, scheme.hpp:133-138 with
+// injectable bounds): nothing is skipped and the value is 1 + the RejectStage the reference
+// would report -- the first failing check in ITS order (z, r0, c t0, hint weight).
+template <class P, bool DBG>
+__device__ __forceinline__ int stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp, int par,
+                                            const int2* zs, const int2* nzs, int lane,
+                                            const uint8_t* ybytes, int32_t* wrows,
+                                            const int8_t* next_c8, const uint64_t* ct,
+                                            const int32_t* shat, uint8_t* stage_sig,
+                                            const int32_t* bounds) {
+  const int32_t z_bound = DBG ? bounds[0] : P::GAMMA1 - P::BETA;
+  const int32_t r0_bound = DBG ? bounds[1] : P::GAMMA2 - P::BETA;
+  const int32_t vt_bound = DBG ? bounds[2] : P::GAMMA2;
+  unsigned fails = 0;  // DBG: bit 0 z, bit 1 r0, bit 2 c t0
   using S = Sizes<P>;
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int R = P::K + P::L;  // ring chunks of a slot: w_0..w_{K-1}, y_0..y_{L-1}
@@ -371,29 +403,26 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
     if (p < P::K) {
       const int32_t* wrow = reinterpret_cast<const int32_t*>(cur);
       int32_t* wdst = wrows + (size_t)p * kN;
-#if DLB_R0_MIN
+      constexpr bool R0MIN = DLB_R0_MIN && !DBG;
       uint32_t worst = 0;
-#endif
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int32_t d = freeze_near(wrow[lane + 32 * e] - t[e]);  // [0, q) - (-q, q)
-#if DLB_R0_MIN
-        // |r0| < B without materialising the centred r0: a0 = d - r1 * 2 gamma2 is r0 or, when
-        // HighBits wrapped to 0, r0 + q; shifted by B - 1 the valid one lands in [0, 2B - 1)
-        constexpr int32_t B = P::GAMMA2 - P::BETA;
-        const int32_t a0 = d - highbits<P::GAMMA2>(d) * 2 * P::GAMMA2;
-        const uint32_t u = (uint32_t)(a0 + B - 1);
-        worst = max(worst, min(u, u - (uint32_t)kQ));
-#else
-        int32_t r0;
-        decompose<P::GAMMA2>(d, r0);
-        bad = bad || abs(r0) >= P::GAMMA2 - P::BETA;
-#endif
+        if constexpr (R0MIN) {
+          // |r0| < B without materialising the centred r0: a0 = d - r1 * 2 gamma2 is r0 or, when
+          // HighBits wrapped to 0, r0 + q; shifted by B - 1 the valid one lands in [0, 2B - 1)
+          constexpr int32_t B = P::GAMMA2 - P::BETA;
+          const int32_t a0 = d - highbits<P::GAMMA2>(d) * 2 * P::GAMMA2;
+          const uint32_t u = (uint32_t)(a0 + B - 1);
+          worst = max(worst, min(u, u - (uint32_t)kQ));
+        } else {
+          int32_t r0;
+          decompose<P::GAMMA2>(d, r0);
+          bad = bad || abs(r0) >= r0_bound;
+        }
         wdst[lane + 32 * e] = d;  // read back by this same lane in the hint phase
       }
-#if DLB_R0_MIN
-      bad = worst >= 2u * (P::GAMMA2 - P::BETA) - 1u;
-#endif
+      if constexpr (R0MIN) bad = worst >= 2u * (P::GAMMA2 - P::BETA) - 1u;
     } else if (p < R) {
       uint32_t raw[8];
       unpack_strided<P::Z_BITS>(cur, lane, raw);
@@ -401,23 +430,27 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
       for (int e = 0; e < 8; ++e) {
         const int32_t y = P::GAMMA1 - (int32_t)raw[e];
         const int32_t z = y + reduce32(t[e]);  // |y| <= gamma1, |c s1| <= beta: no wrap, centred
-        bad = bad || abs(z) >= P::GAMMA1 - P::BETA;
+        bad = bad || abs(z) >= z_bound;
         ws.vhat[p - P::K][e][lane] = z;
       }
     } else {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int32_t vt = reduce32(t[e]);  // |c t0| <= tau * 2^12 < 2^22: already centred
-        bad = bad || abs(vt) >= P::GAMMA2;
+        bad = bad || abs(vt) >= vt_bound;
         const int h = highbits<P::GAMMA2>(freeze_near(wcs2[e] + vt)) != highbits<P::GAMMA2>(wcs2[e]);
         const unsigned mask = __ballot_sync(FULL, h);
         if (lane == 0) ws.hbits[p - R][e] = mask;
         weight += __popc(mask);
       }
     }
-    if (__any_sync(FULL, bad)) return false;
+    if (__any_sync(FULL, bad)) {
+      if (!DBG) return 1;
+      fails |= p < P::K ? 2u : (p < R ? 1u : 4u);
+    }
   }
-  if (weight > (unsigned)P::OMEGA) return false;
+  if (DBG && fails) return 1 + (int)(__ffs(fails) - 1);
+  if (weight > (unsigned)P::OMEGA) return DBG ? 4 : 1;
 
   // accepted: c~ | z | hints into the staging slot
   if (lane < 2 * Hashing<P>::CTW) reinterpret_cast<uint32_t*>(stage_sig)[lane] =
@@ -444,10 +477,10 @@ __device__ __forceinline__ bool stage_finish(SignWarpScratch<P>& ws, SlotPipe& p
     }
     if (lane == 0) hint[P::OMEGA + i] = (uint8_t)count;
   }
-  return true;
+  return 0;
 }
 
-template <class P>
+template <class P, bool DBG>
 __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44) ? DLB_SIGN_MINB : 4)
     k_sign_persistent(SignArgs a) {
   using S = Sizes<P>;
@@ -467,60 +500,166 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
   load_twiddles(sm.zs, sm.nzs);
   if (tid == 0) {
     sm.U = 0;
-    sm.st_rounds = sm.st_attempts = sm.st_spec = sm.st_idle = 0;
-    unsigned long long now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    atomicMin(&a.q->t_first_start, now);
-    atomicMax(&a.q->t_last_start, now);
+    sm.seen = 0;
+    sm.rounds = 0;
   }
+  if (tid < kWindow) sm.bcnt[tid] = sm.bfin[tid] = 0;
   __syncthreads();
 
   while (true) {
-    // ---- refill from the device work queue -----------------------------------------
-    if (tid == 0) {
-      const unsigned U = sm.U;
-      unsigned got = 0, base = 0;
-      if (U < a.tcap && !(a.single_round && sm.st_rounds > 0)) {
-        const unsigned want = a.tcap - U;
-        if (*(volatile unsigned*)&a.q->head < a.n) {
-          base = atomicAdd(&a.q->head, want);
-          if (base < a.n) got = min(want, a.n - base);
-        }
+    // ---- refill from the device work queues of the batches in this kernel's window ------
+    // Warp 0: lane i looks at ticket own + i.  A batch becomes visible through an acquire
+    // load of its gate word (the host writes it after the descriptor and all inputs are in
+    // place; the acquire also drops stale L1 lines of whatever occupied those arenas before).
+    // Tasks are claimed oldest batch first, up to tcap per batch and 128 per CTA.
+    if (warp == 0) {
+      unsigned U = sm.U;
+      if (lane == 0) {
+        sm.span = 0;
+        sm.Uold = U;
+        sm.need_hash = 0;
       }
-      sm.got = got;
-      sm.base = base;
+      if (U < (unsigned)kSignThreads && !(a.single_round && sm.rounds > 0)) {
+        bool avail = false;
+        if ((unsigned)lane < a.window) {
+          SignBatch* g = a.ring + ((a.ticket + lane) % kRing);
+          bool seen = (sm.seen >> lane) & 1u;
+          if (!seen && ld_acquire(&g->gate) == a.ticket + lane + 1u && g->level == P::LEVEL &&
+              (lane == 0 || !g->exclusive)) {
+            BatchView& v = sm.bv[lane];
+            v.n = g->n;
+            v.tcap = g->tcap;
+            v.max_attempt = g->max_attempt;
+            v.spec_depth = g->spec_depth;
+            v.key_stride = g->key_stride;
+            v.mu = g->mu;
+            v.rho_prime = g->rho_prime;
+            v.kappa0 = g->kappa0;
+            v.A = g->A;
+            v.shat = g->shat;
+            v.key_idx = g->key_idx;
+            v.sigs = g->sigs;
+            v.attempts_out = g->attempts_out;
+            v.failed_out = g->failed_out;
+            v.dbg_ctilde = g->dbg_ctilde;
+            v.dbg_stage = g->dbg_stage;
+            v.bounds[0] = g->bounds[0];
+            v.bounds[1] = g->bounds[1];
+            v.bounds[2] = g->bounds[2];
+            v.plen = g->plen;
+            v.sk_base = g->sk_base;
+            v.msgs = g->msgs;
+            v.msg_off = g->msg_off;
+            v.pfx = g->pfx;
+            v.mu_w = g->mu_w;
+            v.rp_w = g->rp_w;
+            v.g = g;
+            atomicOr(&sm.seen, 1u << lane);
+            seen = true;
+          }
+          if (seen) avail = ld_relaxed(&g->head) < sm.bv[lane].n && sm.bcnt[lane] < sm.bv[lane].tcap;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, avail);
+        while (m && U < (unsigned)kSignThreads) {
+          const int i = __ffs(m) - 1;
+          m &= m - 1;
+          const BatchView& v = sm.bv[i];
+          const unsigned want = min(v.tcap - sm.bcnt[i], (unsigned)kSignThreads - U);
+          unsigned base = 0, got = 0;
+          if (lane == 0) {
+            base = atomicAdd(&v.g->head, want);
+            if (base < v.n) got = min(want, v.n - base);
+            if (got) {
+              unsigned long long now;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+              atomicMin(&v.g->t_first_start, now);
+              atomicMax(&v.g->t_last_start, now);
+              sm.bcnt[i] += got;
+              if (v.msg_off) sm.need_hash = 1;
+            }
+          }
+          base = __shfl_sync(0xffffffffu, base, 0);
+          got = __shfl_sync(0xffffffffu, got, 0);
+          for (unsigned t = lane; t < got; t += 32) {
+            sm.utask[U + t] = base + t;
+            sm.unext[U + t] = 0;
+            sm.ubatch[U + t] = (uint8_t)i;
+          }
+          U += got;
+        }
+        if (lane == 0) sm.U = U;
+      }
     }
     __syncthreads();
-    {
-      const unsigned U = sm.U, got = sm.got;
-      if ((unsigned)tid < got) {
-        sm.utask[U + tid] = sm.base + tid;
-        sm.unext[U + tid] = 0;
-      }
-      __syncthreads();
-      if (tid == 0) sm.U = U + got;
-      __syncthreads();
-    }
     const unsigned U = sm.U;
     if (U == 0) break;
 
+    // ---- S0: mu = H(tr || M), rho' = H(K || mu) of the tasks just claimed (scheme.hpp:240-248)
+    if (sm.need_hash) {
+      if ((unsigned)tid >= sm.Uold && (unsigned)tid < U) {
+        const BatchView& v = sm.bv[sm.ubatch[tid]];
+        if (v.msg_off) {
+          const unsigned task = sm.utask[tid];
+          const size_t kt = v.key_idx ? (size_t)ld_weak(v.key_idx + task) : (size_t)task * v.key_stride;
+          const uint8_t* sk = v.sk_base + kt * S::SK;
+          const uint64_t m0 = ld_weak(v.msg_off + task), m1 = ld_weak(v.msg_off + task + 1);
+          hash_mu_task<Hashing<P>::MLDSA, false>(
+              reinterpret_cast<const uint64_t*>(sk + 64), reinterpret_cast<const uint64_t*>(sk + 32),
+              v.pfx, v.plen, v.msgs + m0, (size_t)(m1 - m0), v.mu_w + (size_t)task * 8,
+              v.rp_w ? v.rp_w + (size_t)task * 8 : nullptr);
+        }
+      }
+      __syncthreads();
+    }
+
     // ---- schedule: slot s -> open task s % U, depth s / U (scheduler.hpp:58-92) ------
+    // Depth 0 (pass 1) always runs.  Speculative depths (pass 2) only use the first a.slots
+    // slots and only exist when the queues could not fill the table, because the refill above
+    // comes first.
     {
       const unsigned u = tid % U, depth = tid / U;
+      const unsigned bi = sm.ubatch[u];
+      const BatchView& v = sm.bv[bi];
       const unsigned att = sm.unext[u] + depth;
-      const bool on = (unsigned)tid < a.slots && (depth == 0 || (a.speculate && depth <= a.spec_depth)) &&
-                      att <= a.max_attempt;
-      sm.slot_task[tid] = on ? sm.utask[u] : kNoSlot;
+      const bool on = (depth == 0 || ((unsigned)tid < a.slots && depth <= v.spec_depth)) &&
+                      att <= v.max_attempt;
+      const unsigned task = sm.utask[u];
+      sm.slot_task[tid] = on ? task : kNoSlot;
       sm.slot_attempt[tid] = att;
+      sm.slot_batch[tid] = (uint8_t)bi;
       sm.slot_valid[tid] = 0;
       if (tid == 0) sm.cursor2 = sm.cursor4 = 0;
+      // per-batch counters, one atomic per warp and batch
+      const unsigned grp = __match_any_sync(0xffffffffu, on ? bi : 0xFFu);
+      const unsigned specm = __ballot_sync(0xffffffffu, on && depth > 0);
+      if (on && lane == __ffs(grp) - 1) {
+        atomicAdd(&v.g->attempts, (unsigned long long)__popc(grp));
+        const unsigned ns = __popc(grp & specm);
+        if (ns) atomicAdd(&v.g->speculative, (unsigned long long)ns);
+      }
+      const unsigned hi = __reduce_max_sync(0xffffffffu, on ? (unsigned)tid + 1u : 0u);
+      if (lane == 0 && hi) atomicMax(&sm.span, hi);
+      if (a.alog && on) {  // Assignment{slot, task, attempt, kappa} (scheduler.hpp:14-19)
+        const unsigned long long idx = atomicAdd(&a.log->alog_count, 1ull);
+        if (idx < a.alog_cap) {
+          const unsigned k0 = v.kappa0 ? ld_weak(v.kappa0 + task) : 0u;
+          reinterpret_cast<uint4*>(a.alog)[idx] =
+              make_uint4((unsigned)cta * kSignThreads + tid, task, att, k0 + att * P::L);
+        }
+      }
       const unsigned n_on = __syncthreads_count(on);
       const unsigned n_spec = __syncthreads_count(on && depth > 0);
+      if (warp == 0) {  // a round counts for every batch present; idle slots go to the oldest
+        const bool present = lane < kWindow && sm.bcnt[lane] > 0;
+        const unsigned pm = __ballot_sync(0xffffffffu, present);
+        if (present) {
+          atomicAdd(&sm.bv[lane].g->rounds, 1ull);
+          if (lane == __ffs(pm) - 1 && a.slots > n_on)
+            atomicAdd(&sm.bv[lane].g->idle_slots, (unsigned long long)(a.slots - n_on));
+        }
+      }
       if (tid == 0) {
-        sm.st_rounds += 1;
-        sm.st_attempts += n_on;
-        sm.st_spec += n_spec;
-        sm.st_idle += a.slots - n_on;
+        sm.rounds += 1;
         sm.r_on = n_on;
         sm.r_spec = n_spec;
       }
@@ -532,21 +671,21 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
     // streams (nonces kappa .. kappa + L - 1), so when a round runs fewer slots than the CTA
     // has threads -- small batches, the tail of a large one -- they spread over the idle
     // threads and the round's longest sequential Keccak chain shrinks from 5 L permutations
-    // towards 5.  Active slots are a prefix [0, span); items are laid out polynomial-major so
+    // towards 5.  Active slots lie in [0, span); items are laid out polynomial-major so
     // the lanes of a warp share j.  With all 128 slots active this is thread t -> slot t,
-    // j = 0 .. L-1, as before.
+    // j = 0 .. L-1.
     {
-      const unsigned cap = a.speculate ? a.spec_depth + 1u : 1u;
-      const unsigned span = min(a.slots, U * cap);
+      const unsigned span = sm.span;
 #pragma unroll 1
       for (unsigned item = tid; item < span * P::L; item += kSignThreads) {
         const unsigned slot = item % span, j = item / span;
         const unsigned task = sm.slot_task[slot];
         if (task == kNoSlot) continue;
-        const unsigned k0 = a.kappa0 ? a.kappa0[task] : 0u;
+        const BatchView& v = sm.bv[sm.slot_batch[slot]];
+        const unsigned k0 = v.kappa0 ? ld_weak(v.kappa0 + task) : 0u;
         const unsigned kappa = k0 + sm.slot_attempt[slot] * P::L;
-        expand_mask_stream<P>(a.rho_prime + (size_t)task * 8, kappa + j,
-                              ybytes + (size_t)slot * Z::Y_SLOT + j * S::Z_POLY);
+        expand_mask_stream<P, false>(v.rho_prime + (size_t)task * 8, kappa + j,
+                                     ybytes + (size_t)slot * Z::Y_SLOT + j * S::Z_POLY);
       }
     }
     __syncthreads();
@@ -567,6 +706,11 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       }
       return (int)__shfl_sync(0xffffffffu, s, 0);
     };
+    auto key_of = [&](int s) -> size_t {  // key table index of the task in slot s
+      const BatchView& v = sm.bv[sm.slot_batch[s]];
+      return v.key_idx ? (size_t)ld_weak(v.key_idx + sm.slot_task[s])
+                       : (size_t)sm.slot_task[s] * v.key_stride;
+    };
     {
       int s = grab(&sm.cursor2);
       if (s < kSignThreads) {  // prologue: first mask polynomial of the first slot
@@ -577,12 +721,10 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
 #pragma unroll 1
       while (s < kSignThreads) {
         const int nx = grab(&sm.cursor2);
-        const size_t key = a.key_idx ? (size_t)__ldg(a.key_idx + sm.slot_task[s])
-                                     : (size_t)sm.slot_task[s] * a.key_stride;
         stage_w<P>(sm.u.a.ws[warp], pp, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
                    nx < kSignThreads ? ybytes + (size_t)nx * Z::Y_SLOT : nullptr,
-                   a.A + key * (P::K * P::L * kN), wbuf + (size_t)s * Z::W_SLOT,
-                   w1buf + (size_t)s * S::W1_ALL);
+                   sm.bv[sm.slot_batch[s]].A + key_of(s) * (P::K * P::L * kN),
+                   wbuf + (size_t)s * Z::W_SLOT, w1buf + (size_t)s * S::W1_ALL);
         s = nx;
       }
       cp_async_wait<0>();
@@ -594,7 +736,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       if (my_task != kNoSlot) {
         uint64_t ct[CTW];
         hash_ctilde_stream<S::W1_ALL, false, CTW>(
-            a.mu + (size_t)my_task * 8,
+            sm.bv[sm.slot_batch[tid]].mu + (size_t)my_task * 8,
             reinterpret_cast<const uint64_t*>(w1buf + (size_t)tid * S::W1_ALL), ct);
 #pragma unroll
         for (int w = 0; w < CTW; ++w) ctbuf[tid * CTW + w] = ct[w];
@@ -624,14 +766,17 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
 #pragma unroll 1
       while (s < kSignThreads) {
         const int nx = grab(&sm.cursor4);
-        const size_t key = a.key_idx ? (size_t)__ldg(a.key_idx + sm.slot_task[s])
-                                     : (size_t)sm.slot_task[s] * a.key_stride;
-        const bool ok = stage_finish<P>(
+        const BatchView& v = sm.bv[sm.slot_batch[s]];
+        const int rej = stage_finish<P, DBG>(
             sm.u.a.ws[warp], pp, par, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
             wbuf + (size_t)s * Z::W_SLOT, nx < kSignThreads ? c8buf + (size_t)nx * kN : nullptr,
-            ctbuf + s * CTW, a.shat + key * ((P::L + 2 * P::K) * kN),
-            staging + (size_t)s * Z::SIG_PAD);
-        if (lane == 0) sm.slot_valid[s] = ok ? 1 : 0;
+            ctbuf + s * CTW, v.shat + key_of(s) * ((P::L + 2 * P::K) * kN),
+            staging + (size_t)s * Z::SIG_PAD, v.bounds);
+        if (lane == 0) {
+          sm.slot_valid[s] = rej == 0 ? 1 : 0;
+          // RejectStage of the reference (scheme.hpp:34): 0 z, 1 r0, 2 c t0, 3 hint weight; 255 accepted
+          if (DBG && v.dbg_stage) v.dbg_stage[sm.slot_task[s]] = rej ? (uint8_t)(rej - 1) : (uint8_t)255;
+        }
         s = nx;
         par ^= 1;
       }
@@ -641,13 +786,15 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
 
     // ---- commit: smallest valid attempt per task wins (scheduler.hpp:97-136) --------
     bool keep = false;
-    unsigned my_u_task = 0, my_u_next = 0;
+    unsigned my_u_task = 0, my_u_next = 0, my_u_batch = 0;
     if ((unsigned)tid < U) {
       const unsigned task = sm.utask[tid];
       unsigned next = sm.unext[tid];
+      const unsigned bi = sm.ubatch[tid];
+      const BatchView& v = sm.bv[bi];
       int win = -1;
       unsigned ran = 0;
-      for (unsigned s = tid; s < a.slots; s += U) {
+      for (unsigned s = tid; s < (unsigned)kSignThreads; s += U) {
         if (sm.slot_task[s] == kNoSlot) break;
         ++ran;
         if (sm.slot_valid[s]) {
@@ -655,29 +802,31 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
           break;
         }
       }
-      if (a.dbg_ctilde) {
+      if (v.dbg_ctilde) {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(ctbuf + tid * CTW);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(a.dbg_ctilde + (size_t)task * Hashing<P>::CT);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(v.dbg_ctilde + (size_t)task * Hashing<P>::CT);
         for (int w = 0; w < 2 * CTW; ++w) dst[w] = src[w];
       }
       if (win >= 0) {
         const unsigned ordinal = sm.slot_attempt[win] + 1;
-        if (a.attempts_out) a.attempts_out[task] = ordinal;
-        if (a.failed_out) a.failed_out[task] = 0;
-        atomicAdd(&a.q->accepted_sum, (unsigned long long)ordinal);
+        if (v.attempts_out) v.attempts_out[task] = ordinal;
+        if (v.failed_out) v.failed_out[task] = 0;
+        atomicAdd(&v.g->accepted_sum, (unsigned long long)ordinal);
       } else {
         next += ran;
-        if (next > a.max_attempt || a.single_round) {
+        if (next > v.max_attempt || a.single_round) {
           win = -2;  // nonce space exhausted (scheduler.hpp:122-128)
-          if (a.attempts_out) a.attempts_out[task] = 0;
-          if (a.failed_out) a.failed_out[task] = 1;
-          atomicAdd(&a.q->failed, 1ull);
+          if (v.attempts_out) v.attempts_out[task] = 0;
+          if (v.failed_out) v.failed_out[task] = 1;
+          atomicAdd(&v.g->failed, 1ull);
         }
       }
       sm.winner[tid] = win;
       keep = win == -1;
+      if (!keep) atomicAdd(&sm.bfin[bi], 1u);
       my_u_task = task;
       my_u_next = next;
+      my_u_batch = bi;
     }
     // compact the open-task table
     {
@@ -691,38 +840,64 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
         total += sm.warp_sums[w];
       }
       const unsigned pos = off + __popc(bal & ((1u << lane) - 1));
-      // copy winners' staged signatures out before the table is overwritten
+      // copy winners' staged signatures out before the table is overwritten; a failed task's
+      // signature is all zero like the reference's (batch.hpp:128-131 leaves the default array)
 #pragma unroll 1
       for (unsigned u = warp; u < U; u += kSignWarps) {
         const int win = sm.winner[u];
-        if (win < 0) continue;
-        const uint8_t* src = staging + (size_t)win * Z::SIG_PAD;
-        uint8_t* dst = a.sigs + (size_t)sm.utask[u] * S::SIG;
+        if (win == -1) continue;
+        const uint8_t* src = staging + (size_t)(win < 0 ? 0 : win) * Z::SIG_PAD;
+        uint8_t* dst = sm.bv[sm.ubatch[u]].sigs + (size_t)sm.utask[u] * S::SIG;
         // word-granular, coalesced copy to a destination of any alignment (sig_bytes is
         // odd at levels 3/5): the destination may be pinned host memory, where 128-byte
         // write bursts matter
         const unsigned head = (4u - (unsigned)(reinterpret_cast<uintptr_t>(dst) & 3)) & 3u;
-        if (lane < (int)head) dst[lane] = src[lane];
         const unsigned nwords = (S::SIG - head) / 4;
         uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
+        const unsigned done = head + 4 * nwords;
+        if (win < 0) {
+          if (lane < (int)head) dst[lane] = 0;
+          for (unsigned w = lane; w < nwords; w += 32) d32[w] = 0;
+          if (lane < (int)(S::SIG - done)) dst[done + lane] = 0;
+          continue;
+        }
+        if (lane < (int)head) dst[lane] = src[lane];
         const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);  // staging is 16-byte aligned
         for (unsigned w = lane; w < nwords; w += 32)
           d32[w] = head ? __funnelshift_r(s32[w], s32[w + 1], 8 * head) : s32[w];
-        const unsigned done = head + 4 * nwords;
         if (lane < (int)(S::SIG - done)) dst[done + lane] = src[done + lane];
       }
       __syncthreads();
       if (keep) {
         sm.utask[pos] = my_u_task;
         sm.unext[pos] = my_u_next;
+        sm.ubatch[pos] = (uint8_t)my_u_batch;
+      }
+      // per-batch completion: everything this CTA wrote for the finished tasks is made
+      // visible system-wide before `done` moves; whoever completes the batch raises its flag
+      if (tid < kWindow && sm.bfin[tid]) {
+        const unsigned f = sm.bfin[tid];
+        sm.bfin[tid] = 0;
+        sm.bcnt[tid] -= f;
+        const BatchView& v = sm.bv[tid];
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        atomicMin(&v.g->t_first_exit, now);
+        __threadfence_system();
+        const unsigned old = atomicAdd(&v.g->done, f);
+        if (old + f == v.n) {
+          atomicMax(&v.g->t_last_exit, now);
+          __threadfence_system();
+          *v.g->host_flag = a.ticket + tid + 1u;
+        }
       }
       if (tid == 0) {
         if (a.trace) {  // RoundTrace of this CTA's round (scheduler.hpp:21-28)
-          const unsigned long long idx = atomicAdd(&a.q->trace_count, 1ull);
+          const unsigned long long idx = atomicAdd(&a.log->trace_count, 1ull);
           if (idx < a.trace_cap) {
             uint4* rec = reinterpret_cast<uint4*>(a.trace + idx * 8);
-            rec[0] = make_uint4(blockIdx.x, (unsigned)sm.st_rounds - 1u, U, sm.r_on);
-            rec[1] = make_uint4(sm.r_spec, a.slots - sm.r_on, U - total, 0u);
+            rec[0] = make_uint4(blockIdx.x, sm.rounds - 1u, U, sm.r_on);
+            rec[1] = make_uint4(sm.r_spec, a.slots > sm.r_on ? a.slots - sm.r_on : 0u, U - total, a.ticket);
           }
         }
         sm.U = total;
@@ -730,79 +905,244 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       __syncthreads();
     }
   }
-  if (tid == 0) {
-    unsigned long long now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    atomicMin(&a.q->t_first_exit, now);
-    atomicMax(&a.q->t_last_exit, now);
-    atomicAdd(&a.q->rounds, sm.st_rounds);
-    atomicAdd(&a.q->attempts, sm.st_attempts);
-    atomicAdd(&a.q->speculative, sm.st_spec);
-    atomicAdd(&a.q->idle_slots, sm.st_idle);
-  }
 }
 
 // ---- host side ---------------------------------------------------------------------
+//
+// Submission and completion are separate (dlb_sign_submit / dlb_sign_wait); the synchronous
+// entry points are submit + wait.  Everything a submission needs is enqueued on the stream lane
+// of its ticket: inputs, the descriptor body, the per-key and per-task precomputation, the
+// gate word that publishes the batch to running scheduler kernels, and the batch's own
+// scheduler kernel.  The precompute kernels use one-warp CTAs so they fit beside a fully
+// resident scheduler grid (114 registers x 512 threads leave one warp's worth per SM).
 
+namespace {
+
+// Stream lane (and scratch set) for the scheduler kernel of a ticket: the lowest lane whose last
+// kernel has finished -- synchronous callers only ever touch lane 0 -- else round robin.
+inline int pick_lane(dlb_ctx* c, unsigned ticket) {
+  for (int l = 0; l < kLanes; ++l)
+    if (!c->lane_used[l] || cudaEventQuery(c->lane_done[l]) == cudaSuccess) return l;
+  return (int)(ticket % kLanes);
+}
+
+int sign_state_init(dlb_ctx* c) {
+  if (c->sign_ready) return 0;
+  DLB_CUDA_CHECK(cudaMalloc(&c->d_ring, kRing * sizeof(SignBatch)));
+  DLB_CUDA_CHECK(cudaMemset(c->d_ring, 0, kRing * sizeof(SignBatch)));
+  DLB_CUDA_CHECK(cudaMalloc(&c->d_log, sizeof(SignLog)));
+  DLB_CUDA_CHECK(cudaMemset(c->d_log, 0, sizeof(SignLog)));
+  DLB_CUDA_CHECK(cudaHostAlloc(&c->h_ring, kRing * sizeof(SignBatch), cudaHostAllocDefault));
+  memset(c->h_ring, 0, kRing * sizeof(SignBatch));
+  DLB_CUDA_CHECK(cudaHostAlloc(&c->h_flags, kRing * sizeof(unsigned), cudaHostAllocMapped));
+  memset((void*)c->h_flags, 0, kRing * sizeof(unsigned));
+  DLB_CUDA_CHECK(cudaHostGetDevicePointer((void**)&c->d_flags, (void*)c->h_flags, 0));
+  for (int l = 0; l < kLanes; ++l)
+    DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->sign_lane[l], cudaStreamNonBlocking));
+  for (int l = 0; l < kLanes; ++l)
+    DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->lane_done[l], cudaEventDisableTiming));
+  DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->sign_pub, cudaStreamNonBlocking));
+  DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->sign_pubd, cudaEventDisableTiming));
+  for (int r = 0; r < kRing; ++r) {
+    DLB_CUDA_CHECK(cudaEventCreate(&c->sign_evs[r]));
+    DLB_CUDA_CHECK(cudaEventCreate(&c->sign_ev0[r]));
+    DLB_CUDA_CHECK(cudaEventCreate(&c->sign_ev1[r]));
+  }
+  DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->sign_dep, cudaEventDisableTiming));
+  c->sign_ready = true;
+  return 0;
+}
+
+template <class P, bool DBG>
+int sign_kernel_config(dlb_ctx* c, int* occ_out, size_t* smem_out) {
+  static_assert(sizeof(SignSmem<P>) <= 56 * 1024, "four CTAs per SM");
+  const int li = level_index(P::LEVEL) * 2 + (DBG ? 1 : 0);
+  if (!c->sign_occ[li]) {
+    const size_t smem_bytes = sizeof(SignSmem<P>) + c->knob_sign_pad_smem;
+    DLB_CUDA_CHECK(cudaFuncSetAttribute(k_sign_persistent<P, DBG>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    int occ = 0;
+    DLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sign_persistent<P, DBG>,
+                                                                 kSignThreads, smem_bytes));
+    // Registers are per SM sub-partition: four resident CTAs (16 warps x 120 registers) leave
+    // 1,024 registers in each -- no room for a single warp of any Keccak kernel, so the
+    // precompute kernels of the NEXT batch could not start before CTAs of this one exit.  Three
+    // resident CTAs per SM cost ~1 % of the scheduler's throughput (occupancy is not its
+    // limiter, profiles/r01_summary.md section 3) and leave a quarter of every SM to them.
+    if (c->knob_sign_occ && occ > (int)c->knob_sign_occ) occ = (int)c->knob_sign_occ;
+    c->sign_occ[li] = occ < 1 ? 1 : occ;
+    c->sign_smem[li] = smem_bytes;
+    // One L1 / shared-memory split for the scheduler kernel and the precompute kernels that must
+    // run beside its resident grid: a kernel preferring another split waits until the SM has
+    // drained (profiles/r01_summary.md, negative results), which would delay the publication of
+    // the next batch to the tail of this one.  Smallest split that holds the resident CTAs.
+    const size_t need = (size_t)c->sign_occ[li] * (smem_bytes + 1024);
+    int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+    if (pct > 100) pct = 100;
+    c->sign_carveout[li] = pct;
+    prefer_carveout(k_sign_persistent<P, DBG>, pct);
+    prefer_carveout(k_expand_a<P, 1>, pct);
+    prefer_carveout(k_sign_unpack<P, 1>, pct);
+  }
+  *occ_out = c->sign_occ[li];
+  *smem_out = c->sign_smem[li];
+  return 0;
+}
+
+// eta range check of the packed secret vectors (packing.hpp:79-86) on the host
 template <class P>
-static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, size_t n_keys,
-                     const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off, const uint64_t* d_mu_in,
-                     const uint8_t* d_rho_prime, const uint32_t* d_kappa0, size_t psi,
-                     int speculate, int single_round, uint8_t* d_sigs, uint32_t* d_attempts,
-                     uint8_t* d_failed, uint8_t* d_dbg_ct, dlb_sign_stats* stats) {
+bool sk_eta_ok(const uint8_t* sk) {
+  const uint8_t* p = sk + Sizes<P>::SK_S1;
+  const size_t fields = (size_t)(P::K + P::L) * kN;
+  uint64_t acc = 0;
+  unsigned nbits = 0;
+  size_t seen = 0;
+  while (seen < fields) {
+    acc |= (uint64_t)(*p++) << nbits;
+    nbits += 8;
+    while (nbits >= (unsigned)P::ETA_BITS && seen < fields) {
+      if ((acc & ((1u << P::ETA_BITS) - 1)) > 2u * P::ETA) return false;
+      acc >>= P::ETA_BITS;
+      nbits -= P::ETA_BITS;
+      ++seen;
+    }
+  }
+  return true;
+}
+
+inline uint64_t fnv1a(const uint8_t* p, size_t n) {
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
+  return h;
+}
+
+// Finds or builds the cache entry of a shared key (host bytes hk, device copy dsk); the per-key
+// kernels of a miss run on `st`.
+// Returns nullptr when the cache is off or full of entries that batches in flight may use.
+template <class P>
+KeyCacheEntry* key_cache_get(dlb_ctx* c, const uint8_t* hk, const uint8_t* dsk, cudaStream_t st, int* rc) {
+  using S = Sizes<P>;
+  constexpr int KL = P::K * P::L, PV = P::L + 2 * P::K;
+  *rc = 0;
+  if (!c->knob_key_cache) return nullptr;
+  const uint64_t h = fnv1a(hk, S::SK);
+  for (auto& e : c->key_cache)
+    if (e.level == P::LEVEL && e.hash == h && memcmp(e.sk.data(), hk, S::SK) == 0) {
+      e.last_use = ++c->key_cache_clock;
+      ++c->key_cache_hits;
+      cudaStreamWaitEvent(st, e.ready, 0);
+      return &e;
+    }
+  ++c->key_cache_misses;
+  KeyCacheEntry* e = nullptr;
+  if (c->key_cache.size() < c->knob_key_cache) {
+    c->key_cache.emplace_back();
+    e = &c->key_cache.back();
+  } else {
+    for (int r = 0; r < kRing; ++r)
+      if (c->tickets[r].active) return nullptr;  // an entry may be in use: sign uncached this time
+    for (auto& x : c->key_cache)
+      if (!e || x.last_use < e->last_use) e = &x;
+  }
+  if (!e->A) {  // entries are sized for the largest parameter set and reused across levels
+    constexpr size_t kMaxKL = 8 * 7, kMaxPV = 7 + 2 * 8;
+    if (cudaMalloc(&e->A, kMaxKL * kN * 4) != cudaSuccess || cudaMalloc(&e->shat, kMaxPV * kN * 4) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ready, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      if (e->A) cudaFree(e->A);
+      if (e->shat) cudaFree(e->shat);
+      c->key_cache.pop_back();
+      *rc = DLB_E_NOMEM;
+      return nullptr;
+    }
+  }
+  e->level = P::LEVEL;
+  e->hash = h;
+  e->sk.assign(hk, hk + S::SK);
+  e->last_use = ++c->key_cache_clock;
+  unsigned* bad;
+  *rc = dalloc(c, "s.kbad", 1, &bad);
+  if (*rc != 0) return nullptr;
+  k_expand_a<P, 1><<<cdiv(KL, 32), 32, 0, st>>>(dsk, 0, (unsigned)KL, e->A);
+  k_sign_unpack<P, 1><<<(unsigned)PV, 32, 0, st>>>(1u, dsk, 0, e->shat, bad);  // range already checked
+  cudaEventRecord(e->ready, st);
+  c->launches += 2;
+  return e;
+}
+
+}  // namespace
+
+// Everything that publishes a batch (input copies, descriptor, per-key kernels of uncached keys,
+// gate) goes through one publication stream that never holds a scheduler kernel, so it cannot
+// queue up behind a running one; the scheduler kernel of the ticket then goes to its lane.
+int sign_reserve(dlb_ctx* c, unsigned* ticket, cudaStream_t* pub) {
+  DLB_TRY(sign_state_init(c));
+  const unsigned t = c->next_ticket;
+  if (c->tickets[t % kRing].active) return DLB_E_BUSY;  // kRing batches in flight: wait for the oldest first
+  *ticket = t;
+  *pub = c->sign_pub;
+  cudaStream_t* lane = pub;
+  int set = 0;
+  while (set < kRing - 1 && c->set_busy[set]) ++set;  // at most kRing - 1 others are in flight
+  c->cur_set = set;
+  // inputs produced on the caller's stream (the *_dev entry points) are ordered before the lane's work
+  DLB_CUDA_CHECK(cudaEventRecord(c->sign_dep, c->s()));
+  DLB_CUDA_CHECK(cudaStreamWaitEvent(*lane, c->sign_dep, 0));
+  return 0;
+}
+
+template <class P, bool DBG>
+static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   using S = Sizes<P>;
   using Z = SignSizes<P>;
   constexpr int KL = P::K * P::L, PV = P::L + 2 * P::K;
-  if (n == 0) return 0;
-  if (n > 0x7fffffffu) return DLB_E_ARG;
-  cudaStream_t st = c->s();
-  if (d_key_idx && (n_keys == 0 || sk_stride == 0)) return DLB_E_ARG;
+  const size_t n = io.n;
+  if (n == 0 || n > 0x7fffffffu) return DLB_E_ARG;
+  if (io.d_key_idx && (io.n_keys == 0 || io.sk_stride == 0)) return DLB_E_ARG;
+  const int slot = (int)(ticket % kRing), ln = pick_lane(c, ticket);
+  cudaStream_t st = c->sign_pub, lane = c->sign_lane[ln];
   // distinct keys to precompute: the key table, one key per task, or one shared key
-  const size_t nk = d_key_idx ? n_keys : (sk_stride ? n : 1);
+  const size_t nk = io.d_key_idx ? io.n_keys : (io.sk_stride ? n : 1);
 
-  int32_t *A, *shat;
+  PhaseProf prof;
+  int32_t *A = nullptr, *shat = nullptr;
   uint64_t *mu, *rp;
-  SignQueue* q;
-  DLB_TRY(dalloc(c, "s.A", nk * KL * kN, &A));
-  DLB_TRY(dalloc(c, "s.shat", nk * PV * kN, &shat));
-  DLB_TRY(dalloc(c, "s.mu", n * 8, &mu));
-  DLB_TRY(dalloc(c, "s.rp", n * 8, &rp));
-  DLB_TRY(dalloc(c, "s.q", 1, &q));
-  DLB_CUDA_CHECK(cudaMemsetAsync(q, 0, sizeof(SignQueue), st));
-  DLB_CUDA_CHECK(cudaMemsetAsync(&q->t_first_start, 0xFF, 8, st));
-  DLB_CUDA_CHECK(cudaMemsetAsync(&q->t_first_exit, 0xFF, 8, st));
-
-  // per-key precomputation (scheme.hpp:106-125)
-  k_expand_a<P, 4><<<cdiv(nk * KL, 128), 128, 0, st>>>(d_sks, sk_stride, (unsigned)(nk * KL), A);
-  k_sign_unpack<P, 4><<<cdiv(nk * PV, 4), 128, 0, st>>>((unsigned)nk, d_sks, sk_stride, shat,
-                                                        &q->key_bad);
-  c->launches += 2;
-  // mu = H(tr || M), rho' = H(K || mu)  (scheme.hpp:240-248)
-  const uint64_t* mu_use = mu;
-  const uint64_t* rp_use = rp;
-  if (d_mu_in) {
-    mu_use = d_mu_in;  // stage tests supply mu and rho' directly
-    rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
-  } else {
-    const uint8_t* pfx = nullptr;
-    unsigned plen = 0;
-    if (Hashing<P>::MLDSA) DLB_TRY(mldsa_prefix(c, st, &pfx, &plen));
-    k_hash_mu<Hashing<P>::MLDSA><<<cdiv(n, 128), 128, 0, st>>>(
-        d_sks + 64, sk_stride, d_sks + 32, sk_stride, d_key_idx, pfx, plen, d_msgs, d_msg_off,
-        (unsigned)n, mu, d_rho_prime ? nullptr : rp);
-    c->launches += 1;
-    if (d_rho_prime) rp_use = reinterpret_cast<const uint64_t*>(d_rho_prime);
+  // a shared key is looked up in (or added to) the cross-call cache: a hit needs no per-key kernels
+  bool cached = false;
+  if (nk == 1 && !io.single_round) {
+    std::vector<uint8_t> tmp;
+    const uint8_t* hk = io.h_sks;
+    if (!hk && c->knob_key_cache) {  // device-resident key: fetch its bytes for the lookup
+      tmp.resize(S::SK);
+      DLB_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), io.d_sks, S::SK, cudaMemcpyDeviceToHost, c->s()));
+      DLB_CUDA_CHECK(cudaStreamSynchronize(c->s()));
+      hk = tmp.data();
+    }
+    if (hk) {
+      if (!sk_eta_ok<P>(hk)) return DLB_E_KEY;  // packing.hpp:79-86: nothing is signed
+      int rc = 0;
+      if (KeyCacheEntry* e = key_cache_get<P>(c, hk, io.d_sks, st, &rc)) {
+        A = e->A;
+        shat = e->shat;
+        cached = true;
+      } else if (rc != 0) {
+        return rc;
+      }
+    }
   }
+  if (!cached) {
+    DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "s.A"), nk * KL * kN, &A));
+    DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "s.shat"), nk * PV * kN, &shat));
+  }
+  DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "s.mu"), n * 8, &mu));
+  DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "s.rp"), n * 8, &rp));
 
   // grid: resident CTAs of the persistent kernel
   int occ = 0;
-  size_t smem_bytes = sizeof(SignSmem<P>);
-  if (const char* e = getenv("DLB_SIGN_PAD_SMEM")) smem_bytes += (size_t)atoi(e);  // occupancy experiments
-  DLB_CUDA_CHECK(cudaFuncSetAttribute(k_sign_persistent<P>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-  DLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sign_persistent<P>,
-                                                               kSignThreads, smem_bytes));
-  if (occ < 1) occ = 1;
+  size_t smem_bytes = 0;
+  prof.mark(" arenas");
+  DLB_TRY((sign_kernel_config<P, DBG>(c, &occ, &smem_bytes)));
+  prof.mark(" config");
   const size_t grid_max = (size_t)c->sm_count * occ;
   // Psi = resident attempt slots (BatchConfig::psi).  Default (measured, profiles/
   // r01_summary.md): nine slots per task -- the speculation depth cap plus one -- while that
@@ -812,9 +1152,9 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   // machine's capacity is spread over as many CTAs as there are tasks (up to the resident
   // maximum), each using fewer of its 128 slots: the warp-per-slot stages of a round then
   // take proportionally less time.
-  size_t want_slots = psi;
+  size_t want_slots = io.psi;
   if (!want_slots) {
-    if (!speculate) want_slots = n;
+    if (!io.speculate) want_slots = n;
     else want_slots = 9 * n <= grid_max * 32 ? 9 * n : 3 * n;
   }
   if (want_slots < 1) want_slots = 1;
@@ -833,59 +1173,176 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
   }
   size_t tcap = (n + grid - 1) / grid;
   if (tcap > slots_per) tcap = slots_per;
-  if (single_round) {
+  if (io.single_round) {
     slots_per = kSignThreads;
     tcap = kSignThreads;
     grid = (n + kSignThreads - 1) / kSignThreads;
   }
 
-  SignArgs a;
-  memset(&a, 0, sizeof a);
-  a.n = (unsigned)n;
-  a.tcap = (unsigned)tcap;
-  a.slots = (unsigned)slots_per;
-  a.max_attempt = (65535u - (P::L - 1)) / P::L;
-  a.speculate = single_round ? 0 : speculate;
+  // ---- descriptor body (everything but the gate), then the precomputation it points at
+  SignBatch& h = c->h_ring[slot];
+  memset(&h, 0, sizeof h);
+  h.n = (unsigned)n;
+  h.tcap = (unsigned)tcap;
+  h.max_attempt = (65535u - (P::L - 1)) / P::L;
+  if (c->dbg_max_attempt && c->dbg_max_attempt < h.max_attempt) h.max_attempt = c->dbg_max_attempt;
   // Deepest speculative attempt a task may run in one round.  Filling every idle slot
   // (the reference's pass 2) wastes work once few tasks remain: attempt d is only needed
   // with probability (1-p)^d.  Measured on B200 (profiles/r01_summary.md): cap 8 gives the
   // best batch-10k latency and batch-100k throughput; speculate > 1 sets the cap explicitly.
-  a.spec_depth = speculate > 1 ? (unsigned)speculate : 8u;
-  if (const char* e = getenv("DLB_SPEC_DEPTH")) a.spec_depth = (unsigned)atoi(e);  // experiments
-  a.single_round = single_round;
-  a.mu = mu_use;
-  a.rho_prime = rp_use;
-  a.kappa0 = d_kappa0;
-  a.A = A;
-  a.shat = shat;
-  a.key_stride = sk_stride ? 1u : 0u;
-  a.key_idx = d_key_idx;
-  if (c->trace_cap && !single_round) {
+  h.spec_depth = io.single_round || !io.speculate ? 0u
+                 : (io.speculate > 1 ? (unsigned)io.speculate : c->knob_spec_depth);
+  h.key_stride = io.sk_stride ? 1u : 0u;
+  h.level = P::LEVEL;
+  h.exclusive = (io.single_round || DBG) ? 1u : 0u;
+  h.ticket1 = ticket + 1u;
+  h.mu = io.d_mu_in ? io.d_mu_in : mu;
+  h.rho_prime = io.d_rho_prime ? reinterpret_cast<const uint64_t*>(io.d_rho_prime) : rp;
+  h.kappa0 = io.d_kappa0;
+  h.A = A;
+  h.shat = shat;
+  h.key_idx = io.d_key_idx;
+  h.sigs = io.d_sigs;
+  h.attempts_out = io.d_attempts;
+  h.failed_out = io.d_failed;
+  h.dbg_ctilde = io.d_dbg_ct;
+  h.dbg_stage = io.d_dbg_stage;
+  for (int i = 0; i < 3; ++i) h.bounds[i] = io.bounds[i];
+  if (!io.d_mu_in) {  // digests are computed by the scheduler when it claims a task
+    h.sk_base = io.d_sks;
+    h.msgs = io.d_msgs;
+    h.msg_off = io.d_msg_off;
+    if (Hashing<P>::MLDSA) DLB_TRY(mldsa_prefix(c, st, &h.pfx, &h.plen));
+    h.mu_w = mu;
+    h.rp_w = io.d_rho_prime ? nullptr : rp;
+  }
+  h.host_flag = c->d_flags + slot;
+  h.t_first_start = h.t_first_exit = ~0ull;
+  h.gate = ticket + 1u;
+  SignBatch* g = c->d_ring + slot;
+  c->h_flags[slot] = 0;
+  cudaEventRecord(c->sign_evs[slot], st);
+  DLB_CUDA_CHECK(cudaMemcpyAsync(g, &h, offsetof(SignBatch, gate), cudaMemcpyHostToDevice, st));
+
+  prof.mark(" body copy");
+  // per-key precomputation (scheme.hpp:106-125), unless the shared key came from the cache
+  if (!cached) {
+    k_expand_a<P, 1><<<cdiv(nk * KL, 32), 32, 0, st>>>(io.d_sks, io.sk_stride, (unsigned)(nk * KL), A);
+    k_sign_unpack<P, 1><<<(unsigned)(nk * PV), 32, 0, st>>>((unsigned)nk, io.d_sks, io.sk_stride, shat,
+                                                           &g->key_bad);
+    c->launches += 2;
+  }
+  prof.mark(" prep launches");
+  // publish: running scheduler kernels of earlier tickets may start claiming tasks now
+  DLB_CUDA_CHECK(cudaMemcpyAsync(&g->gate, &h.gate, sizeof(unsigned), cudaMemcpyHostToDevice, st));
+
+  prof.mark(" gate copy");
+  SignArgs a;
+  memset(&a, 0, sizeof a);
+  a.ring = c->d_ring;
+  a.ticket = ticket;
+  a.window = h.exclusive ? 1u : (unsigned)kWindow;
+  a.slots = (unsigned)slots_per;
+  a.single_round = io.single_round;
+  a.log = c->d_log;
+  if (c->trace_cap && !io.single_round) {
     DLB_TRY(dalloc(c, "s.trace", c->trace_cap * 8, &a.trace));
     a.trace_cap = (unsigned)(c->trace_cap > 0xFFFFFFFFu ? 0xFFFFFFFFu : c->trace_cap);
   }
-  const size_t slots = grid * kSignThreads;
-  DLB_TRY(dalloc(c, "s.y", slots * Z::Y_SLOT + 16, &a.ybytes));
-  DLB_TRY(dalloc(c, "s.w", slots * Z::W_SLOT, &a.wbuf));
-  DLB_TRY(dalloc(c, "s.w1", slots * S::W1_ALL, &a.w1buf));
-  DLB_TRY(dalloc(c, "s.ct", slots * Hashing<P>::CTW, &a.ctbuf));
-  DLB_TRY(dalloc(c, "s.c8", slots * kN, &a.c8buf));
-  DLB_TRY(dalloc(c, "s.stage", slots * Z::SIG_PAD, &a.staging));
-  a.sigs = d_sigs;
-  a.attempts_out = d_attempts;
-  a.failed_out = d_failed;
-  a.dbg_ctilde = d_dbg_ct;
-  a.q = q;
-  cudaEventRecord(c->ev2, st);
-  k_sign_persistent<P><<<(unsigned)grid, kSignThreads, smem_bytes, st>>>(a);
-  cudaEventRecord(c->ev3, st);
+  if (c->alog_cap && !io.single_round) {
+    DLB_TRY(dalloc(c, "s.alog", c->alog_cap * 4, &a.alog));
+    a.alog_cap = (unsigned)(c->alog_cap > 0xFFFFFFFFu ? 0xFFFFFFFFu : c->alog_cap);
+  }
+  if (a.trace || a.alog) DLB_CUDA_CHECK(cudaMemsetAsync(c->d_log, 0, sizeof(SignLog), st));
+  // one scratch set per lane, sized for the full resident grid so it never moves under a
+  // running kernel of the same lane
+  const size_t slots = grid_max * kSignThreads;
+  DLB_TRY(dalloc(c, c->lane_name(ln, "s.y"), slots * Z::Y_SLOT + 16, &a.ybytes));
+  DLB_TRY(dalloc(c, c->lane_name(ln, "s.w"), slots * Z::W_SLOT, &a.wbuf));
+  DLB_TRY(dalloc(c, c->lane_name(ln, "s.w1"), slots * S::W1_ALL, &a.w1buf));
+  DLB_TRY(dalloc(c, c->lane_name(ln, "s.ct"), slots * Hashing<P>::CTW, &a.ctbuf));
+  DLB_TRY(dalloc(c, c->lane_name(ln, "s.c8"), slots * kN, &a.c8buf));
+  DLB_TRY(dalloc(c, c->lane_name(ln, "s.stage"), slots * Z::SIG_PAD, &a.staging));
+  prof.mark(" scratch");
+  DLB_CUDA_CHECK(cudaEventRecord(c->sign_pubd, st));
+  DLB_CUDA_CHECK(cudaStreamWaitEvent(lane, c->sign_pubd, 0));
+  cudaEventRecord(c->sign_ev0[slot], lane);
+  k_sign_persistent<P, DBG><<<(unsigned)grid, kSignThreads, smem_bytes, lane>>>(a);
+  cudaEventRecord(c->sign_ev1[slot], lane);
+  cudaEventRecord(c->lane_done[ln], lane);
+  c->lane_used[ln] = true;
   c->launches += 1;
   DLB_LAUNCH_CHECK();
+  prof.mark(" launch");
 
-  SignQueue hq;
-  DLB_CUDA_CHECK(cudaMemcpyAsync(&hq, q, sizeof hq, cudaMemcpyDeviceToHost, st));
-  DLB_CUDA_CHECK(cudaStreamSynchronize(st));
-  cudaEventElapsedTime(&c->last_main_ms, c->ev2, c->ev3);
+  SignTicket& tk = c->tickets[slot];
+  tk = SignTicket{};
+  tk.active = true;
+  tk.ticket = ticket;
+  tk.level = P::LEVEL;
+  tk.n = n;
+  tk.sig_bytes = S::SIG;
+  tk.had_trace = a.trace != nullptr;
+  tk.had_alog = a.alog != nullptr;
+  tk.set = c->cur_set;
+  c->set_busy[tk.set] = true;
+  c->next_ticket = ticket + 1u;
+  return 0;
+}
+
+template <class P>
+int sign_submit(dlb_ctx* c, unsigned ticket, const SignIo& io) {
+  return io.dbg_bounds ? sign_submit_t<P, true>(c, ticket, io) : sign_submit_t<P, false>(c, ticket, io);
+}
+
+// Blocks until the batch of `ticket` is complete (its flag in mapped host memory), then
+// fetches its counters.  drain = also wait for the batch's own scheduler kernel to exit
+// (the synchronous entry points: kernel time is reported and nothing is left running).
+int sign_wait(dlb_ctx* c, unsigned ticket, dlb_sign_stats* stats, bool drain) {
+  const int slot = (int)(ticket % kRing);
+  SignTicket& tk = c->tickets[slot];
+  if (!c->sign_ready || !tk.active || tk.ticket != ticket) return DLB_E_ARG;
+  struct Release {  // the ticket and its arena set are free again however the wait ends
+    dlb_ctx* c;
+    SignTicket& tk;
+    ~Release() {
+      tk.active = false;
+      c->set_busy[tk.set] = false;
+    }
+  } release{c, tk};
+  volatile unsigned* flag = c->h_flags + slot;
+  unsigned spins = 0;
+  while (*flag != ticket + 1u) {
+    if ((++spins & 0x3FF) == 0) {
+      // safety net: if every lane has drained and the flag is still down, something faulted
+      bool idle = true;
+      for (int l = 0; l <= kLanes && idle; ++l) {
+        const cudaError_t e = cudaStreamQuery(l < kLanes ? c->sign_lane[l] : c->sign_pub);
+        if (e == cudaErrorNotReady) idle = false;
+        else if (e != cudaSuccess) return -1000 - (int)e;
+      }
+      if (idle && *flag != ticket + 1u) return DLB_E_INTERNAL;
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  if (drain) {
+    DLB_CUDA_CHECK(cudaEventSynchronize(c->sign_ev1[slot]));
+    cudaEventElapsedTime(&c->last_main_ms, c->sign_ev0[slot], c->sign_ev1[slot]);
+    cudaEventSynchronize(c->sign_evs[slot]);
+    cudaEventElapsedTime(&c->last_ms, c->sign_evs[slot], c->sign_ev1[slot]);
+  }
+  SignBatch hq;
+  cudaStream_t co = c->copy_out;
+  DLB_CUDA_CHECK(cudaMemcpyAsync(&hq, c->d_ring + slot, sizeof hq, cudaMemcpyDeviceToHost, co));
+  SignLog hl{};
+  if (tk.had_trace || tk.had_alog)
+    DLB_CUDA_CHECK(cudaMemcpyAsync(&hl, c->d_log, sizeof hl, cudaMemcpyDeviceToHost, co));
+  if (tk.h_sigs) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_sigs, tk.d_sigs, tk.n * tk.sig_bytes, cudaMemcpyDeviceToHost, co));
+  if (tk.h_att) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_att, tk.d_att, tk.n * 4, cudaMemcpyDeviceToHost, co));
+  if (tk.h_failed) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_failed, tk.d_failed, tk.n, cudaMemcpyDeviceToHost, co));
+  DLB_CUDA_CHECK(cudaStreamSynchronize(co));
   if (stats) {
     stats->rounds = hq.rounds;
     stats->attempts = hq.attempts;
@@ -898,26 +1355,17 @@ static int sign_core(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_strid
     stats->t_first_exit_ns = hq.t_first_exit;
     stats->t_last_exit_ns = hq.t_last_exit;
   }
-  c->trace_count = a.trace ? hq.trace_count : 0;
-  if (hq.key_bad) return DLB_E_KEY;
+  if (tk.had_trace) c->trace_count = hl.trace_count;
+  if (tk.had_alog) c->alog_count = hl.alog_count;
+  if (hq.key_bad) {  // no signature is produced for a malformed key (scheme.hpp:271)
+    if (tk.zero_host) memset(tk.zero_host, 0, tk.n * tk.sig_bytes);
+    if (tk.zero_dev) cudaMemset(tk.zero_dev, 0, tk.n * tk.sig_bytes);
+    return DLB_E_KEY;
+  }
   return 0;
 }
 
-template <class P>
-int sign_dev(dlb_ctx* c, size_t n, const uint8_t* d_sks, size_t sk_stride, size_t n_keys,
-             const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
-             const uint8_t* d_rho_prime, size_t psi, int speculate, uint8_t* d_sigs,
-             uint32_t* d_attempts, uint8_t* d_failed, dlb_sign_stats* stats) {
-  return sign_core<P>(c, n, d_sks, sk_stride, n_keys, d_key_idx, d_msgs, d_msg_off, nullptr,
-                      d_rho_prime, nullptr, psi, speculate, 0, d_sigs, d_attempts, d_failed, nullptr,
-                      stats);
-}
-
-#define DLB_INST(LV)                                                                            \
-  template int sign_dev<Params<LV>>(dlb_ctx*, size_t, const uint8_t*, size_t, size_t,           \
-                                    const uint32_t*, const uint8_t*, const uint64_t*,           \
-                                    const uint8_t*, size_t, int, uint8_t*, uint32_t*, uint8_t*, \
-                                    dlb_sign_stats*);
+#define DLB_INST(LV) template int sign_submit<Params<LV>>(dlb_ctx*, unsigned, const SignIo&);
 DLB_INST(2)
 DLB_INST(3)
 DLB_INST(5)
@@ -929,72 +1377,109 @@ DLB_INST(87)
 
 using namespace dlb;
 
-// sign_attempt<P> for n independent (key, mu, rho', kappa) tuples: one scheduler round
-// with one attempt per task; z and hints are decoded back from the staged signature.
-extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8_t* sks,
-                                    size_t sk_stride, const uint8_t* mus, const uint8_t* rho_primes,
-                                    const uint32_t* kappas, uint8_t* accepted, uint8_t* c_tilde,
-                                    int32_t* z, int32_t* hints) {
+// sign_attempt<P> (scheme.hpp:225-230) / detail::sign_attempt_bounded<P> (:133-219) for n
+// independent (key, mu, rho', kappa) tuples: one scheduler round with one attempt per task; z
+// and hints are decoded back from the staged signature.  bounds == nullptr runs the production
+// kernel; otherwise the DBG instantiation with the three norm bounds injected, which also
+// reports the reject stage in the reference's check order.
+static int dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride,
+                            const uint8_t* mus, const uint8_t* rho_primes, const uint32_t* kappas,
+                            const int32_t* bounds, uint8_t* accepted, uint8_t* stage, uint8_t* c_tilde,
+                            int32_t* z, int32_t* hints) {
   if (!c || !sks || !mus || !rho_primes || !kappas || !accepted || !c_tilde || !z || !hints)
     return DLB_E_ARG;
+  if (n == 0) return 0;
+  // chknorm refuses bounds above (q-1)/8 (rounding.hpp:65); the device check has the same domain
+  if (bounds)
+    for (int i = 0; i < 3; ++i)
+      if (bounds[i] < 0 || bounds[i] > (kQ - 1) / 8) return DLB_E_ARG;
   cudaSetDevice(c->device);
   auto run = [&](auto p) -> int {
     using P = decltype(p);
     using S = Sizes<P>;
     const size_t nk = sk_stride ? n : 1;
-    uint8_t *dsk, *dsig, *dfail, *dct, *drp;
+    uint8_t *dsk, *dsig, *dfail, *dct, *drp, *dstage;
     uint64_t* dmu;
     uint32_t *dk, *datt;
-    DLB_TRY(dalloc(c, "io.sk", nk * S::SK, &dsk));
+    DLB_TRY(dalloc(c, "dbg.sk", nk * S::SK, &dsk));
     DLB_TRY(dalloc(c, "dbg.a", n * 8, &dmu));
     DLB_TRY(dalloc(c, "dbg.b", n * 64, &drp));
     DLB_TRY(dalloc(c, "dbg.c", n, &dk));
-    DLB_TRY(dalloc(c, "io.sig", n * S::SIG + 8, &dsig));
-    DLB_TRY(dalloc(c, "io.att", n, &datt));
-    DLB_TRY(dalloc(c, "io.fail", n, &dfail));
+    DLB_TRY(dalloc(c, "dbg.sig", n * S::SIG + 8, &dsig));
+    DLB_TRY(dalloc(c, "dbg.att", n, &datt));
+    DLB_TRY(dalloc(c, "dbg.fail", n, &dfail));
     DLB_TRY(dalloc(c, "dbg.d", n * Hashing<P>::CT, &dct));
-    cudaStream_t st = c->s();
+    DLB_TRY(dalloc(c, "dbg.stage", n, &dstage));
+    unsigned t;
+    cudaStream_t st;
+    DLB_TRY(sign_reserve(c, &t, &st));
     DLB_CUDA_CHECK(cudaMemcpyAsync(dsk, sks, nk * S::SK, cudaMemcpyHostToDevice, st));
     DLB_CUDA_CHECK(cudaMemcpyAsync(dmu, mus, n * 64, cudaMemcpyHostToDevice, st));
     DLB_CUDA_CHECK(cudaMemcpyAsync(drp, rho_primes, n * 64, cudaMemcpyHostToDevice, st));
     DLB_CUDA_CHECK(cudaMemcpyAsync(dk, kappas, n * 4, cudaMemcpyHostToDevice, st));
     DLB_CUDA_CHECK(cudaMemsetAsync(dsig, 0, n * S::SIG, st));
-    DLB_TRY(sign_core<P>(c, n, dsk, sk_stride, 0, nullptr, nullptr, nullptr, dmu, drp, dk, 0, 0, 1,
-                         dsig, datt, dfail, dct, nullptr));
+    DLB_CUDA_CHECK(cudaMemsetAsync(dstage, 0xFF, n, st));
+    SignIo io;
+    io.n = n;
+    io.d_sks = dsk;
+    io.sk_stride = sk_stride;
+    io.d_mu_in = dmu;
+    io.d_rho_prime = drp;
+    io.d_kappa0 = dk;
+    io.speculate = 0;
+    io.single_round = 1;
+    io.d_sigs = dsig;
+    io.d_attempts = datt;
+    io.d_failed = dfail;
+    io.d_dbg_ct = dct;
+    if (bounds) {
+      io.dbg_bounds = true;
+      io.d_dbg_stage = dstage;
+      for (int i = 0; i < 3; ++i) io.bounds[i] = bounds[i];
+    }
+    const int src = sign_submit<P>(c, t, io);
+    if (src != 0) {
+      cudaStreamSynchronize(st);
+      return src;
+    }
+    const int wrc = sign_wait(c, t, nullptr, true);
+    if (wrc != 0 && wrc != DLB_E_KEY) return wrc;
     uint8_t* hsig = new uint8_t[n * S::SIG];
     uint8_t* hfail = new uint8_t[n];
     cudaMemcpyAsync(hsig, dsig, n * S::SIG, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(hfail, dfail, n, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(c_tilde, dct, n * Hashing<P>::CT, cudaMemcpyDeviceToHost, st);
+    if (stage) cudaMemcpyAsync(stage, dstage, n, cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) {
       memset(z, 0, n * P::L * kN * 4);
       memset(hints, 0, n * P::K * kN * 4);
-      for (size_t t = 0; t < n; ++t) {
-        accepted[t] = hfail[t] ? 0 : 1;
-        if (!accepted[t]) continue;
-        const uint8_t* sg = hsig + t * S::SIG;
+      for (size_t t2 = 0; t2 < n; ++t2) {
+        accepted[t2] = hfail[t2] ? 0 : 1;
+        if (!accepted[t2]) continue;
+        const uint8_t* sg = hsig + t2 * S::SIG;
         for (int j = 0; j < P::L; ++j)
           for (int m = 0; m < kN; ++m) {
             const size_t bit = (size_t)m * P::Z_BITS;
             uint32_t raw = 0;
             for (int b = 0; b < P::Z_BITS; ++b)
               raw |= (uint32_t)((sg[S::SIG_Z + j * S::Z_POLY + ((bit + b) >> 3)] >> ((bit + b) & 7)) & 1) << b;
-            z[(t * P::L + j) * kN + m] = P::GAMMA1 - (int32_t)raw;
+            z[(t2 * P::L + j) * kN + m] = P::GAMMA1 - (int32_t)raw;
           }
         const uint8_t* h = sg + S::SIG_Z + P::L * S::Z_POLY;
         unsigned prev = 0;
         for (int i = 0; i < P::K; ++i) {
           const unsigned cnt = h[P::OMEGA + i];
           for (unsigned k = prev; k < cnt && k < (unsigned)P::OMEGA; ++k)
-            hints[(t * P::K + i) * kN + h[k]] = 1;
+            hints[(t2 * P::K + i) * kN + h[k]] = 1;
           prev = cnt;
         }
       }
     }
     delete[] hsig;
     delete[] hfail;
-    return e == cudaSuccess ? 0 : -1000 - (int)e;
+    if (e != cudaSuccess) return -1000 - (int)e;
+    return wrc;
   };
   switch (level) {
     case 2: return run(Params<2>{});
@@ -1005,4 +1490,24 @@ extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8
     case 87: return run(Params<87>{});
     default: return DLB_E_LEVEL;
   }
+}
+
+extern "C" int dlb_dbg_sign_attempt(dlb_ctx* c, int level, size_t n, const uint8_t* sks,
+                                    size_t sk_stride, const uint8_t* mus, const uint8_t* rho_primes,
+                                    const uint32_t* kappas, uint8_t* accepted, uint8_t* c_tilde,
+                                    int32_t* z, int32_t* hints) {
+  return dbg_sign_attempt(c, level, n, sks, sk_stride, mus, rho_primes, kappas, nullptr, accepted, nullptr,
+                          c_tilde, z, hints);
+}
+
+extern "C" int dlb_dbg_sign_attempt_bounded(dlb_ctx* c, int level, size_t n, const uint8_t* sks,
+                                            size_t sk_stride, const uint8_t* mus,
+                                            const uint8_t* rho_primes, const uint32_t* kappas,
+                                            int32_t z_bound, int32_t r0_bound, int32_t vt_bound,
+                                            uint8_t* accepted, uint8_t* stage, uint8_t* c_tilde,
+                                            int32_t* z, int32_t* hints) {
+  if (!stage) return DLB_E_ARG;
+  const int32_t bounds[3] = {z_bound, r0_bound, vt_bound};
+  return dbg_sign_attempt(c, level, n, sks, sk_stride, mus, rho_primes, kappas, bounds, accepted, stage,
+                          c_tilde, z, hints);
 }

@@ -32,7 +32,7 @@ __global__ void k_verify_final(unsigned n, const uint64_t* __restrict__ mu,
   flags[t] = (eq && pre_ok[t]) ? 1 : 0;
 }
 
-constexpr size_t kVerifyChunk = 65536;  // measured: 16k -> 64k tasks per chunk = +7..15 %
+// device chunk: dlb_ctx::knob_chunk = 65536 tasks -- measured: 16k -> 64k tasks per chunk = +7..15 %
 
 // Chunks alternate between two compute lanes (streams forked from / joined to the
 // caller's stream): the sponge-per-task kernels of one chunk (tr, mu, challenge, final
@@ -58,8 +58,7 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
   if (!keyed) n_keys = 1;
   size_t chunk = (n + 1) / 2;
   if (chunk < 2048) chunk = 2048;
-  size_t cmax = kVerifyChunk;
-  if (const char* e = getenv("DLB_CHUNK")) cmax = (size_t)atol(e);  // experiments
+  const size_t cmax = c->knob_chunk;  // DLB_CHUNK at dlb_create for experiments
   if (chunk > cmax) chunk = cmax;
   if (chunk > n) chunk = n;
   const size_t keys_cap = shared_key ? n_keys : chunk;
@@ -83,7 +82,7 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
     DLB_TRY(dalloc(c, nm[b][4], chunk * S::W1_ALL, &w1buf[b]));
     DLB_TRY(dalloc(c, nm[b][5], chunk, &pre_ok[b]));
   }
-  if (const int co = pipeline_carveout(); co >= 0) {
+  if (const int co = pipeline_carveout(c); co >= 0) {
     prefer_carveout(k_expand_a<P, HW>, co);
     prefer_carveout(k_hash_tr, co);
     prefer_carveout(k_hash_mu<Hashing<P>::MLDSA>, co);

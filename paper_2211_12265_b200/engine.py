@@ -89,6 +89,16 @@ def load_library():
         "dlb_dbg_ntt": (C.c_int, [vp, sz, _i32p, C.c_int]),
         "dlb_dbg_sign_attempt": (C.c_int, [vp, C.c_int, sz, _u8p, sz, _u8p, _u8p, _u32p, _u8p,
                                            _u8p, _i32p, _i32p]),
+        "dlb_dbg_sign_attempt_bounded": (C.c_int, [vp, C.c_int, sz, _u8p, sz, _u8p, _u8p, _u32p, C.c_int32,
+                                                   C.c_int32, C.c_int32, _u8p, _u8p, _u8p, _i32p, _i32p]),
+        "dlb_dbg_set_max_attempt": (C.c_int, [vp, C.c_uint]),
+        "dlb_set_assignment_log": (C.c_int, [vp, sz]),
+        "dlb_get_assignment_log": (C.c_longlong, [vp, vp, sz]),
+        "dlb_sign_submit": (C.c_int, [vp, C.c_int, sz, vp, sz, sz, vp, vp, vp, vp, sz, C.c_int, vp, vp, vp,
+                                      C.POINTER(C.c_uint64)]),
+        "dlb_sign_submit_dev": (C.c_int, [vp, C.c_int, sz, vp, sz, sz, vp, vp, vp, vp, sz, C.c_int, vp, vp, vp,
+                                          C.POINTER(C.c_uint64)]),
+        "dlb_sign_wait": (C.c_int, [vp, C.c_uint64, C.POINTER(SignStats)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)  # AttributeError here = header/library mismatch
@@ -104,6 +114,8 @@ EXPORTED_SYMBOLS = [
     "dlb_keygen_batch_dev", "dlb_sign_batch_dev", "dlb_verify_batch_dev", "dlb_dbg_keccak_f1600",
     "dlb_dbg_shake256", "dlb_dbg_expand_a", "dlb_dbg_expand_s", "dlb_dbg_expand_mask",
     "dlb_dbg_sample_in_ball", "dlb_dbg_rounding", "dlb_dbg_ntt", "dlb_dbg_sign_attempt",
+    "dlb_dbg_sign_attempt_bounded", "dlb_dbg_set_max_attempt", "dlb_set_assignment_log",
+    "dlb_get_assignment_log", "dlb_sign_submit", "dlb_sign_submit_dev", "dlb_sign_wait",
 ]
 
 
@@ -189,6 +201,26 @@ class Engine:
             raise EngineError("dlb_get_trace failed: %d" % total)
         return buf[:min(total, len(buf)), :7].copy(), int(total)
 
+    ASSIGNMENT_FIELDS = ("slot", "task", "attempt", "kappa")
+
+    def set_assignment_log(self, cap):
+        """Log of executed (task, attempt) pairs of the following synchronous sign calls
+        (BatchConfig::assignment_hook, batch.hpp:28); 0 = off."""
+        self._chk(self.lib.dlb_set_assignment_log(self.ctx, cap), "dlb_set_assignment_log")
+        self._alog_cap = cap
+
+    def get_assignment_log(self):
+        """(records as an (m, 4) uint32 array in ASSIGNMENT_FIELDS order, records produced)."""
+        buf = np.zeros((max(1, getattr(self, "_alog_cap", 0)), 4), np.uint32)
+        total = self.lib.dlb_get_assignment_log(self.ctx, buf.ctypes.data_as(C.c_void_p), len(buf))
+        if total < 0:
+            raise EngineError("dlb_get_assignment_log failed: %d" % total)
+        return buf[:min(total, len(buf))].copy(), int(total)
+
+    def dbg_set_max_attempt(self, max_attempt):
+        """Stage tests: tasks whose attempts 0..max_attempt all fail are reported failed; 0 = scheme limit."""
+        self._chk(self.lib.dlb_dbg_set_max_attempt(self.ctx, max_attempt), "dlb_dbg_set_max_attempt")
+
     def set_mldsa_context(self, context=b""):
         """FIPS 204 context string (<= 255 bytes) for levels 44 / 65 / 87; sticky, default empty."""
         buf = np.frombuffer(bytes(context), np.uint8)
@@ -248,6 +280,52 @@ class Engine:
         if return_info:
             return sigs, att, failed, {f[0]: getattr(st, f[0]) for f in SignStats._fields_}
         return sigs
+
+    # ---- batches in flight (tools/dilithium_cli.cpp:309-345)
+    def sign_submit(self, level, sks, messages, rho_prime=None, psi=0, speculate=True, key_idx=None,
+                    out=None):
+        """Enqueues a batch and returns a handle at once; sign_wait(handle) returns what
+        batch_sign(..., return_info=True) would.  `out`: optional (n, sig_bytes) uint8 array
+        for the signatures (e.g. pinned memory); inputs are kept alive by the handle."""
+        k, l, pkb, skb, sgb = LEVELS[level]
+        sk, skp = _u8(sks)
+        flat, off = _msgs(messages)
+        n = len(off) - 1
+        stride = 0 if sk.ndim == 1 else skb
+        kidx = None
+        n_keys = 0
+        if key_idx is not None:
+            kidx = np.ascontiguousarray(key_idx, np.uint32)
+            n_keys = sk.size // skb
+            stride = skb
+        sigs = out if out is not None else np.zeros((n, sgb), np.uint8)
+        att = np.zeros(n, np.uint32)
+        failed = np.zeros(n, np.uint8)
+        rpa = None
+        if rho_prime is not None:
+            rpa = np.ascontiguousarray(rho_prime, np.uint8)
+            assert rpa.size == n * 64
+        ticket = C.c_uint64(0)
+        vp = C.c_void_p
+        rc = self.lib.dlb_sign_submit(self.ctx, level, n_keys, vp(sk.ctypes.data), stride, n,
+                                      vp(kidx.ctypes.data) if kidx is not None else None,
+                                      vp(flat.ctypes.data), vp(off.ctypes.data),
+                                      vp(rpa.ctypes.data) if rpa is not None else None, psi,
+                                      1 if speculate else 0, vp(sigs.ctypes.data), vp(att.ctypes.data),
+                                      vp(failed.ctypes.data), C.byref(ticket))
+        self._chk(rc, "dlb_sign_submit")
+        return {"ticket": ticket.value, "sigs": sigs, "att": att, "failed": failed,
+                "keep": (sk, flat, off, kidx, rpa)}
+
+    def sign_wait(self, handle):
+        st = SignStats()
+        rc = self.lib.dlb_sign_wait(self.ctx, handle["ticket"], C.byref(st))
+        handle["keep"] = None
+        if rc == -3:
+            raise ValueError("sign: malformed secret key")
+        self._chk(rc, "dlb_sign_wait")
+        return (handle["sigs"], handle["att"], handle["failed"],
+                {f[0]: getattr(st, f[0]) for f in SignStats._fields_})
 
     # ---- batch.hpp:148-156
     def batch_verify(self, level, pks, messages, sigs, key_idx=None):
@@ -368,3 +446,26 @@ class Engine:
                                                 ct.ctypes.data_as(_u8p), z.ctypes.data_as(_i32p),
                                                 h.ctypes.data_as(_i32p)), "sign_attempt")
         return acc, ct, z, h
+
+    REJECT_STAGES = ("ZNorm", "R0Norm", "VtNorm", "HintWeight")  # scheme.hpp:34
+
+    def dbg_sign_attempt_bounded(self, level, sks, mus, rho_primes, kappas, z_bound, r0_bound, vt_bound):
+        """detail::sign_attempt_bounded (scheme.hpp:133-219): (accepted, stage, c_tilde, z, hints);
+        stage 255 = accepted, else an index into REJECT_STAGES."""
+        k, l, pkb, skb, sgb = LEVELS[level]
+        sk, skp = _u8(sks)
+        mu, mup = _u8(mus)
+        rp, rpp = _u8(rho_primes)
+        kap = np.ascontiguousarray(kappas, np.uint32)
+        n = kap.size
+        stride = 0 if sk.ndim == 1 else skb
+        acc = np.zeros(n, np.uint8)
+        stage = np.zeros(n, np.uint8)
+        ct = np.zeros((n, {65: 48, 87: 64}.get(level, 32)), np.uint8)
+        z = np.zeros((n, l, 256), np.int32)
+        h = np.zeros((n, k, 256), np.int32)
+        self._chk(self.lib.dlb_dbg_sign_attempt_bounded(
+            self.ctx, level, n, skp, stride, mup, rpp, kap.ctypes.data_as(_u32p), z_bound, r0_bound,
+            vt_bound, acc.ctypes.data_as(_u8p), stage.ctypes.data_as(_u8p), ct.ctypes.data_as(_u8p),
+            z.ctypes.data_as(_i32p), h.ctypes.data_as(_i32p)), "sign_attempt_bounded")
+        return acc, stage, ct, z, h
