@@ -112,6 +112,16 @@ long long dlb_get_assignment_log(dlb_ctx* ctx, dlb_assignment* out, size_t max_r
  * context until changed; ignored by the round-3 levels. */
 int dlb_set_mldsa_context(dlb_ctx* ctx, const uint8_t* context_string, size_t len);
 
+/* Several GPUs of one box: the transport limit is host memory and PCIe, so the host thread that
+ * drives a GPU -- and the pinned staging it allocates -- should live on that GPU's NUMA node.
+ * dlb_bind_thread_to_device pins the CALLING thread to the CPUs local to CUDA device `device`
+ * (/sys/bus/pci/devices/<id>/local_cpulist); memory it allocates afterwards (dlb_host_alloc,
+ * dlb_create's staging) is then node-local by first touch.  Returns 0 when the affinity was
+ * set, 1 when the box exposes no locality information (nothing changed), < 0 on errors.
+ * dlb_device_numa_node: the node id, or -1 when unknown. */
+int dlb_bind_thread_to_device(int device);
+int dlb_device_numa_node(int device);
+
 /* Pinned host memory for callers that want zero-staging transfers (the engine copies
  * straight from/to these buffers with cudaMemcpyAsync). */
 void* dlb_host_alloc(size_t bytes);

@@ -1,12 +1,18 @@
 // api.hpp -- C++ host shim over the C ABI (dilithium_b200.h) with the reference's API
 // surface for the batched hot path, so call sites written against
-// proj/include/dilithium/{scheme,batch}.hpp compile after switching the namespace:
+// proj/include/dilithium/{params,scheme,scheduler,batch}.hpp compile after switching the namespace:
 //
-//   dilithium::keygen<P>(zeta)                 scheme.hpp:68-69    -> dilithium::b200::keygen<P>
+//   dilithium::Params, kDilithium2/3/5,        params.hpp:17-55    -> dilithium::b200::Params, ...
+//     ParamsTag, with_params                   params.hpp:84-106   -> b200::ParamsTag, b200::with_params
+//   dilithium::keygen<P>(zeta)                 scheme.hpp:68-69    -> b200::keygen<P>
 //   dilithium::make_precomp<P>(sk)             scheme.hpp:106-107  -> b200::make_precomp<P>
+//   dilithium::message_digest<P>, deterministic_rho_prime<P>   :240-248
+//   dilithium::sign_attempt<P>, detail::sign_attempt_bounded<P>, AttemptResult, RejectStage
+//                                              scheme.hpp:34-43,133-230
 //   dilithium::sign_with_precomp<P>(pre,msg,rho')   :253-255       -> b200::sign_with_precomp<P>
 //   dilithium::sign<P>(sk,msg)                 scheme.hpp:268-269  -> b200::sign<P>
 //   dilithium::verify<P>(pk,msg,sig)           scheme.hpp:277-279  -> b200::verify<P>
+//   dilithium::Assignment, RoundTrace          scheduler.hpp:14-28
 //   dilithium::batch_sign<P>(jobs,cfg,stats)   batch.hpp:53-55     -> b200::batch_sign<P>
 //   dilithium::batch_verify<P>(jobs,workers)   batch.hpp:148-149   -> b200::batch_verify<P>
 //   dilithium::batch_keygen<P>(zetas,workers)  batch.hpp:159-161   -> b200::batch_keygen<P>
@@ -16,7 +22,13 @@
 // verify never throws and rejects wrong lengths (scheme.hpp:280-283), batch_sign reports
 // per-task failures in BatchStats::failed_tasks (batch.hpp:128-131).  `workers` is
 // accepted and ignored (the GPU grid replaces the worker pool); cfg.psi = resident
-// attempt slots; cfg.speculate honoured.  Header-only, C++20, links libdilithium_b200.so.
+// attempt slots; cfg.speculate honoured; cfg.trace / cfg.assignment_hook are replayed from
+// device logs after the batch.  Header-only, C++20, links libdilithium_b200.so.
+//
+// Transfers: every batch call stages through pinned buffers the Engine owns (grown on demand,
+// reused across calls).  batch_sign submits the batch as a few tickets in flight
+// (dlb_sign_submit) whose signatures the device writes straight into the pinned staging; each
+// finished part is appended to the result vector while the later parts are still signing.
 #pragma once
 #include <algorithm>
 #include <array>
@@ -38,29 +50,47 @@
 
 namespace dilithium::b200 {
 
+inline constexpr int32_t kQ = 8380417;
+inline constexpr size_t kN = 256;
+inline constexpr int kD = 13;
 inline constexpr size_t kSeedBytes = 32;
 inline constexpr size_t kCrhBytes = 64;
 
+// params.hpp:17-51 plus the two sizes that differ in the FIPS 204 sets
 struct Params {
   int level;
   size_t k, l;
-  int eta;
-  size_t eta_bits, z_bits, omega;
+  int32_t eta, tau, beta, gamma1, gamma2;
+  size_t omega, eta_bits, z_bits, w1_bits;
   size_t tr_bytes = 32, ctilde_bytes = 32;  // 64 and lambda/4 for the FIPS 204 sets
-  constexpr size_t pk_bytes() const { return 32 + k * 320; }
-  constexpr size_t sk_bytes() const { return 64 + tr_bytes + (k + l) * 32 * eta_bits + k * 416; }
-  constexpr size_t sig_bytes() const { return ctilde_bytes + l * 32 * z_bits + omega + k; }
+
+  constexpr int32_t alpha() const { return 2 * gamma2; }
+  constexpr int32_t decomp_m() const { return (kQ - 1) / alpha(); }
+  constexpr size_t poly_eta_bytes() const { return kN * eta_bits / 8; }
+  constexpr size_t poly_z_bytes() const { return kN * z_bits / 8; }
+  constexpr size_t poly_w1_bytes() const { return kN * w1_bits / 8; }
+  static constexpr size_t poly_t1_bytes() { return kN * 10 / 8; }
+  static constexpr size_t poly_t0_bytes() { return kN * kD / 8; }
+  constexpr size_t pk_bytes() const { return kSeedBytes + k * poly_t1_bytes(); }
+  constexpr size_t sk_bytes() const {
+    return 2 * kSeedBytes + tr_bytes + (k + l) * poly_eta_bytes() + k * poly_t0_bytes();
+  }
+  constexpr size_t hint_bytes() const { return omega + k; }
+  constexpr size_t sig_bytes() const { return ctilde_bytes + l * poly_z_bytes() + hint_bytes(); }
   friend constexpr bool operator==(const Params&, const Params&) = default;
 };
 
-inline constexpr Params kDilithium2{2, 4, 4, 2, 3, 18, 80};
-inline constexpr Params kDilithium3{3, 6, 5, 4, 4, 20, 55};
-inline constexpr Params kDilithium5{5, 8, 7, 2, 3, 20, 75};
+inline constexpr Params kDilithium2{2, 4, 4, 2, 39, 78, 1 << 17, (kQ - 1) / 88, 80, 3, 18, 6};
+inline constexpr Params kDilithium3{3, 6, 5, 4, 49, 196, 1 << 19, (kQ - 1) / 32, 55, 4, 20, 4};
+inline constexpr Params kDilithium5{5, 8, 7, 2, 60, 120, 1 << 19, (kQ - 1) / 32, 75, 3, 20, 4};
 // FIPS 204 parameter sets (not in the reference, which declares them a non-goal): the same
 // engine with the standard's hashing conventions; deterministic signing, empty context.
-inline constexpr Params kMLDSA44{44, 4, 4, 2, 3, 18, 80, 64, 32};
-inline constexpr Params kMLDSA65{65, 6, 5, 4, 4, 20, 55, 64, 48};
-inline constexpr Params kMLDSA87{87, 8, 7, 2, 3, 20, 75, 64, 64};
+inline constexpr Params kMLDSA44{44, 4, 4, 2, 39, 78, 1 << 17, (kQ - 1) / 88, 80, 3, 18, 6, 64, 32};
+inline constexpr Params kMLDSA65{65, 6, 5, 4, 49, 196, 1 << 19, (kQ - 1) / 32, 55, 4, 20, 4, 64, 48};
+inline constexpr Params kMLDSA87{87, 8, 7, 2, 60, 120, 1 << 19, (kQ - 1) / 32, 75, 3, 20, 4, 64, 64};
+static_assert(kDilithium2.gamma2 == 95232 && kDilithium2.decomp_m() == 44);
+static_assert(kDilithium3.gamma2 == 261888 && kDilithium3.decomp_m() == 16);
+static_assert(kDilithium2.beta == kDilithium2.tau * kDilithium2.eta && kDilithium5.beta == 120);
 static_assert(kMLDSA44.sk_bytes() == 2560 && kMLDSA44.sig_bytes() == 2420);
 static_assert(kMLDSA65.sk_bytes() == 4032 && kMLDSA65.sig_bytes() == 3309);
 static_assert(kMLDSA87.sk_bytes() == 4896 && kMLDSA87.sig_bytes() == 4627);
@@ -68,13 +98,70 @@ static_assert(kDilithium2.pk_bytes() == 1312 && kDilithium2.sk_bytes() == 2528 &
 static_assert(kDilithium3.pk_bytes() == 1952 && kDilithium3.sk_bytes() == 4000 && kDilithium3.sig_bytes() == 3293);
 static_assert(kDilithium5.pk_bytes() == 2592 && kDilithium5.sk_bytes() == 4864 && kDilithium5.sig_bytes() == 4595);
 
+// params.hpp:84-106
+template <Params P>
+struct ParamsTag {
+  static constexpr Params value = P;
+};
+
+// Dispatches a runtime level to the matching compile-time parameter set; fn receives a
+// ParamsTag; false for unsupported levels.  (44 / 65 / 87 select the FIPS 204 sets.)
+template <class Fn>
+bool with_params(int level, Fn&& fn) {
+  switch (level) {
+    case 2: fn(ParamsTag<kDilithium2>{}); return true;
+    case 3: fn(ParamsTag<kDilithium3>{}); return true;
+    case 5: fn(ParamsTag<kDilithium5>{}); return true;
+    case 44: fn(ParamsTag<kMLDSA44>{}); return true;
+    case 65: fn(ParamsTag<kMLDSA65>{}); return true;
+    case 87: fn(ParamsTag<kMLDSA87>{}); return true;
+    default: return false;
+  }
+}
+
 template <Params P> using PkBytes = std::array<uint8_t, P.pk_bytes()>;
 template <Params P> using SkBytes = std::array<uint8_t, P.sk_bytes()>;
 template <Params P> using SigBytes = std::array<uint8_t, P.sig_bytes()>;
 using SeedArray = std::array<uint8_t, kSeedBytes>;
 using CrhArray = std::array<uint8_t, kCrhBytes>;
 
-// One engine per GPU, created on first use (device 0) or explicitly.
+inline void check(int rc, const char* what) {
+  if (rc != 0) throw std::runtime_error(std::string(what) + " failed: status " + std::to_string(rc));
+}
+
+// Pinned host buffer owned by an Engine, grown geometrically, reused across calls.
+class PinnedBuf {
+ public:
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() { release(); }
+  uint8_t* get(size_t bytes) {
+    if (bytes > cap_) {
+      release();
+      const size_t want = bytes + bytes / 4 + 4096;
+      p_ = static_cast<uint8_t*>(dlb_host_alloc(want));
+      if (!p_) throw std::bad_alloc();
+      cap_ = want;
+    }
+    return p_;
+  }
+
+ private:
+  void release() {
+    if (p_) {
+      std::memset(p_, 0, cap_);  // may have held keys
+      dlb_host_free(p_);
+    }
+    p_ = nullptr;
+    cap_ = 0;
+  }
+  uint8_t* p_ = nullptr;
+  size_t cap_ = 0;
+};
+
+// One engine per GPU, created on first use (device 0) or explicitly.  One host thread drives
+// an engine at a time.
 class Engine {
  public:
   explicit Engine(int device = 0) {
@@ -87,26 +174,23 @@ class Engine {
   dlb_ctx* ctx() const { return ctx_; }
   // FIPS 204 context string (<= 255 bytes) for the ML-DSA parameter sets; sticky, default empty
   void set_mldsa_context(std::span<const uint8_t> context) {
-    check_rc(dlb_set_mldsa_context(ctx_, context.data(), context.size()));
+    const int rc = dlb_set_mldsa_context(ctx_, context.data(), context.size());
+    if (rc != 0) throw std::invalid_argument("dlb_set_mldsa_context: status " + std::to_string(rc));
   }
   static Engine& instance() {
     static Engine e(0);
     return e;
   }
+  // pinned staging, by role
+  PinnedBuf in_a, in_b, in_c, in_d, out_a, out_b, out_c;
 
  private:
-  static void check_rc(int rc) {
-    if (rc != 0) throw std::invalid_argument("dlb_set_mldsa_context: status " + std::to_string(rc));
-  }
   dlb_ctx* ctx_ = nullptr;
 };
 
-inline void check(int rc, const char* what) {
-  if (rc != 0) throw std::runtime_error(std::string(what) + " failed: status " + std::to_string(rc));
-}
-
-// Per-key signing state.  On the GPU the transformed key lives in device memory for
-// the duration of a batch call; the host object keeps the validated packed key.
+// Per-key signing state.  On the GPU the transformed key lives in a device-side cache keyed
+// by the packed key (built on first use, kept across calls); the host object keeps the
+// validated packed key.
 template <Params P>
 struct SignPrecomp {
   SkBytes<P> sk{};
@@ -140,6 +224,11 @@ std::optional<SignPrecomp<P>> make_precomp(std::span<const uint8_t> sk_bytes) {
   return pre;
 }
 
+// scheduler.hpp:14-19.  `slot` is the device's global attempt slot (CTA * 128 + slot).
+struct Assignment {
+  uint32_t slot, task, attempt, kappa;
+};
+
 // scheduler.hpp:21-28.  The device scheduler runs one round loop per CTA, so a record is one
 // round of one CTA (`stream`); the remaining fields are RoundTrace's, restricted to that CTA.
 struct RoundTrace {
@@ -152,8 +241,10 @@ struct BatchConfig {  // batch.hpp:23-29
   size_t psi = 0;
   size_t workers = 1;
   bool speculate = true;
-  std::function<void(const RoundTrace&)> trace;  // called once per logged round after the batch
-  size_t trace_capacity = 1 << 20;               // records kept per call when `trace` is set
+  std::function<void(const RoundTrace&)> trace;            // called once per logged round after the batch
+  std::function<void(const Assignment&)> assignment_hook;  // per executed attempt, after the batch
+  size_t trace_capacity = 1 << 20;                         // records kept per call when `trace` is set
+  size_t assignment_capacity = 0;                          // 0 = 64 records per task
 };
 
 struct BatchStats {  // batch.hpp:31-38
@@ -178,84 +269,249 @@ struct SignOutput {
   uint32_t attempts;
 };
 
+// coefficient vectors of an attempt, shaped like the reference's PolyVec (`v.p[i].c[m]`)
+struct CoeffPoly {
+  std::array<int32_t, kN> c{};
+  friend bool operator==(const CoeffPoly&, const CoeffPoly&) = default;
+};
+template <size_t Dim>
+struct CoeffVec {
+  std::array<CoeffPoly, Dim> p{};
+  friend bool operator==(const CoeffVec&, const CoeffVec&) = default;
+};
+
+enum class RejectStage { ZNorm, R0Norm, VtNorm, HintWeight };  // scheme.hpp:34
+
+template <Params P>
+struct AttemptResult {  // scheme.hpp:36-43
+  bool accepted = false;
+  RejectStage stage = RejectStage::ZNorm;  // meaningful only when rejected
+  std::array<uint8_t, P.ctilde_bytes> c_tilde{};
+  CoeffVec<P.l> z{};      // centered
+  CoeffVec<P.k> hints{};  // 0/1 coefficients
+};
+
 namespace detail {
+
+// messages of jobs[lo, hi) back to back in `flat` (pinned), offsets relative to the part
 template <class Jobs>
-void flatten_messages(const Jobs& jobs, std::vector<uint8_t>& flat, std::vector<uint64_t>& off) {
-  off.assign(jobs.size() + 1, 0);
-  for (size_t i = 0; i < jobs.size(); ++i) off[i + 1] = off[i] + jobs[i].message.size();
-  flat.resize(off.back() + 8);
-  for (size_t i = 0; i < jobs.size(); ++i)
-    if (!jobs[i].message.empty())
-      std::memcpy(flat.data() + off[i], jobs[i].message.data(), jobs[i].message.size());
+void flatten_messages(const Jobs& jobs, size_t lo, size_t hi, uint8_t* flat, uint64_t* off) {
+  off[0] = 0;
+  for (size_t i = lo; i < hi; ++i) {
+    const auto& m = jobs[i].message;
+    if (!m.empty()) std::memcpy(flat + off[i - lo], m.data(), m.size());
+    off[i - lo + 1] = off[i - lo] + m.size();
+  }
 }
+
+template <class Jobs>
+size_t message_bytes(const Jobs& jobs, size_t lo, size_t hi) {
+  size_t s = 0;
+  for (size_t i = lo; i < hi; ++i) s += jobs[i].message.size();
+  return s;
+}
+
+// scheme.hpp:133-219 through the device's single-round entry; bounds == nullptr = the scheme's
+template <Params P>
+AttemptResult<P> sign_attempt_impl(const SignPrecomp<P>& pre, std::span<const uint8_t, kCrhBytes> mu,
+                                   std::span<const uint8_t, kCrhBytes> rho_prime, uint32_t kappa,
+                                   const int32_t* bounds, Engine& eng) {
+  AttemptResult<P> res;
+  std::vector<int32_t> z(P.l * kN), h(P.k * kN);
+  uint8_t accepted = 0, stage = 255;
+  const int32_t b[3] = {bounds ? bounds[0] : P.gamma1 - P.beta, bounds ? bounds[1] : P.gamma2 - P.beta,
+                        bounds ? bounds[2] : P.gamma2};
+  check(dlb_dbg_sign_attempt_bounded(eng.ctx(), P.level, 1, pre.sk.data(), 0, mu.data(), rho_prime.data(),
+                                     &kappa, b[0], b[1], b[2], &accepted, &stage, res.c_tilde.data(), z.data(),
+                                     h.data()),
+        "dlb_dbg_sign_attempt_bounded");
+  res.accepted = accepted != 0;
+  if (!res.accepted) res.stage = static_cast<RejectStage>(stage < 4 ? stage : 0);
+  if (res.accepted) {
+    for (size_t j = 0; j < P.l; ++j) std::memcpy(res.z.p[j].c.data(), z.data() + j * kN, kN * 4);
+    for (size_t i = 0; i < P.k; ++i) std::memcpy(res.hints.p[i].c.data(), h.data() + i * kN, kN * 4);
+  }
+  return res;
+}
+
+// One rejection-loop iteration with injectable norm bounds (scheme.hpp:133-138; tests force
+// individual reject stages through them)
+template <Params P>
+AttemptResult<P> sign_attempt_bounded(const SignPrecomp<P>& pre, std::span<const uint8_t, kCrhBytes> mu,
+                                      std::span<const uint8_t, kCrhBytes> rho_prime, uint32_t kappa,
+                                      int32_t z_bound, int32_t r0_bound, int32_t vt_bound,
+                                      Engine& eng = Engine::instance()) {
+  const int32_t b[3] = {z_bound, r0_bound, vt_bound};
+  return sign_attempt_impl<P>(pre, mu, rho_prime, kappa, b, eng);
+}
+
 }  // namespace detail
 
-// batch.hpp:159-166
+// scheme.hpp:225-230
+template <Params P>
+AttemptResult<P> sign_attempt(const SignPrecomp<P>& pre, std::span<const uint8_t, kCrhBytes> mu,
+                              std::span<const uint8_t, kCrhBytes> rho_prime, uint32_t kappa,
+                              Engine& eng = Engine::instance()) {
+  return detail::sign_attempt_impl<P>(pre, mu, rho_prime, kappa, nullptr, eng);
+}
+
+// scheme.hpp:240-248: mu = H(tr || M), rho' = H(K || mu), 64 bytes each, hashed on the device
+template <Params P>
+CrhArray message_digest(const SignPrecomp<P>& pre, std::span<const uint8_t> msg, Engine& eng = Engine::instance()) {
+  static_assert(P.tr_bytes == 32, "round-3 sets only: FIPS 204 hashes a context prefix as well");
+  std::vector<uint8_t> buf(pre.tr.size() + msg.size() + 8);
+  std::memcpy(buf.data(), pre.tr.data(), pre.tr.size());
+  if (!msg.empty()) std::memcpy(buf.data() + pre.tr.size(), msg.data(), msg.size());
+  const uint64_t off[2] = {0, pre.tr.size() + msg.size()};
+  CrhArray mu;
+  check(dlb_dbg_shake256(eng.ctx(), 1, buf.data(), off, mu.data()), "dlb_dbg_shake256");
+  return mu;
+}
+
+template <Params P>
+CrhArray deterministic_rho_prime(const SignPrecomp<P>& pre, const CrhArray& mu, Engine& eng = Engine::instance()) {
+  static_assert(P.tr_bytes == 32, "round-3 sets only");
+  uint8_t buf[kSeedBytes + kCrhBytes + 8];
+  std::memcpy(buf, pre.key.data(), kSeedBytes);
+  std::memcpy(buf + kSeedBytes, mu.data(), kCrhBytes);
+  const uint64_t off[2] = {0, kSeedBytes + kCrhBytes};
+  CrhArray rp;
+  check(dlb_dbg_shake256(eng.ctx(), 1, buf, off, rp.data()), "dlb_dbg_shake256");
+  return rp;
+}
+
+// batch.hpp:159-166.  The batch is cut into parts; while the device generates part i + 1 a
+// helper thread moves part i from the pinned staging into the result vector.
 template <Params P>
 std::vector<std::pair<PkBytes<P>, SkBytes<P>>> batch_keygen(std::span<const SeedArray> zetas,
                                                             size_t /*workers*/ = 1,
                                                             Engine& eng = Engine::instance()) {
+  using KeyPair = std::pair<PkBytes<P>, SkBytes<P>>;
   const size_t n = zetas.size();
-  std::vector<std::pair<PkBytes<P>, SkBytes<P>>> out(n);
+  std::vector<KeyPair> out;
   if (n == 0) return out;
-  std::vector<uint8_t> pks(n * P.pk_bytes()), sks(n * P.sk_bytes());
-  check(dlb_keygen_batch(eng.ctx(), P.level, n, zetas.data()->data(), pks.data(), sks.data()),
-        "dlb_keygen_batch");
-  for (size_t i = 0; i < n; ++i) {
-    std::memcpy(out[i].first.data(), pks.data() + i * P.pk_bytes(), P.pk_bytes());
-    std::memcpy(out[i].second.data(), sks.data() + i * P.sk_bytes(), P.sk_bytes());
+  out.reserve(n);
+  constexpr size_t kPart = 16384;
+  const size_t part = std::min(n, kPart);
+  uint8_t* pk_stage[2] = {eng.out_a.get(2 * part * P.pk_bytes()), nullptr};
+  uint8_t* sk_stage[2] = {eng.out_b.get(2 * part * P.sk_bytes()), nullptr};
+  pk_stage[1] = pk_stage[0] + part * P.pk_bytes();
+  sk_stage[1] = sk_stage[0] + part * P.sk_bytes();
+  uint8_t* zin = eng.in_a.get(n * kSeedBytes);
+  std::memcpy(zin, zetas.data()->data(), n * kSeedBytes);
+  std::thread mover;
+  auto move_part = [&out](const uint8_t* pks, const uint8_t* sks, size_t cnt) {
+    for (size_t i = 0; i < cnt; ++i) {
+      KeyPair& kp = out.emplace_back();  // capacity reserved: no reallocation
+      std::memcpy(kp.first.data(), pks + i * P.pk_bytes(), P.pk_bytes());
+      std::memcpy(kp.second.data(), sks + i * P.sk_bytes(), P.sk_bytes());
+    }
+  };
+  size_t pi = 0;
+  for (size_t lo = 0; lo < n; lo += part, ++pi) {
+    const size_t cnt = std::min(part, n - lo);
+    const int b = static_cast<int>(pi & 1);
+    const int rc = dlb_keygen_batch(eng.ctx(), P.level, cnt, zin + lo * kSeedBytes, pk_stage[b], sk_stage[b]);
+    if (mover.joinable()) mover.join();  // part pi - 1 is in place; its buffer (b ^ 1) is free again
+    check(rc, "dlb_keygen_batch");
+    mover = std::thread(move_part, pk_stage[b], sk_stage[b], cnt);
   }
+  if (mover.joinable()) mover.join();
   return out;
 }
 
-// batch.hpp:53-137
+// batch.hpp:53-137.  rho_prime_override: nullptr (deterministic signing), or ONE rho' used
+// for every task (the reference's sign_with_precomp argument), or -- rho_prime_per_task --
+// one rho' per task.
 template <Params P>
 std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const BatchConfig& cfg = {},
                                     BatchStats* stats = nullptr, Engine& eng = Engine::instance(),
                                     const CrhArray* rho_prime_override = nullptr,
-                                    std::vector<uint32_t>* attempts_out = nullptr) {
+                                    std::vector<uint32_t>* attempts_out = nullptr,
+                                    std::span<const CrhArray> rho_prime_per_task = {}) {
   const size_t n = jobs.size();
-  std::vector<SigBytes<P>> out(n);
+  std::vector<SigBytes<P>> out;
   if (n == 0) return out;
+  if (!rho_prime_per_task.empty() && rho_prime_per_task.size() != n)
+    throw std::invalid_argument("batch_sign: one rho' per task expected");
+  static_assert(sizeof(SigBytes<P>) == P.sig_bytes());
   // SignJob.key is a non-owning pointer and jobs may share keys (batch.hpp:41-44): collect the
   // distinct keys once so the device precomputes each of them once, not once per task
   std::unordered_map<const SignPrecomp<P>*, uint32_t> key_of;
   std::vector<const SignPrecomp<P>*> keys;
   std::vector<uint32_t> key_idx(n);
   for (size_t i = 0; i < n; ++i) {
+    if (!jobs[i].key) throw std::invalid_argument("batch_sign: job without a key");
     auto [it, fresh] = key_of.try_emplace(jobs[i].key, static_cast<uint32_t>(keys.size()));
     if (fresh) keys.push_back(jobs[i].key);
     key_idx[i] = it->second;
   }
   const bool shared = keys.size() == 1;
-  std::vector<uint8_t> sks;
-  const uint8_t* skp = jobs[0].key->sk.data();
-  if (!shared) {
-    sks.resize(keys.size() * P.sk_bytes());
-    for (size_t k = 0; k < keys.size(); ++k)
-      std::memcpy(sks.data() + k * P.sk_bytes(), keys[k]->sk.data(), P.sk_bytes());
-    skp = sks.data();
+  uint8_t* skp = eng.in_a.get(keys.size() * P.sk_bytes());
+  for (size_t k = 0; k < keys.size(); ++k) std::memcpy(skp + k * P.sk_bytes(), keys[k]->sk.data(), P.sk_bytes());
+
+  // parts in flight: logs and an explicit psi describe ONE scheduler run, so they force one part
+  const bool logged = static_cast<bool>(cfg.trace) || static_cast<bool>(cfg.assignment_hook);
+  size_t parts = (logged || cfg.psi != 0) ? 1 : std::min<size_t>(8, (n + 4095) / 4096);
+  if (parts < 1) parts = 1;
+  const size_t total_msg = detail::message_bytes(jobs, 0, n);
+  uint8_t* flat = eng.in_b.get(total_msg + 8 * parts + 8);
+  uint64_t* off = reinterpret_cast<uint64_t*>(eng.in_c.get((n + parts + 1) * 8));
+  uint8_t* rp = nullptr;
+  if (rho_prime_override || !rho_prime_per_task.empty()) {
+    rp = eng.in_d.get(n * kCrhBytes);
+    for (size_t i = 0; i < n; ++i)
+      std::memcpy(rp + i * kCrhBytes,
+                  rho_prime_override ? rho_prime_override->data() : rho_prime_per_task[i].data(), kCrhBytes);
   }
-  std::vector<uint8_t> flat;
-  std::vector<uint64_t> off;
-  detail::flatten_messages(jobs, flat, off);
-  std::vector<uint32_t> att(n);
-  std::vector<uint8_t> failed(n);
-  dlb_sign_stats st{};
-  static_assert(sizeof(SigBytes<P>) == P.sig_bytes());
-  const uint8_t* rp = rho_prime_override ? rho_prime_override->data() : nullptr;
+  uint8_t* sig_stage = eng.out_a.get(n * P.sig_bytes() + 8);
+  uint32_t* att = reinterpret_cast<uint32_t*>(eng.out_b.get(n * 4));
+  uint8_t* failed = eng.out_c.get(n);
+
+  const size_t acap = cfg.assignment_capacity ? cfg.assignment_capacity : 64 * n;
   if (cfg.trace) check(dlb_set_trace(eng.ctx(), cfg.trace_capacity), "dlb_set_trace");
-  const int rc =
-      shared ? dlb_sign_batch(eng.ctx(), P.level, n, skp, 0, flat.data(), off.data(), rp, cfg.psi,
-                              cfg.speculate ? 1 : 0, out[0].data(), att.data(), failed.data(), &st)
-             : dlb_sign_batch_keyed(eng.ctx(), P.level, keys.size(), skp, n, key_idx.data(), flat.data(),
-                                    off.data(), rp, cfg.psi, cfg.speculate ? 1 : 0, out[0].data(),
-                                    att.data(), failed.data(), &st);
+  if (cfg.assignment_hook) check(dlb_set_assignment_log(eng.ctx(), acap), "dlb_set_assignment_log");
+
+  struct Part {
+    size_t lo, hi;
+    uint64_t ticket = 0;
+  };
+  std::vector<Part> ps(parts);
+  int rc = 0;
+  size_t flat_pos = 0, off_pos = 0, submitted = 0;
+  for (size_t p = 0; p < parts && rc == 0; ++p) {
+    ps[p].lo = n * p / parts;
+    ps[p].hi = n * (p + 1) / parts;
+    const size_t cnt = ps[p].hi - ps[p].lo;
+    detail::flatten_messages(jobs, ps[p].lo, ps[p].hi, flat + flat_pos, off + off_pos);
+    rc = dlb_sign_submit(eng.ctx(), P.level, shared ? 0 : keys.size(), skp, shared ? 0 : P.sk_bytes(), cnt,
+                         shared ? nullptr : key_idx.data() + ps[p].lo, flat + flat_pos, off + off_pos,
+                         rp ? rp + ps[p].lo * kCrhBytes : nullptr, cfg.psi, cfg.speculate ? 1 : 0,
+                         sig_stage + ps[p].lo * P.sig_bytes(), att + ps[p].lo, failed + ps[p].lo, &ps[p].ticket);
+    flat_pos += (off[off_pos + cnt] + 7) / 8 * 8;
+    off_pos += cnt + 1;
+    if (rc == 0) ++submitted;
+  }
+  out.reserve(n);
+  dlb_sign_stats total{};
+  for (size_t p = 0; p < submitted; ++p) {
+    dlb_sign_stats st{};
+    const int wrc = dlb_sign_wait(eng.ctx(), ps[p].ticket, &st);
+    if (wrc != 0 && rc == 0) rc = wrc;
+    if (rc != 0) continue;  // keep draining the tickets in flight
+    total.rounds += st.rounds;
+    total.attempts += st.attempts;
+    total.speculative += st.speculative;
+    total.idle_slot_rounds += st.idle_slot_rounds;
+    total.accepted_attempt_sum += st.accepted_attempt_sum;
+    const auto* first = reinterpret_cast<const SigBytes<P>*>(sig_stage + ps[p].lo * P.sig_bytes());
+    out.insert(out.end(), first, first + (ps[p].hi - ps[p].lo));  // while later parts still sign
+  }
   if (cfg.trace) {
     std::vector<dlb_round_trace> recs(cfg.trace_capacity);
-    const long long total = rc == 0 ? dlb_get_trace(eng.ctx(), recs.data(), recs.size()) : 0;
+    const long long tot = rc == 0 ? dlb_get_trace(eng.ctx(), recs.data(), recs.size()) : 0;
     dlb_set_trace(eng.ctx(), 0);
-    const size_t have = total < 0 ? 0 : std::min<size_t>(static_cast<size_t>(total), recs.size());
+    const size_t have = tot < 0 ? 0 : std::min<size_t>(static_cast<size_t>(tot), recs.size());
     std::sort(recs.begin(), recs.begin() + have, [](const dlb_round_trace& a, const dlb_round_trace& b) {
       return a.stream != b.stream ? a.stream < b.stream : a.round < b.round;
     });
@@ -263,19 +519,27 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
       cfg.trace(RoundTrace{recs[i].round, recs[i].unfinished, recs[i].assigned, recs[i].speculative,
                            recs[i].idle_slots, recs[i].newly_done, recs[i].stream});
   }
+  if (cfg.assignment_hook) {
+    std::vector<dlb_assignment> recs(acap);
+    const long long tot = rc == 0 ? dlb_get_assignment_log(eng.ctx(), recs.data(), recs.size()) : 0;
+    dlb_set_assignment_log(eng.ctx(), 0);
+    const size_t have = tot < 0 ? 0 : std::min<size_t>(static_cast<size_t>(tot), recs.size());
+    for (size_t i = 0; i < have; ++i)
+      cfg.assignment_hook(Assignment{recs[i].slot, recs[i].task, recs[i].attempt, recs[i].kappa});
+  }
   if (rc == DLB_E_KEY) throw std::invalid_argument("batch_sign: malformed secret key");
-  check(rc, "dlb_sign_batch");
+  check(rc, "dlb_sign_submit / dlb_sign_wait");
   if (stats) {
-    stats->rounds = st.rounds;
-    stats->attempts = st.attempts;
-    stats->speculative = st.speculative;
-    stats->idle_slot_rounds = st.idle_slot_rounds;
-    stats->accepted_attempt_sum = st.accepted_attempt_sum;
+    stats->rounds = total.rounds;
+    stats->attempts = total.attempts;
+    stats->speculative = total.speculative;
+    stats->idle_slot_rounds = total.idle_slot_rounds;
+    stats->accepted_attempt_sum = total.accepted_attempt_sum;
     stats->failed_tasks.clear();
     for (size_t i = 0; i < n; ++i)
       if (failed[i]) stats->failed_tasks.push_back(i);
   }
-  if (attempts_out) *attempts_out = att;
+  if (attempts_out) attempts_out->assign(att, att + n);
   return out;
 }
 
@@ -286,6 +550,7 @@ std::vector<uint8_t> batch_verify(std::span<const VerifyJob<P>> jobs, size_t /*w
   const size_t n = jobs.size();
   std::vector<uint8_t> flags(n, 0);
   std::vector<size_t> live;
+  live.reserve(n);
   for (size_t i = 0; i < n; ++i)
     if (jobs[i].pk.size() == P.pk_bytes() && jobs[i].sig.size() == P.sig_bytes()) live.push_back(i);
   if (live.empty()) return flags;
@@ -300,23 +565,25 @@ std::vector<uint8_t> batch_verify(std::span<const VerifyJob<P>> jobs, size_t /*w
     if (fresh) keys.push_back(pkp);
     key_idx[a] = it->second;
   }
-  std::vector<uint8_t> pks(keys.size() * P.pk_bytes()), sigs(m * P.sig_bytes() + 8), flat, f(m);
-  for (size_t k = 0; k < keys.size(); ++k) std::memcpy(pks.data() + k * P.pk_bytes(), keys[k], P.pk_bytes());
-  std::vector<uint64_t> off(m + 1, 0);
-  for (size_t a = 0; a < m; ++a) off[a + 1] = off[a] + jobs[live[a]].message.size();
-  flat.resize(off.back() + 8);
+  uint8_t* pks = eng.in_a.get(keys.size() * P.pk_bytes());
+  for (size_t k = 0; k < keys.size(); ++k) std::memcpy(pks + k * P.pk_bytes(), keys[k], P.pk_bytes());
+  size_t total_msg = 0;
+  for (size_t a = 0; a < m; ++a) total_msg += jobs[live[a]].message.size();
+  uint8_t* flat = eng.in_b.get(total_msg + 8);
+  uint64_t* off = reinterpret_cast<uint64_t*>(eng.in_c.get((m + 1) * 8));
+  uint8_t* sigs = eng.in_d.get(m * P.sig_bytes() + 8);
+  uint8_t* f = eng.out_c.get(m);
+  off[0] = 0;
   for (size_t a = 0; a < m; ++a) {
     const auto& j = jobs[live[a]];
-    std::memcpy(sigs.data() + a * P.sig_bytes(), j.sig.data(), P.sig_bytes());
-    if (!j.message.empty()) std::memcpy(flat.data() + off[a], j.message.data(), j.message.size());
+    std::memcpy(sigs + a * P.sig_bytes(), j.sig.data(), P.sig_bytes());
+    if (!j.message.empty()) std::memcpy(flat + off[a], j.message.data(), j.message.size());
+    off[a + 1] = off[a] + j.message.size();
   }
   if (keys.size() == 1)
-    check(dlb_verify_batch(eng.ctx(), P.level, m, pks.data(), 0, flat.data(), off.data(), sigs.data(),
-                           f.data()),
-          "dlb_verify_batch");
+    check(dlb_verify_batch(eng.ctx(), P.level, m, pks, 0, flat, off, sigs, f), "dlb_verify_batch");
   else
-    check(dlb_verify_batch_keyed(eng.ctx(), P.level, keys.size(), pks.data(), m, key_idx.data(),
-                                 flat.data(), off.data(), sigs.data(), f.data()),
+    check(dlb_verify_batch_keyed(eng.ctx(), P.level, keys.size(), pks, m, key_idx.data(), flat, off, sigs, f),
           "dlb_verify_batch_keyed");
   for (size_t a = 0; a < m; ++a) flags[live[a]] = f[a];
   return flags;
@@ -368,47 +635,62 @@ bool verify(std::span<const uint8_t> pk_bytes, std::span<const uint8_t> msg,
 // hi = n*(g+1)/G exactly like the reference tool's multi-engine mode
 // (tools/dilithium_cli.cpp:319-339), one Engine and one host thread per device, results
 // land in order.  No collective, no NCCL.  (Listing a device twice gives two contexts on
-// that GPU -- used by the tests, which see a single GPU.)
+// that GPU -- used by the tests, which see a single GPU.)  Each shard thread is pinned to the
+// CPUs of its GPU's NUMA node (dlb_bind_thread_to_device) before it allocates or touches its
+// engine's pinned staging, so staging pages and the copies through them stay node-local.
 class ShardedEngine {
  public:
-  explicit ShardedEngine(const std::vector<int>& devices) {
-    for (int d : devices) engines_.push_back(std::make_unique<Engine>(d));
-    if (engines_.empty()) throw std::invalid_argument("ShardedEngine: no devices");
+  explicit ShardedEngine(const std::vector<int>& devices) : devices_(devices) {
+    if (devices.empty()) throw std::invalid_argument("ShardedEngine: no devices");
+    engines_.resize(devices.size());
+    // engines are created by their own (bound) threads: first-touch places the pinned staging
+    run(devices.size(), [&](size_t g, size_t, size_t) { engines_[g] = std::make_unique<Engine>(devices_[g]); },
+        /*per_engine=*/true);
   }
   size_t size() const { return engines_.size(); }
+  // shard boundaries of an n-task batch (the partition run() uses)
+  std::vector<size_t> partition(size_t n) const {
+    std::vector<size_t> b(engines_.size() + 1);
+    for (size_t g = 0; g <= engines_.size(); ++g) b[g] = n * g / engines_.size();
+    return b;
+  }
 
   template <Params P>
   std::vector<std::pair<PkBytes<P>, SkBytes<P>>> batch_keygen(std::span<const SeedArray> zetas) {
-    std::vector<std::pair<PkBytes<P>, SkBytes<P>>> out(zetas.size());
-    run(zetas.size(), [&](Engine& e, size_t lo, size_t hi) {
-      auto part = b200::batch_keygen<P>(zetas.subspan(lo, hi - lo), 1, e);
-      std::move(part.begin(), part.end(), out.begin() + lo);
+    std::vector<std::vector<std::pair<PkBytes<P>, SkBytes<P>>>> parts(engines_.size());
+    run(zetas.size(), [&](size_t g, size_t lo, size_t hi) {
+      parts[g] = b200::batch_keygen<P>(zetas.subspan(lo, hi - lo), 1, *engines_[g]);
     });
+    std::vector<std::pair<PkBytes<P>, SkBytes<P>>> out;
+    out.reserve(zetas.size());
+    for (auto& p : parts) out.insert(out.end(), p.begin(), p.end());
     return out;
   }
 
   template <Params P>
   std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const BatchConfig& cfg = {},
                                       BatchStats* stats = nullptr) {
-    std::vector<SigBytes<P>> out(jobs.size());
-    std::vector<BatchStats> part_stats(engines_.size());
-    std::vector<size_t> los(engines_.size(), 0);
-    run(jobs.size(), [&](Engine& e, size_t lo, size_t hi) {
-      const size_t g = index_of(e);
+    const size_t G = engines_.size();
+    std::vector<std::vector<SigBytes<P>>> parts(G);
+    std::vector<BatchStats> part_stats(G);
+    std::vector<size_t> los(G, 0);
+    run(jobs.size(), [&](size_t g, size_t lo, size_t hi) {
       los[g] = lo;
-      auto part = b200::batch_sign<P>(jobs.subspan(lo, hi - lo), cfg, &part_stats[g], e);
-      std::copy(part.begin(), part.end(), out.begin() + lo);
+      parts[g] = b200::batch_sign<P>(jobs.subspan(lo, hi - lo), cfg, &part_stats[g], *engines_[g]);
     });
+    std::vector<SigBytes<P>> out;
+    out.reserve(jobs.size());
+    for (auto& p : parts) out.insert(out.end(), p.begin(), p.end());
     if (stats) {
       *stats = BatchStats{};
-      for (size_t g = 0; g < engines_.size(); ++g) {
+      for (size_t g = 0; g < G; ++g) {
         const BatchStats& s = part_stats[g];
         stats->rounds += s.rounds;
         stats->attempts += s.attempts;
         stats->speculative += s.speculative;
         stats->idle_slot_rounds += s.idle_slot_rounds;
         stats->accepted_attempt_sum += s.accepted_attempt_sum;
-        for (size_t t : s.failed_tasks) stats->failed_tasks.push_back(los[g] + t);
+        for (size_t t : s.failed_tasks) stats->failed_tasks.push_back(los[g] + t);  // rebased to the batch
       }
     }
     return out;
@@ -417,31 +699,27 @@ class ShardedEngine {
   template <Params P>
   std::vector<uint8_t> batch_verify(std::span<const VerifyJob<P>> jobs) {
     std::vector<uint8_t> flags(jobs.size(), 0);
-    run(jobs.size(), [&](Engine& e, size_t lo, size_t hi) {
-      auto part = b200::batch_verify<P>(jobs.subspan(lo, hi - lo), 1, e);
+    run(jobs.size(), [&](size_t g, size_t lo, size_t hi) {
+      auto part = b200::batch_verify<P>(jobs.subspan(lo, hi - lo), 1, *engines_[g]);
       std::copy(part.begin(), part.end(), flags.begin() + lo);
     });
     return flags;
   }
 
  private:
-  size_t index_of(const Engine& e) const {
-    for (size_t g = 0; g < engines_.size(); ++g)
-      if (engines_[g].get() == &e) return g;
-    return 0;
-  }
   // fork-join over the shards; the first exception is rethrown like WorkerPool::parallel_for
   template <class Fn>
-  void run(size_t n, Fn&& fn) {
+  void run(size_t n, Fn&& fn, bool per_engine = false) {
     const size_t G = engines_.size();
     std::vector<std::thread> threads;
     std::vector<std::exception_ptr> errs(G);
     for (size_t g = 0; g < G; ++g) {
-      const size_t lo = n * g / G, hi = n * (g + 1) / G;
+      const size_t lo = per_engine ? g : n * g / G, hi = per_engine ? g + 1 : n * (g + 1) / G;
       if (hi == lo) continue;
       threads.emplace_back([&, g, lo, hi] {
         try {
-          fn(*engines_[g], lo, hi);
+          dlb_bind_thread_to_device(devices_[g]);  // best effort: NUMA-local CPUs of that GPU
+          fn(g, lo, hi);
         } catch (...) {
           errs[g] = std::current_exception();
         }
@@ -451,6 +729,7 @@ class ShardedEngine {
     for (auto& e : errs)
       if (e) std::rethrow_exception(e);
   }
+  std::vector<int> devices_;
   std::vector<std::unique_ptr<Engine>> engines_;
 };
 

@@ -543,10 +543,10 @@ static void mul_c(int32_t out[N], const int32_t chat[N], const int32_t shat[N]) 
   for (int m = 0; m < N; ++m) out[m] = centered(out[m]);
 }
 
-/* scheme.hpp:133-219 with the production bounds of :225-230 */
-static int attempt(const precomp* pre, const orc_params* P, const uint8_t mu[64],
-                   const uint8_t rho_prime[64], uint32_t kappa, int* stage, uint8_t* c_tilde,
-                   int32_t z[][N], int32_t hints[][N]) {
+/* scheme.hpp:133-219 (sign_attempt_bounded): bounds = {z, r0, c t0} norm bounds */
+static int attempt_bounded(const precomp* pre, const orc_params* P, const uint8_t mu[64],
+                           const uint8_t rho_prime[64], uint32_t kappa, const int32_t bounds[3],
+                           int* stage, uint8_t* c_tilde, int32_t z[][N], int32_t hints[][N]) {
   static _Thread_local int32_t y[LMAX][N], yh[LMAX][N], w[KMAX][N], w1[KMAX][N], wcs2[KMAX][N],
       vt[KMAX][N];
   int32_t c[N], chat[N], tmp[N];
@@ -572,7 +572,7 @@ static int attempt(const precomp* pre, const orc_params* P, const uint8_t mu[64]
   for (int j = 0; j < P->l; ++j) { /* scheme.hpp:167-174 */
     mul_c(tmp, chat, pre->s1h[j]);
     for (int m = 0; m < N; ++m) z[j][m] = centered((int64_t)y[j][m] + tmp[m]);
-    if (norm_ge(z[j], P->gamma1 - P->beta)) {
+    if (norm_ge(z[j], bounds[0])) {
       *stage = 0;
       return 0;
     }
@@ -584,14 +584,14 @@ static int attempt(const precomp* pre, const orc_params* P, const uint8_t mu[64]
       wcs2[i][m] = modq((int64_t)w[i][m] - tmp[m]);
       orc_decompose(wcs2[i][m], P->gamma2, &r1, &r0[m]);
     }
-    if (norm_ge(r0, P->gamma2 - P->beta)) {
+    if (norm_ge(r0, bounds[1])) {
       *stage = 1;
       return 0;
     }
   }
   for (int i = 0; i < P->k; ++i) { /* scheme.hpp:192-199 */
     mul_c(vt[i], chat, pre->t0h[i]);
-    if (norm_ge(vt[i], P->gamma2)) {
+    if (norm_ge(vt[i], bounds[2])) {
       *stage = 2;
       return 0;
     }
@@ -611,11 +611,31 @@ static int attempt(const precomp* pre, const orc_params* P, const uint8_t mu[64]
   return 1;
 }
 
+/* the production bounds of scheme.hpp:225-230 */
+static int attempt(const precomp* pre, const orc_params* P, const uint8_t mu[64],
+                   const uint8_t rho_prime[64], uint32_t kappa, int* stage, uint8_t* c_tilde,
+                   int32_t z[][N], int32_t hints[][N]) {
+  const int32_t b[3] = {P->gamma1 - P->beta, P->gamma2 - P->beta, P->gamma2};
+  return attempt_bounded(pre, P, mu, rho_prime, kappa, b, stage, c_tilde, z, hints);
+}
+
 int orc_sign_attempt(int level, const uint8_t* sk, const uint8_t mu[64],
                      const uint8_t rho_prime[64], uint32_t kappa, int* stage,
                      uint8_t* c_tilde, int32_t* z, int32_t* hints) {
   const orc_params* P = orc_get_params(level);
   if (!P) return -1;
+  const int32_t b[3] = {P->gamma1 - P->beta, P->gamma2 - P->beta, P->gamma2};
+  return orc_sign_attempt_bounded(level, sk, mu, rho_prime, kappa, b[0], b[1], b[2], stage, c_tilde, z,
+                                  hints);
+}
+
+int orc_sign_attempt_bounded(int level, const uint8_t* sk, const uint8_t mu[64],
+                             const uint8_t rho_prime[64], uint32_t kappa, int32_t z_bound,
+                             int32_t r0_bound, int32_t vt_bound, int* stage, uint8_t* c_tilde,
+                             int32_t* z, int32_t* hints) {
+  const orc_params* P = orc_get_params(level);
+  if (!P) return -1;
+  const int32_t bounds[3] = {z_bound, r0_bound, vt_bound};
   precomp* pre = malloc(sizeof *pre);
   if (!make_precomp(pre, sk, P)) {
     free(pre);
@@ -624,7 +644,7 @@ int orc_sign_attempt(int level, const uint8_t* sk, const uint8_t mu[64],
   int32_t(*zz)[N] = calloc(LMAX, sizeof *zz);
   int32_t(*hh)[N] = calloc(KMAX, sizeof *hh);
   int st = 0;
-  int ok = attempt(pre, P, mu, rho_prime, kappa, &st, c_tilde, zz, hh);
+  int ok = attempt_bounded(pre, P, mu, rho_prime, kappa, bounds, &st, c_tilde, zz, hh);
   memcpy(z, zz, sizeof(int32_t) * N * (size_t)P->l);
   memcpy(hints, hh, sizeof(int32_t) * N * (size_t)P->k);
   if (stage) *stage = st;

@@ -87,6 +87,12 @@ int orc_sign_attempt(int level, const uint8_t* sk, const uint8_t mu[64],
                      const uint8_t rho_prime[64], uint32_t kappa, int* stage,
                      uint8_t* c_tilde, int32_t* z, int32_t* hints);
 
+/* detail::sign_attempt_bounded (scheme.hpp:133-138): the same with the norm bounds injected */
+int orc_sign_attempt_bounded(int level, const uint8_t* sk, const uint8_t mu[64],
+                             const uint8_t rho_prime[64], uint32_t kappa, int32_t z_bound,
+                             int32_t r0_bound, int32_t vt_bound, int* stage, uint8_t* c_tilde,
+                             int32_t* z, int32_t* hints);
+
 #ifdef __cplusplus
 }
 #endif

@@ -151,6 +151,24 @@ int ref_sign_attempt(int level, const uint8_t* sk, const uint8_t* mu, const uint
   });
 }
 
+int ref_sign_attempt_bounded(int level, const uint8_t* sk, const uint8_t* mu, const uint8_t* rho_prime,
+                             uint32_t kappa, int32_t z_bound, int32_t r0_bound, int32_t vt_bound,
+                             int* stage, uint8_t* c_tilde, int32_t* z, int32_t* hints) {
+  return dispatch(level, [&](auto tag) {
+    constexpr Params P = decltype(tag)::value;
+    auto pre = make_precomp<P>(std::span<const uint8_t>(sk, P.sk_bytes()));
+    if (!pre) return -1;
+    auto r = detail::sign_attempt_bounded<P>(*pre, std::span<const uint8_t, 64>(mu, 64),
+                                             std::span<const uint8_t, 64>(rho_prime, 64), kappa, z_bound,
+                                             r0_bound, vt_bound);
+    if (stage) *stage = static_cast<int>(r.stage);
+    std::memcpy(c_tilde, r.c_tilde.data(), 32);
+    for (size_t j = 0; j < P.l; ++j) std::memcpy(z + 256 * j, r.z.p[j].c.data(), 1024);
+    for (size_t i = 0; i < P.k; ++i) std::memcpy(hints + 256 * i, r.hints.p[i].c.data(), 1024);
+    return r.accepted ? 1 : 0;
+  });
+}
+
 int ref_batch_keygen(int level, size_t n, const uint8_t* zetas, uint8_t* pks, uint8_t* sks,
                      size_t workers) {
   return dispatch(level, [&](auto tag) {

@@ -1,5 +1,7 @@
 // engine.cu -- C ABI (include/dilithium_b200.h): context, host<->device marshalling,
 // level dispatch, and the stage-level entry points used by the device parity tests.
+#include <sched.h>
+
 #include "engine.cuh"
 #include "ntt.cuh"
 #include "samplers.cuh"
@@ -318,6 +320,67 @@ int dlb_set_mldsa_context(dlb_ctx* c, const uint8_t* ctx_bytes, size_t len) {
   return 0;
 }
 
+namespace {
+
+// "/sys/bus/pci/devices/<domain:bus:dev.fn>/<leaf>" of a CUDA device, first line
+bool pci_sysfs_line(int device, const char* leaf, char* out, size_t cap) {
+  char id[32] = {};
+  if (cudaDeviceGetPCIBusId(id, sizeof id, device) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  for (char* p = id; *p; ++p)
+    if (*p >= 'A' && *p <= 'Z') *p = (char)(*p - 'A' + 'a');
+  char path[128];
+  snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/%s", id, leaf);
+  FILE* f = fopen(path, "r");
+  if (!f) return false;
+  const bool ok = fgets(out, (int)cap, f) != nullptr;
+  fclose(f);
+  return ok;
+}
+
+}  // namespace
+
+int dlb_device_numa_node(int device) {
+  char line[64];
+  if (!pci_sysfs_line(device, "numa_node", line, sizeof line)) return -1;
+  return atoi(line);
+}
+
+int dlb_bind_thread_to_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    return DLB_E_ARG;
+  }
+  if (device < 0 || device >= count) return DLB_E_ARG;
+  char line[4096];
+  if (!pci_sysfs_line(device, "local_cpulist", line, sizeof line)) return 1;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  int n_set = 0;
+  for (char* p = line; *p && *p != '\n';) {  // "0-15,32-47"
+    char* end;
+    const long a = strtol(p, &end, 10);
+    if (end == p) break;
+    long b = a;
+    p = end;
+    if (*p == '-') {
+      b = strtol(p + 1, &end, 10);
+      p = end;
+    }
+    for (long cpu = a; cpu <= b && cpu < CPU_SETSIZE; ++cpu) {
+      CPU_SET((int)cpu, &set);
+      ++n_set;
+    }
+    if (*p == ',') ++p;
+  }
+  if (n_set == 0) return 1;
+  if (sched_setaffinity(0, sizeof set, &set) != 0) return 1;  // e.g. a cgroup that excludes those CPUs
+  return 0;
+}
+
 void* dlb_host_alloc(size_t bytes) {
   void* p = nullptr;
   if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
@@ -485,6 +548,21 @@ inline size_t pipe_chunk(const dlb_ctx* ctx, size_t n) {
   return c < n ? c : n;
 }
 
+// On an early error return of a host pipeline, copies and kernels that reference the caller's
+// buffers may still be in flight on the engine's streams: drain them before the call returns.
+struct DrainOnError {
+  dlb_ctx* c;
+  bool ok = false;
+  explicit DrainOnError(dlb_ctx* ctx) : c(ctx) {}
+  ~DrainOnError() {
+    if (ok) return;
+    cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->copy_in);
+    cudaStreamSynchronize(c->copy_out);
+    cudaGetLastError();
+  }
+};
+
 struct OwnStream {  // host-buffer calls always run on the engine's own streams
   dlb_ctx* c;
   cudaStream_t saved;
@@ -520,6 +598,7 @@ int dlb_keygen_batch(dlb_ctx* c, int level, size_t n, const uint8_t* zetas, uint
   if (!zetas || !pks || !sks) return DLB_E_ARG;
   cudaSetDevice(c->device);
   OwnStream own(c);
+  DrainOnError drain(c);
   cudaStream_t S = c->stream, CO = c->copy_out;
   const size_t chunk = pipe_chunk(c, n);
   uint8_t *dz, *dpk[2], *dsk[2];
@@ -549,6 +628,7 @@ int dlb_keygen_batch(dlb_ctx* c, int level, size_t n, const uint8_t* zetas, uint
   DLB_CU(cudaStreamSynchronize(CO));
   DLB_CU(cudaStreamSynchronize(S));
   cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  drain.ok = true;
   return 0;
 }
 
@@ -561,6 +641,13 @@ bool key_idx_ok(const uint32_t* key_idx, size_t n, size_t n_keys) {
   return true;
 }
 
+// offsets must be non-decreasing (task i uses msgs[off[i] .. off[i+1])) and msgs non-null when any byte is used
+bool msg_off_ok(const uint8_t* msgs, const uint64_t* msg_off, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (msg_off[i + 1] < msg_off[i]) return false;
+  return msg_off[n] == msg_off[0] || msgs != nullptr;
+}
+
 int verify_host(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_stride, size_t n_keys,
                 const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,
                 const uint8_t* sigs, uint8_t* flags) {
@@ -571,8 +658,10 @@ int verify_host(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_s
   if (!pks || !msg_off || !sigs || !flags) return DLB_E_ARG;
   if (pk_stride != 0 && pk_stride != ls.pk) return DLB_E_ARG;
   if (key_idx && (n_keys == 0 || pk_stride == 0 || !key_idx_ok(key_idx, n, n_keys))) return DLB_E_ARG;
+  if (msg_off[0] != 0 || !msg_off_ok(msgs, msg_off, n)) return DLB_E_ARG;
   cudaSetDevice(c->device);
   OwnStream own(c);
+  DrainOnError drain(c);
   cudaStream_t S = c->stream, CI = c->copy_in;
   const size_t mbytes = msg_off[n];
   const size_t chunk = pipe_chunk(c, n);
@@ -610,8 +699,10 @@ int verify_host(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_s
     DLB_CU(cudaEventRecord(c->ev_in[b], CI));
     DLB_CU(cudaStreamWaitEvent(S, c->ev_in[b], 0));
     DLB_TRY(with_level(level, [&](auto p) {
+      // a shared key or a key table is expanded by the first chunk only (every distinct key once)
       return verify_dev<decltype(p)>(c, cnt, (pk_stride && !keyed) ? dpk[b] : dpk[0], pk_stride, n_keys,
-                                     keyed ? dkidx + lo : nullptr, dm, doff + lo, dsig[b], dfl + lo);
+                                     keyed ? dkidx + lo : nullptr, dm, doff + lo, dsig[b], dfl + lo,
+                                     ci > 0 && (keyed || !pk_stride));
     }));
     DLB_CU(cudaEventRecord(c->ev_comp[b], S));
   }
@@ -619,6 +710,7 @@ int verify_host(dlb_ctx* c, int level, size_t n, const uint8_t* pks, size_t pk_s
   DLB_CU(cudaEventRecord(c->ev1, S));
   DLB_CU(cudaStreamSynchronize(S));
   cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+  drain.ok = true;
   return 0;
 }
 
@@ -640,13 +732,6 @@ int dlb_verify_batch_keyed(dlb_ctx* c, int level, size_t n_keys, const uint8_t* 
 }
 
 namespace {
-
-// offsets must be non-decreasing (task i signs msgs[off[i] .. off[i+1])) and msgs non-null when any byte is used
-bool msg_off_ok(const uint8_t* msgs, const uint64_t* msg_off, size_t n) {
-  for (size_t i = 0; i < n; ++i)
-    if (msg_off[i + 1] < msg_off[i]) return false;
-  return msg_off[n] == msg_off[0] || msgs != nullptr;
-}
 
 int sign_host_submit(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t sk_stride, size_t n_keys,
                      const uint32_t* key_idx, const uint8_t* msgs, const uint64_t* msg_off,

@@ -299,7 +299,7 @@ int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uin
 template <class P>
 int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, size_t n_keys,
                const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
-               const uint8_t* d_sigs, uint8_t* d_flags);
+               const uint8_t* d_sigs, uint8_t* d_flags, bool keys_expanded = false);
 // signing: reserve a ticket (and learn its stream lane, for the caller's input copies), enqueue
 // the batch, later wait for it (sign.cu)
 int sign_reserve(dlb_ctx* c, unsigned* ticket, cudaStream_t* lane);

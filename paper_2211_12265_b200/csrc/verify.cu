@@ -46,7 +46,7 @@ __global__ void k_verify_final(unsigned n, const uint64_t* __restrict__ mu,
 template <class P>
 int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, size_t n_keys,
                const uint32_t* d_key_idx, const uint8_t* d_msgs, const uint64_t* d_msg_off,
-               const uint8_t* d_sigs, uint8_t* d_flags) {
+               const uint8_t* d_sigs, uint8_t* d_flags, bool keys_expanded) {
   using S = Sizes<P>;
   constexpr int KL = P::K * P::L;
   constexpr int HW = 4;  // warps per CTA for the sponge kernels
@@ -93,7 +93,9 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
   const uint8_t* pfx = nullptr;
   unsigned plen = 0;
   if (Hashing<P>::MLDSA) DLB_TRY(mldsa_prefix(c, main, &pfx, &plen));
-  if (shared_key) {  // expand once on the caller's stream, before the fork
+  // (keys_expanded: a previous call of the same host-side batch already expanded this key
+  // table into the context's arenas -- the host pipeline calls once per transfer chunk)
+  if (shared_key && !keys_expanded) {  // expand once on the caller's stream, before the fork
     k_expand_a<P, HW><<<cdiv(n_keys * KL, HW * 32), HW * 32, 0, main>>>(d_pks, pk_stride,
                                                                         (unsigned)(n_keys * KL), A[0]);
     k_hash_tr<<<cdiv(n_keys, 128), 128, 0, main>>>(d_pks, pk_stride, S::PK, (unsigned)n_keys, tr[0],
@@ -141,7 +143,7 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
 #define DLB_INST(LV)                                                                          \
   template int verify_dev<Params<LV>>(dlb_ctx*, size_t, const uint8_t*, size_t, size_t,       \
                                       const uint32_t*, const uint8_t*, const uint64_t*,       \
-                                      const uint8_t*, uint8_t*);
+                                      const uint8_t*, uint8_t*, bool);
 DLB_INST(2)
 DLB_INST(3)
 DLB_INST(5)

@@ -63,6 +63,8 @@ def load_library():
         "dlb_set_mldsa_context": (C.c_int, [vp, _u8p, sz]),
         "dlb_set_trace": (C.c_int, [vp, sz]),
         "dlb_get_trace": (C.c_longlong, [vp, vp, sz]),
+        "dlb_bind_thread_to_device": (C.c_int, [C.c_int]),
+        "dlb_device_numa_node": (C.c_int, [C.c_int]),
         "dlb_host_alloc": (vp, [sz]),
         "dlb_host_free": (None, [vp]),
         "dlb_keygen_batch": (C.c_int, [vp, C.c_int, sz, _u8p, _u8p, _u8p]),
@@ -116,6 +118,7 @@ EXPORTED_SYMBOLS = [
     "dlb_dbg_sample_in_ball", "dlb_dbg_rounding", "dlb_dbg_ntt", "dlb_dbg_sign_attempt",
     "dlb_dbg_sign_attempt_bounded", "dlb_dbg_set_max_attempt", "dlb_set_assignment_log",
     "dlb_get_assignment_log", "dlb_sign_submit", "dlb_sign_submit_dev", "dlb_sign_wait",
+    "dlb_bind_thread_to_device", "dlb_device_numa_node",
 ]
 
 
@@ -313,6 +316,8 @@ class Engine:
                                       vp(rpa.ctypes.data) if rpa is not None else None, psi,
                                       1 if speculate else 0, vp(sigs.ctypes.data), vp(att.ctypes.data),
                                       vp(failed.ctypes.data), C.byref(ticket))
+        if rc == -3:
+            raise ValueError("sign: malformed secret key")  # scheme.hpp:271
         self._chk(rc, "dlb_sign_submit")
         return {"ticket": ticket.value, "sigs": sigs, "att": att, "failed": failed,
                 "keep": (sk, flat, off, kidx, rpa)}

@@ -128,6 +128,8 @@ class _Checker:
         f("verify", C.c_int, [C.c_int, _u8p, C.c_size_t, _u8p, C.c_size_t, _u8p, C.c_size_t])
         f("sign_attempt", C.c_int, [C.c_int, _u8p, _u8p, _u8p, C.c_uint32, C.POINTER(C.c_int),
                                     _u8p, i32p, i32p])
+        f("sign_attempt_bounded", C.c_int, [C.c_int, _u8p, _u8p, _u8p, C.c_uint32, C.c_int32, C.c_int32,
+                                            C.c_int32, C.POINTER(C.c_int), _u8p, i32p, i32p])
 
     def _f(self, name, res, args):
         fn = getattr(self.lib, self.prefix + name)
@@ -222,6 +224,20 @@ class _Checker:
         rc = self._sign_attempt(level, _p(bytes(sk)), _p(bytes(mu)), _p(bytes(rho_prime)), kappa,
                                 C.byref(st), _p(ct), z.ctypes.data_as(i32p),
                                 h.ctypes.data_as(i32p))
+        return rc, st.value, ct.tobytes(), z, h
+
+
+    def sign_attempt_bounded(self, level, sk, mu, rho_prime, kappa, z_bound, r0_bound, vt_bound):
+        """detail::sign_attempt_bounded (scheme.hpp:133-219): (accepted, stage, c_tilde, z, hints)."""
+        P = PARAMS[level]
+        z = np.zeros((P["l"], 256), np.int32)
+        h = np.zeros((P["k"], 256), np.int32)
+        ct = np.zeros(P["ct"], np.uint8)
+        st = C.c_int(0)
+        i32p = C.POINTER(C.c_int32)
+        rc = self._sign_attempt_bounded(level, _p(bytes(sk)), _p(bytes(mu)), _p(bytes(rho_prime)), kappa,
+                                        z_bound, r0_bound, vt_bound, C.byref(st), _p(ct),
+                                        z.ctypes.data_as(i32p), h.ctypes.data_as(i32p))
         return rc, st.value, ct.tobytes(), z, h
 
 

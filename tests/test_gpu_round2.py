@@ -1,0 +1,204 @@
+"""Round-2 boundary and scheduler tests on the device (-m gpu): the assignment hook and the
+scheduler-equivalence criterion (tests/acceptance.cpp:186-244), injected norm bounds and reject
+stages (tests/test_scheme.cpp:147-174), nonce-space exhaustion (scheduler.hpp:52,122-128),
+batches in flight (tools/dilithium_cli.cpp:309-345), the cross-call key cache."""
+import numpy as np
+import pytest
+
+from tests.cpu_checkers import PARAMS, mt19937_64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_2211_12265_b200 import Engine
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+def _cpu_sign_all(checker, ref, level, sk, flat, off):
+    """Sequential signatures of every message: the compiled reference when it is there (all
+    host threads; batch == sequential is its own criterion 5), else the oracle one by one."""
+    n = len(off) - 1
+    try:
+        from tests.cpu_checkers import load_ref, ref_available
+        if ref_available():
+            r = load_ref()
+            return r.batch_sign(level, sk, flat, off, workers=max(1, r.hw_threads()))[0]
+    except Exception:
+        pass
+    return np.stack([np.frombuffer(checker.sign(level, sk.tobytes(), flat[int(off[i]):int(off[i + 1])].tobytes())[0],
+                                   np.uint8) for i in range(n)])
+
+
+def test_acceptance5_scheduler_equivalence_with_hook(eng, oracle):
+    """acceptance.cpp:221-244: 100 random batches (phi <= 512, psi <= phi, 8 of 10 at level 2, one
+    each at 3 and 5): bytes identical to sequential signing, and the assignment hook's records
+    (here: the device's executed-attempt log) hold no (task, nonce) twice and every nonce below
+    each task's accepted one."""
+    rng = mt19937_64(55)
+    for b in range(100):
+        phi = 1 + int(rng()) % 512
+        psi = 1 + int(rng()) % phi
+        level = 2 if b % 10 < 8 else (3 if b % 10 == 8 else 5)
+        L = PARAMS[level]["l"]
+        pk, sk = oracle.keygen(level, rng.bytes(32))
+        sk_a = np.frombuffer(sk, np.uint8)
+        flat = np.frombuffer(rng.bytes(24 * phi), np.uint8)
+        off = np.arange(phi + 1, dtype=np.uint64) * 24
+        eng.set_assignment_log(64 * phi + 4096)
+        sigs, att, failed, st = eng.batch_sign(level, sk_a, (flat, off), psi=psi, return_info=True)
+        recs, total = eng.get_assignment_log()
+        eng.set_assignment_log(0)
+        assert not failed.any()
+        assert total == len(recs) == st["attempts"], (total, len(recs), st["attempts"])
+        pairs = recs[:, 1].astype(np.int64) * 65536 + recs[:, 3]
+        assert len(np.unique(pairs)) == len(pairs), "a (task, nonce) was executed twice"
+        assert np.array_equal(recs[:, 3], recs[:, 2] * L)  # kappa = attempt * l
+        have = set(pairs.tolist())
+        for t in range(phi):
+            for a in range(int(att[t])):
+                assert t * 65536 + a * L in have, "an attempt below the accepted one never ran"
+        assert np.array_equal(sigs, _cpu_sign_all(oracle, None, level, sk_a, flat, off)), "batch != sequential"
+
+
+@pytest.mark.parametrize("level", [2, 3, 5, 65])
+def test_forced_reject_stages(eng, oracle, ref, level):
+    """test_scheme.cpp:147-174 at scale: sign_attempt_bounded with the production bounds, with each
+    bound corrupted to 1, and with bounds tightened just enough that all four stages occur --
+    accepted flag, reject stage, c~, z and hints equal the CPU checker's."""
+    P = PARAMS[level]
+    n = 160
+    rng = mt19937_64(6040 + level)
+    pk, sk = oracle.keygen(level, rng.bytes(32))
+    sk_a = np.frombuffer(sk, np.uint8)
+    mus = np.frombuffer(rng.bytes(64 * n), np.uint8).reshape(n, 64)
+    rps = np.frombuffer(rng.bytes(64 * n), np.uint8).reshape(n, 64)
+    kappas = np.array([(int(rng()) % 50) * P["l"] for _ in range(n)], np.uint32)
+    g1b, g2b, g2 = P["gamma1"] - P["beta"], P["gamma2"] - P["beta"], P["gamma2"]
+    checker = oracle if level > 5 else ref  # the reference has no FIPS 204 sets
+    seen = set()
+    for zb, rb, vb in ((g1b, g2b, g2), (1, g2b, g2), (g1b, 1, g2), (g1b, g2b, 1),
+                       (g1b, g2b, g2 // 3), (g1b - g1b // 40, g2b - g2b // 12, (g2 * 2) // 5)):
+        acc, stage, ct, z, h = eng.dbg_sign_attempt_bounded(level, sk_a, mus, rps, kappas, zb, rb, vb)
+        for i in range(n):
+            rc, st, ect, ez, eh = checker.sign_attempt_bounded(level, sk, mus[i].tobytes(), rps[i].tobytes(),
+                                                               int(kappas[i]), zb, rb, vb)
+            assert acc[i] == rc, (i, zb, rb, vb)
+            assert ct[i].tobytes() == ect
+            if rc:
+                assert stage[i] == 255 and np.array_equal(z[i], ez) and np.array_equal(h[i], eh)
+            else:
+                assert stage[i] == st, (i, stage[i], st, zb, rb, vb)
+                seen.add(int(st))
+    assert seen == {0, 1, 2} or seen == {0, 1, 2, 3}, seen
+    with pytest.raises(Exception):  # chknorm's domain (rounding.hpp:65)
+        eng.dbg_sign_attempt_bounded(level, sk_a, mus[:1], rps[:1], kappas[:1], (8380417 - 1) // 8 + 1, rb, vb)
+
+
+@pytest.mark.parametrize("level", [2, 5])
+def test_nonce_space_exhaustion_reports_failed_tasks(eng, oracle, level):
+    """scheduler.hpp:52,122-128 / batch.hpp:128-131: a task whose nonce space runs out is reported
+    failed, gets an all-zero signature, and the others still complete.  The real limit is
+    unreachable, so the stage-test knob shrinks it to three attempts."""
+    n = 600
+    rng = mt19937_64(1220 + level)
+    pk, sk = oracle.keygen(level, rng.bytes(32))
+    sk_a = np.frombuffer(sk, np.uint8)
+    flat = np.frombuffer(rng.bytes(20 * n), np.uint8)
+    off = np.arange(n + 1, dtype=np.uint64) * 20
+    expect = [oracle.sign(level, sk, flat[20 * i:20 * i + 20].tobytes()) for i in range(n)]
+    eng.dbg_set_max_attempt(2)
+    try:
+        for psi, spec in ((0, True), (64, False), (4096, True)):
+            sigs, att, failed, st = eng.batch_sign(level, sk_a, (flat, off), psi=psi, speculate=spec,
+                                                   return_info=True)
+            want_failed = np.array([a > 3 for _, a in expect], np.uint8)
+            assert np.array_equal(failed, want_failed) and 0 < want_failed.sum() < n
+            assert st["failed_tasks"] == int(want_failed.sum())
+            for i in range(n):
+                if want_failed[i]:
+                    assert not sigs[i].any() and att[i] == 0
+                else:
+                    assert sigs[i].tobytes() == expect[i][0] and att[i] == expect[i][1]
+    finally:
+        eng.dbg_set_max_attempt(0)
+    sigs = eng.batch_sign(level, sk_a, (flat, off))
+    assert all(sigs[i].tobytes() == expect[i][0] for i in range(n))
+
+
+def test_batches_in_flight_mixed_levels_and_keys(eng, oracle):
+    """dlb_sign_submit / dlb_sign_wait: sixteen batches of different sizes, levels, keys and key
+    modes in flight at once, waited out of order -- every byte as if each had run alone."""
+    rng = mt19937_64(31415)
+    shapes = [(2, 3000, "shared"), (3, 700, "shared"), (2, 1, "shared"), (5, 900, "per_task"),
+              (2, 5000, "table"), (2, 64, "shared"), (3, 2000, "table"), (44, 800, "shared"),
+              (2, 12000, "shared"), (5, 300, "shared"), (2, 2500, "per_task"), (87, 100, "shared"),
+              (2, 9000, "shared"), (3, 33, "per_task"), (2, 777, "shared"), (65, 400, "table")]
+    jobs = []
+    for level, n, mode in shapes:
+        nk = {"shared": 1, "per_task": n, "table": 5}[mode]
+        zetas = np.frombuffer(rng.bytes(32 * nk), np.uint8).reshape(nk, 32)
+        pks, sks = eng.batch_keygen(level, zetas)
+        lens = [int(rng()) % 70 for _ in range(n)]
+        off = np.zeros(n + 1, np.uint64)
+        off[1:] = np.cumsum(lens)
+        flat = np.frombuffer(rng.bytes(int(off[-1]) + 1), np.uint8)
+        kidx = np.array([int(rng()) % nk for _ in range(n)], np.uint32) if mode == "table" else None
+        jobs.append((level, n, mode, sks, flat, off, kidx))
+    alone = []
+    for level, n, mode, sks, flat, off, kidx in jobs:
+        alone.append(eng.batch_sign(level, sks[0] if mode == "shared" else sks, (flat, off), key_idx=kidx,
+                                    return_info=True))
+    handles = [eng.sign_submit(level, sks[0] if mode == "shared" else sks, (flat, off), key_idx=kidx)
+               for level, n, mode, sks, flat, off, kidx in jobs]
+    with pytest.raises(Exception):  # the ring is full: a seventeenth submission is refused
+        eng.sign_submit(2, jobs[0][3][0], (jobs[0][4], jobs[0][5]))
+    order = [7, 0, 15, 3, 8, 1, 2, 12, 4, 5, 6, 9, 10, 11, 13, 14]
+    for j in order:
+        sigs, att, failed, st = eng.sign_wait(handles[j])
+        assert not failed.any() and np.array_equal(sigs, alone[j][0]) and np.array_equal(att, alone[j][1])
+        assert st["accepted_attempt_sum"] == int(att.sum())
+    for j in (0, 3, 4, 7, 15):  # and those bytes are the CPU oracle's
+        level, n, mode, sks, flat, off, kidx = jobs[j]
+        for i in range(0, n, max(1, n // 9)):
+            k = 0 if mode == "shared" else (int(kidx[i]) if mode == "table" else i)
+            assert alone[j][0][i].tobytes() == oracle.sign(level, sks[k].tobytes(),
+                                                           flat[int(off[i]):int(off[i + 1])].tobytes())[0]
+    # the engine is usable afterwards, synchronously and with new tickets
+    h = eng.sign_submit(2, jobs[0][3][0], (jobs[0][4], jobs[0][5]))
+    assert np.array_equal(eng.sign_wait(h)[0], alone[0][0])
+
+
+def test_key_cache_across_calls(oracle, monkeypatch):
+    """SignPrecomp kept across calls (scheme.hpp:106-125): a two-entry cache is hit, missed and
+    evicted; outputs never change; a malformed shared key is refused before any work."""
+    from paper_2211_12265_b200 import Engine
+    monkeypatch.setenv("DLB_KEY_CACHE", "2")
+    e = Engine(0)
+    try:
+        rng = mt19937_64(2718)
+        level = 3
+        keys = [oracle.keygen(level, rng.bytes(32)) for _ in range(4)]
+        msgs = [rng.bytes(40) for _ in range(50)]
+        want = {k: [oracle.sign(level, keys[k][1], m)[0] for m in msgs[:6]] for k in range(4)}
+        for k in (0, 1, 0, 2, 3, 1, 0, 0, 3):
+            sigs = e.batch_sign(level, np.frombuffer(keys[k][1], np.uint8), msgs)
+            assert [sigs[i].tobytes() for i in range(6)] == want[k]
+        bad = bytearray(keys[0][1])
+        bad[64 + 32] = 0xFF  # an eta field out of range (packing.hpp:79-86)
+        with pytest.raises(ValueError):
+            e.batch_sign(level, np.frombuffer(bytes(bad), np.uint8), msgs)
+        with pytest.raises(ValueError):
+            e.sign_submit(level, np.frombuffer(bytes(bad), np.uint8), msgs)
+    finally:
+        e.close()
+    monkeypatch.setenv("DLB_KEY_CACHE", "0")  # cache off: the per-call path
+    e = Engine(0)
+    try:
+        sigs = e.batch_sign(level, np.frombuffer(keys[2][1], np.uint8), msgs)
+        assert [sigs[i].tobytes() for i in range(6)] == want[2]
+    finally:
+        e.close()
