@@ -3,14 +3,17 @@
 
 Contract (driver):  python bench.py --gpus N --steps K --warmup W   (torchrun for N>1)
 prints ONE JSON line on rank 0.  A step is one pass of the hot path over one batch of
-synthetic input on every GPU: the paper's headline shape, 10 in-flight batches of 10,000
-sign tasks = 100,000 tasks per GPU per step, one shared key, 32-byte messages,
-deterministic signing (BASELINE.json configs[1]).
+synthetic input on every GPU: ONE batch of 100,000 Dilithium2 sign tasks (the task count of
+the paper's headline shape, 10 in-flight batches of 10,000), one shared key,
+32-byte messages, deterministic signing (BASELINE.json configs[1]).  Steps are submitted through
+dlb_sign_submit[_dev] / dlb_sign_wait with up to --depth (6) steps in flight, the way the paper
+keeps batches in flight; every step is a separate batch with its own output buffers.
 
-  value     whole-job signatures/s with inputs resident in HBM (CUDA events)
-  e2e       the same through the host-buffer C ABI (dlb_sign_batch): pinned host memory,
-            H2D of messages and D2H of signatures inside the timed region
-  ops       verify / keygen numbers measured the same way + batch-10k latencies
+  value     whole-job signatures/s with inputs resident in HBM (CUDA events around K steps)
+  e2e       the same through the host-buffer C ABI (dlb_sign_submit / dlb_sign_wait): pinned
+            host memory, H2D of messages and D2H of signatures inside the timed region
+  ops       one-synchronous-call-per-step numbers, ten 10k batches in flight, the C++ shim,
+            verify / keygen measured the same way + batch-10k latencies
   roofline  the dominant kernel (k_sign_persistent) against the INT32 issue rate
             measured live on this GPU (dlb_measure_int32_peak), plus the HBM view
   cpu_baseline  the unmodified reference (oracle/_ref) timed on this box's host cores
@@ -230,16 +233,56 @@ def run_reference(args, dist):
 
 
 def workload_config(args):
-    return {"workload": "Dilithium2 batch sign: 10 in-flight batches x 10,000 = %d tasks per GPU per "
-                        "step, one shared key, 32-byte messages, deterministic signing (paper headline "
-                        "shape); verify/keygen/batch-10k latency reported under 'ops'" % args.tasks,
-            "level": LEVEL, "tasks_per_gpu_per_step": args.tasks,
+    return {"workload": "Dilithium2 batch sign: one batch of %d tasks per GPU per step (the task count of "
+                        "the paper's 10 in-flight batches x 10,000), up to %d steps in flight through "
+                        "dlb_sign_submit / dlb_sign_wait, one shared key, 32-byte messages, deterministic "
+                        "signing; ten separate 10k batches in flight, one synchronous call per step, "
+                        "verify / keygen / batch-10k latency under 'ops'" % (args.tasks, args.depth),
+            "level": LEVEL, "tasks_per_gpu_per_step": args.tasks, "steps_in_flight": args.depth,
             "l2": "inputs larger than L2: each step streams %.0f MB of signatures plus ~0.7 GB of "
                   "scheduler scratch through the 126 MB L2" % (args.tasks * 2420 / 1e6)}
 
 
 
-def other_level_numbers(eng, torch, dev, level, n, steps, rank):
+class SignPipe:
+    """K steps of one batch each through dlb_sign_submit[_dev] / dlb_sign_wait with up to `depth`
+    steps in flight.  Every step in flight has its own output buffers (ring of `depth`)."""
+
+    def __init__(self, eng, level, n, depth, sk_ptr, msgs_ptr, off_ptr, sig_ptrs, att_ptrs, fail_ptrs, dev):
+        from paper_2211_12265_b200.engine import SignStats
+        self.eng, self.level, self.n, self.depth = eng, level, n, depth
+        self.args = (sk_ptr, msgs_ptr, off_ptr)
+        self.outs = list(zip(sig_ptrs, att_ptrs, fail_ptrs))
+        self.fn = eng.lib.dlb_sign_submit_dev if dev else eng.lib.dlb_sign_submit
+        self.SignStats = SignStats
+        self.tot = {"attempts": 0, "speculative": 0, "accepted_attempt_sum": 0, "failed_tasks": 0}
+        self.launches = 0
+
+    def run(self, steps):
+        lib, ctx = self.eng.lib, self.eng.ctx
+        sk, msgs, off = self.args
+        inflight = []
+        for i in range(steps):
+            if len(inflight) >= self.depth:
+                self._wait(inflight.pop(0))
+            sig, att, fail = self.outs[i % self.depth]
+            t = C.c_uint64(0)
+            rc = self.fn(ctx, self.level, 0, sk, 0, self.n, None, msgs, off, None, 0, 1, sig, att, fail, C.byref(t))
+            assert rc == 0, rc
+            self.launches += self.eng.last_launches
+            inflight.append(t.value)
+        for t in inflight:
+            self._wait(t)
+
+    def _wait(self, ticket):
+        st = self.SignStats()
+        rc = self.eng.lib.dlb_sign_wait(self.eng.ctx, ticket, C.byref(st))
+        assert rc == 0, rc
+        for k in self.tot:
+            self.tot[k] += getattr(st, k)
+
+
+def other_level_numbers(eng, torch, dev, level, n, steps, rank, depth):
     """configs[2] / configs[3]: Dilithium3 / Dilithium5 keygen, sign, verify throughput with
     inputs resident in HBM (same step shape as the headline), plus host->host batch-10k
     latency.  Single GPU numbers (per rank); reported under ops.levels."""
@@ -288,6 +331,26 @@ def other_level_numbers(eng, torch, dev, level, n, steps, rank):
         out[name] = {"value": n / (ms * 1e-3), "unit": "ops/s", "ms_per_step": ms, "int32_ops_per_unit": work}
     assert bool(d_flags.all().item()) and bool((d_fail == 0).all().item())
     out["sign"]["attempts_per_sig"] = st.accepted_attempt_sum / n
+    # the same step shape with up to `depth` steps in flight (the headline's mode)
+    ring = [(torch.zeros((n, sgb), dtype=torch.uint8, device=dev), torch.zeros(n, dtype=torch.int32, device=dev),
+             torch.zeros(n, dtype=torch.uint8, device=dev)) for _ in range(depth)]
+    pipe = SignPipe(eng, level, n, depth, p(d_sk), p(d_msgs), p(d_off), [p(r[0]) for r in ring],
+                    [p(r[1]) for r in ring], [p(r[2]) for r in ring], dev=True)
+    pipe.run(depth)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ksteps = max(4 * depth, steps)
+    e0.record()
+    pipe.run(ksteps)
+    torch.cuda.synchronize()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / ksteps
+    out["sign"]["sync"] = {"value": out["sign"]["value"], "ms_per_step": out["sign"]["ms_per_step"]}
+    out["sign"]["value"] = n / (ms * 1e-3)
+    out["sign"]["ms_per_step"] = ms
+    out["sign"]["steps_in_flight"] = depth
+    assert torch.equal(ring[0][0], d_sigs), "in-flight and synchronous signatures differ"
     # host -> host batch-10k latency
     m = 10000
     h_m = torch.from_numpy(msgs[:m].copy()).pin_memory()
@@ -319,63 +382,47 @@ def other_level_numbers(eng, torch, dev, level, n, steps, rank):
     assert bool(h_fl.all().item())
     return out
 
-def streamed_sign(torch, dist, dev_index, level, sk, msgs, off, chunk, lanes, steps_total):
-    """configs[4]: a long task stream cut into chunks that flow through `lanes` engine contexts
-    of one GPU, each driven by its own host thread through the host-buffer C ABI (pinned
-    buffers, H2D/D2H inside the timed region).  While one context's persistent kernel drains
-    its rejection-loop tail, the other context's next chunk fills the freed SMs, and its
-    signatures stream back over PCIe meanwhile -- the multi-stream overlap of PAPER.md:710-721.
-    Returns (ops/s over all ranks, sample of (message index, signature) for parity)."""
-    from paper_2211_12265_b200 import Engine, LEVELS
+def streamed_sign(torch, dist, eng, level, sk, msgs, off, chunk, depth, reps):
+    """configs[4]: a long task stream cut into chunks that flow through ONE engine context as
+    batches in flight (dlb_sign_submit / dlb_sign_wait, pinned buffers in and out, H2D / D2H inside
+    the timed region): while the rejection-loop tail of one chunk drains, the scheduler is already
+    claiming tasks of the next chunks, and finished signatures stream back over PCIe meanwhile --
+    the multi-stream overlap of PAPER.md:710-721.  Returns (ops/s over all ranks, parity sample)."""
+    from paper_2211_12265_b200 import LEVELS
     sgb = LEVELS[level][4]
     n_total = len(msgs)
     chunks = [(lo, min(lo + chunk, n_total)) for lo in range(0, n_total, chunk)]
-    engs = [Engine(dev_index) for _ in range(lanes)]
     h_msgs = torch.from_numpy(msgs).pin_memory()
     h_sk = torch.from_numpy(np.ascontiguousarray(sk)).pin_memory()
     h_off = [torch.from_numpy((off[lo:hi + 1] - off[lo]).astype(np.int64)).pin_memory() for lo, hi in chunks]
-    h_sigs = [torch.zeros((chunk, sgb), dtype=torch.uint8).pin_memory() for _ in range(lanes)]
-    u8 = lambda t, o=0: C.cast(C.c_void_p(t.data_ptr() + o), C.POINTER(C.c_uint8))
-    u64 = lambda t: C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_uint64))
-    errs = []
+    h_sigs = torch.zeros((n_total, sgb), dtype=torch.uint8).pin_memory()
+    vp = lambda t, o=0: C.c_void_p(t.data_ptr() + o)
+    lib, ctx = eng.lib, eng.ctx
 
-    def worker(lane, reps):
-        e = engs[lane]
-        for _ in range(reps):
-            for ci in range(lane, len(chunks), lanes):
-                lo, hi = chunks[ci]
-                rc = e.lib.dlb_sign_batch(e.ctx, level, hi - lo, u8(h_sk), 0, u8(h_msgs, int(off[lo])),
-                                          u64(h_off[ci]), None, 0, 1, u8(h_sigs[lane]), None, None, None)
-                if rc != 0:
-                    errs.append(rc)
-                    return
+    def run():
+        inflight = []
+        for ci, (lo, hi) in enumerate(chunks):
+            if len(inflight) >= depth:
+                assert lib.dlb_sign_wait(ctx, inflight.pop(0), None) == 0
+            t = C.c_uint64(0)
+            rc = lib.dlb_sign_submit(ctx, level, 0, vp(h_sk), 0, hi - lo, None, vp(h_msgs, int(off[lo])),
+                                     vp(h_off[ci]), None, 0, 1, vp(h_sigs, lo * sgb), None, None, C.byref(t))
+            assert rc == 0, rc
+            inflight.append(t.value)
+        for t in inflight:
+            assert lib.dlb_sign_wait(ctx, t, None) == 0
 
-    def run(reps):
-        ts = [threading.Thread(target=worker, args=(l, reps)) for l in range(lanes)]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-
-    run(1)  # warm-up: arenas, pinned registrations, first-launch costs
+    run()  # warm-up: arenas, pinned registrations, first-launch costs
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
-    run(steps_total)
+    for _ in range(reps):
+        run()
     torch.cuda.synchronize()
     t = dist.max(time.perf_counter() - t0)
     dist.barrier()
-    assert not errs, errs
-    # parity sample: the last chunk each lane signed
-    sample = []
-    for lane in range(lanes):
-        last = [ci for ci in range(lane, len(chunks), lanes)][-1]
-        lo, hi = chunks[last]
-        for i in range(0, hi - lo, max(1, (hi - lo) // 64)):
-            sample.append((lo + i, h_sigs[lane][i].numpy().tobytes()))
-    for e in engs:
-        e.close()
-    return dist.world * n_total * steps_total / t, sample
+    sample = [(i, h_sigs[i].numpy().tobytes()) for i in range(0, n_total, max(1, n_total // 24))]
+    return dist.world * n_total * reps / t, sample
 
 
 # ----------------------------------------------------------------------------------------
@@ -387,8 +434,14 @@ def run_ours(args, dist):
     dev_index = dist.local
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
+    # this rank's host thread (and every pinned buffer it allocates from here on) goes to the
+    # NUMA node of its GPU: with 8 ranks the host side is the shared resource
+    from paper_2211_12265_b200 import load_library
+    numa_bound = load_library().dlb_bind_thread_to_device(dev_index) == 0
+    numa_node = load_library().dlb_device_numa_node(dev_index)
     eng = Engine(dev_index)  # raises if the CUDA library is missing: no fallback
     lib, ctx = eng.lib, eng.ctx
+    D = max(1, args.depth)
     k, l, pkb, skb, sgb = LEVELS[LEVEL]
     n = args.tasks
     K, W = args.steps, max(args.warmup, 0)
@@ -462,13 +515,41 @@ def run_ours(args, dist):
         ms = dist.max(e0.elapsed_time(e1))
         return ms, launches, main_ms / max(steps, 1)
 
+    # ---- headline: sign, inputs resident in HBM, up to D steps in flight ---------------------
+    ring = [(torch.zeros((n, sgb), dtype=torch.uint8, device=dev), torch.zeros(n, dtype=torch.int32, device=dev),
+             torch.zeros(n, dtype=torch.uint8, device=dev)) for _ in range(D)]
+    pipe = SignPipe(eng, LEVEL, n, D, p(d_sk), p(d_msgs), p(d_off), [p(r[0]) for r in ring],
+                    [p(r[1]) for r in ring], [p(r[2]) for r in ring], dev=True)
+
+    def timed_pipe(pp, steps, warm):
+        """K steps between barrier+synchronize on both sides, CUDA events, max over ranks."""
+        pp.run(max(warm, D))
+        torch.cuda.synchronize()
+        dist.barrier()
+        for k in pp.tot:
+            pp.tot[k] = 0
+        pp.launches = 0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()  # the engine orders each submission behind this stream (dlb_set_stream)
+        pp.run(steps)
+        torch.cuda.synchronize()  # every scheduler kernel has exited
+        e1.record()
+        e1.synchronize()
+        dist.barrier()
+        return dist.max(e0.elapsed_time(e1))
+
     sampler = ClockSampler(dev_index)
     sampler.start()
-    # ---- headline: sign, inputs resident in HBM -------------------------------------------
-    ms_sign, launches, main_ms = timed(sign_dev, K, max(W, 3))
-    useful_attempts = stats.accepted_attempt_sum / n
-    executed_attempts = stats.attempts / n
+    ms_sign = timed_pipe(pipe, K, max(W, 3))
+    launches = pipe.launches
+    useful_attempts = pipe.tot["accepted_attempt_sum"] / (n * K)
+    executed_attempts = pipe.tot["attempts"] / (n * K)
+    spec_share = pipe.tot["speculative"] / max(1, pipe.tot["attempts"])
+    assert pipe.tot["failed_tasks"] == 0 and all(bool((r[2] == 0).all().item()) for r in ring)
+    # one synchronous call per step (round 1's headline mode), for continuity
+    ms_sign_sync, _, main_ms_sync = timed(sign_dev, K, max(W, 3))
     assert bool((d_fail == 0).all().item())
+    assert all(torch.equal(r[0], d_sigs) for r in ring), "in-flight and synchronous signatures differ"
     ms_ver, l_ver, _ = timed(lambda: verify_dev(False), K, max(W, 3))
     assert bool(d_flags.all().item()), "device verify rejected a device signature"
     ms_ver_sh, _, _ = timed(lambda: verify_dev(True), K, max(W, 3))
@@ -477,6 +558,7 @@ def run_ours(args, dist):
 
     world = dist.world
     value = world * n * K / (ms_sign * 1e-3)
+    sync_value = world * n * K / (ms_sign_sync * 1e-3)
     ver_value = world * n * K / (ms_ver * 1e-3)
     ver_sh_value = world * n * K / (ms_ver_sh * 1e-3)
     kg_value = world * n * K / (ms_kg * 1e-3)
@@ -501,6 +583,11 @@ def run_ours(args, dist):
                                 u8(h_sigs), None, None, None)
         assert rc == 0, rc
 
+    vp = lambda t, o=0: C.c_void_p(t.data_ptr() + o)
+    h_ring = [torch.zeros((n, sgb), dtype=torch.uint8).pin_memory() for _ in range(D)]
+    hpipe = SignPipe(eng, LEVEL, n, D, vp(h_sk), vp(h_msgs), vp(h_off), [vp(t) for t in h_ring],
+                     [None] * D, [None] * D, dev=False)
+
     def verify_host(cnt=n):
         rc = lib.dlb_verify_batch(ctx, LEVEL, cnt, u8(h_pk_rep), pkb, u8(h_msgs), u64(h_off), u8(h_sigs),
                                   u8(h_flags))
@@ -523,12 +610,15 @@ def run_ours(args, dist):
         dist.barrier()
         return dist.max(t)
 
-    t_e2e_sign = timed_host(sign_host, K, 3)
+    t_e2e_sign = timed_host(lambda: hpipe.run(K), 1, 1)
+    assert all(torch.equal(t, h_ring[0]) for t in h_ring)
+    t_e2e_sign_sync = timed_host(sign_host, K, 3)
     t_e2e_ver = timed_host(verify_host, K, 3)
     assert bool(h_flags.all().item())
-    assert torch.equal(h_sigs, d_sigs.cpu()), "e2e and device-resident signatures differ"
+    assert torch.equal(h_sigs, d_sigs.cpu()) and torch.equal(h_ring[0], h_sigs), "e2e and device-resident signatures differ"
     t_e2e_kg = timed_host(keygen_host, K, 3)
     e2e_sign = world * n * K / t_e2e_sign
+    e2e_sign_sync = world * n * K / t_e2e_sign_sync
     e2e_ver = world * n * K / t_e2e_ver
     e2e_kg = world * n * K / t_e2e_kg
 
@@ -545,12 +635,65 @@ def run_ours(args, dist):
 
     lat_sign, lat_ver, lat_kg = lat(sign_host), lat(verify_host), lat(keygen_host)
 
+    # ten independent 10,000-task batches submitted back to back, host buffers in and out
+    # (the paper's literal shape; tools/dilithium_cli.cpp:309-345)
+    def ten_in_flight():
+        ts = []
+        for b in range(10):
+            t = C.c_uint64(0)
+            rc = lib.dlb_sign_submit(ctx, LEVEL, 0, vp(h_sk), 0, 10000, None, vp(h_msgs, 320000 * b), vp(h_off),
+                                     None, 0, 1, vp(h_sigs, 10000 * sgb * b), None, None, C.byref(t))
+            assert rc == 0, rc
+            ts.append(t.value)
+        for t in ts:
+            assert lib.dlb_sign_wait(ctx, t, None) == 0
+
+    def ten_sequential():
+        for b in range(10):
+            rc = lib.dlb_sign_batch(ctx, LEVEL, 10000, u8(h_sk), 0,
+                                    C.cast(vp(h_msgs, 320000 * b), C.POINTER(C.c_uint8)), u64(h_off), None, 0, 1,
+                                    C.cast(vp(h_sigs, 10000 * sgb * b), C.POINTER(C.c_uint8)), None, None, None)
+            assert rc == 0, rc
+
+    def med_ms(fn, reps=11):
+        for _ in range(3):
+            fn()
+        xs = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            xs.append((time.perf_counter() - t0) * 1e3)
+        return float(np.median(xs))
+
+    ten = None
+    if n >= 100000:
+        h_sigs.zero_()
+        ms10 = med_ms(ten_in_flight)
+        assert torch.equal(h_sigs[:100000], h_ring[0][:100000]), "ten batches in flight: bytes differ"
+        ms10_seq = med_ms(ten_sequential)
+        ten = {"value": 100000 / ms10 * 1e3, "unit": "ops/s", "ms_all_ten": ms10,
+               "sequential": {"value": 100000 / ms10_seq * 1e3, "ms_all_ten": ms10_seq},
+               "note": "ten independent 10,000-task batches, dlb_sign_submit x 10 then dlb_sign_wait x 10, pinned "
+                       "host buffers in and out, median of 11; sequential = ten dlb_sign_batch calls"}
+
+    # the drop-in C++ API (include/dilithium_b200/api.hpp), std::vector in and out
+    shim = None
+    if dist.rank == 0 and not args.no_shim:
+        exe = os.path.join(ROOT, "tools", "bench_shim")
+        if os.path.exists(exe):
+            try:
+                r = subprocess.run([exe, str(LEVEL), "7"], capture_output=True, text=True, timeout=300)
+                shim = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {"error": r.stderr[-300:]}
+            except Exception as ex:  # the leg is informative; the headline does not depend on it
+                shim = {"error": repr(ex)}
+    dist.barrier()
+
     levels = None
     if not args.no_levels and world == 1:
         eng.set_stream(side.cuda_stream)
         levels = {}
         for lv in (3, 5, 44, 65, 87):  # configs[2], configs[3]; 44/65/87 = ML-DSA (FIPS 204 mode)
-            r = other_level_numbers(eng, torch, dev, lv, n, max(2, K // 2), dist.rank)
+            r = other_level_numbers(eng, torch, dev, lv, n, max(2, K // 2), dist.rank, args.depth)
             for op in ("sign", "verify", "keygen"):
                 r[op]["roofline_frac"] = r[op]["value"] * r[op]["int32_ops_per_unit"] / 1e12 / peaks["lop3"]
             levels[str(lv)] = r
@@ -563,24 +706,27 @@ def run_ours(args, dist):
         # (numpy's PCG64 here: the byte-per-draw mt19937_64 of make_inputs is a Python loop)
         s_msgs = np.random.default_rng(5150 + dist.rank).integers(0, 256, (n_stream, 32), dtype=np.uint8)
         s_off = np.arange(n_stream + 1, dtype=np.uint64) * 32
-        sv, sample = streamed_sign(torch, dist, dev_index, LEVEL, sk1[0], s_msgs, s_off, n, 2, 1)
-        sv1, _ = streamed_sign(torch, dist, dev_index, LEVEL, sk1[0], s_msgs, s_off, n, 1, 1)
+        sv, sample = streamed_sign(torch, dist, eng, LEVEL, sk1[0], s_msgs, s_off, n, D, 1)
+        sv1, _ = streamed_sign(torch, dist, eng, LEVEL, sk1[0], s_msgs, s_off, n, 1, 1)
         if dist.rank == 0:
             from tests.cpu_checkers import load_oracle
             oracle = load_oracle()
-            for idx, sig in sample[::8]:
+            for idx, sig in sample:
                 assert oracle.sign(LEVEL, sk1[0].tobytes(), s_msgs[idx].tobytes())[0] == sig, "streamed parity"
-        streamed = {"value": sv, "unit": "ops/s", "tasks": n_stream * world, "chunk": n, "contexts_per_gpu": 2,
-                    "one_context": sv1,
-                    "note": "host pinned buffers in/out through dlb_sign_batch (signatures land in the caller's "
-                            "pinned buffer straight from the kernel's commit step), chunks alternate over two "
-                            "engine contexts driven by two host threads; one_context = the same stream through "
-                            "a single context; %d sampled signatures equal the CPU oracle's" % len(sample[::8])}
+        streamed = {"value": sv, "unit": "ops/s", "tasks": n_stream * world, "chunk": n, "chunks_in_flight": D,
+                    "one_at_a_time": sv1,
+                    "note": "host pinned buffers in/out, one engine context, chunks submitted with "
+                            "dlb_sign_submit and waited in order (signatures land in the caller's pinned buffer "
+                            "straight from the kernel's commit step); one_at_a_time = the same stream with "
+                            "one chunk in flight; %d sampled signatures equal the CPU oracle's" % len(sample)}
 
     # ---- roofline of the dominant kernel -------------------------------------------------
     wk = WORK[LEVEL]
     w_attempt = int_ops(wk["attempt"])
     ops_per_launch = n * useful_attempts * w_attempt  # useful work only; speculation = overhead
+    # one launch per step; launches of consecutive steps overlap (batches in flight), so the
+    # per-launch duration that throughput follows is the timed region divided by its K launches
+    main_ms = ms_sign / K
     achieved = ops_per_launch / (main_ms * 1e-3) / 1e12
     peak_single = peaks["lop3"]
     peaks_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -603,21 +749,24 @@ def run_ours(args, dist):
         "peak_src": "measured live: LOP3 issue rate (alu pipe), dlb_measure_int32_peak",
         "peak_dual_pipe": peaks["lop3_imad_mix"], "frac_dual_pipe": achieved / peaks["lop3_imad_mix"],
         "traffic": traffic, "traffic_note": traffic_note, "launch_ms": main_ms,
+        "launch_ms_note": "timed region / K launches (steps in flight overlap); one synchronous launch alone: "
+                          "%.3f ms = frac %.3f" % (main_ms_sync, ops_per_launch / (main_ms_sync * 1e-3) / 1e12 / peak_single),
         "model": {"int32_ops_per_attempt": w_attempt, "useful_attempts_per_sig": useful_attempts,
-                  "executed_attempts_per_sig": executed_attempts},
+                  "executed_attempts_per_sig": executed_attempts, "speculative_share": spec_share},
         "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_achieved / hbm_peak,
                 "peak_src": hbm_src, "algorithmic_bytes_per_sig": wk["bytes"]["sign"]},
         "per_op_frac": {
             "keygen": kg_value / world * int_ops(wk["keygen"]) / 1e12 / peak_single,
             "verify": ver_value / world * int_ops(wk["verify"]) / 1e12 / peak_single,
             "sign_whole_call": value / world * (useful_attempts * w_attempt + 2 * W_PERM) / 1e12 / peak_single,
+            "sign_sync_call": sync_value / world * (useful_attempts * w_attempt + 2 * W_PERM) / 1e12 / peak_single,
         },
         "int32_peaks_measured": peaks,
     }
 
     # ---- CPU baseline on this box's host cores (rank 0, N == 1 only) ---------------------
     cpu = None
-    if dist.rank == 0 and world == 1 and not args.no_cpu:
+    if dist.rank == 0 and not args.no_cpu:  # once, on rank 0, at every N
         cpu = cpu_baseline(sk1[0], pk1[0], msgs, off)
 
     if dist.rank == 0:
@@ -628,12 +777,25 @@ def run_ours(args, dist):
             "vs_baseline_note": "value / 574,953 (paper's A100 D2 sign/s, BASELINE.md 1.1; other hardware)",
             "dtype": "int32", "data": "synthetic", "config": workload_config(args),
             "e2e": {"value": e2e_sign, "unit": "ops/s", "h2d_bytes_per_step": int(n * 32 + (n + 1) * 8 + skb),
-                    "d2h_bytes_per_step": int(n * sgb)},
+                    "d2h_bytes_per_step": int(n * sgb), "steps_in_flight": D,
+                    "pcie_gbs_per_gpu": e2e_sign / world * (n * 32 + (n + 1) * 8 + n * sgb) / n / 1e9},
+            "host": {"numa_bound": bool(numa_bound), "numa_node": int(numa_node),
+                     "host_dram_gbs_all_gpus": {"sign": e2e_sign * (32 + 8 + sgb) / 1e9,
+                                                "verify": e2e_ver * (32 + 8 + sgb + pkb) / 1e9,
+                                                "keygen": e2e_kg * (32 + pkb + skb) / 1e9},
+                     "note": "bytes the host memory system moves per second for the e2e legs (pinned buffers, "
+                             "one DMA pass); rank-local NUMA placement via dlb_bind_thread_to_device"},
             "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline,
             "cpu_baseline": cpu,
             "ops": {
-                "sign": {"value": value, "e2e": e2e_sign, "unit": "ops/s",
-                         "attempts_per_sig": useful_attempts, "executed_attempts_per_sig": executed_attempts},
+                "sign": {"value": value, "e2e": e2e_sign, "unit": "ops/s", "steps_in_flight": D,
+                         "attempts_per_sig": useful_attempts, "executed_attempts_per_sig": executed_attempts,
+                         "speculative_share": spec_share,
+                         "sync": {"value": sync_value, "e2e": e2e_sign_sync, "ms_per_step": ms_sign_sync / K,
+                                  "kernel_ms": main_ms_sync,
+                                  "note": "one synchronous dlb_sign_batch[_dev] call per step (round 1's mode)"}},
+                "sign_10x10k_inflight": ten,
+                "shim": shim,
                 "verify": {"value": ver_value, "e2e": e2e_ver, "unit": "ops/s", "ms_per_step": ms_ver / K,
                            "note": "one public key per task (no key sharing assumed): 99 permutations/op",
                            "gpu_launches": int(l_ver)},
@@ -689,10 +851,12 @@ def cpu_baseline(sk, pk, msgs, off):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tasks", type=int, default=100000, help="tasks per GPU per step")
+    ap.add_argument("--depth", type=int, default=6, help="steps (batches) in flight")
+    ap.add_argument("--no-shim", action="store_true", help="skip the C++ shim leg (tools/bench_shim)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-levels", action="store_true", help="skip the Dilithium3/5 extras")
     ap.add_argument("--no-stream", action="store_true", help="skip the streamed 1M-task leg (configs[4])")

@@ -32,6 +32,9 @@
 #pragma once
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -45,6 +48,8 @@
 #include <utility>
 #include <unordered_map>
 #include <vector>
+
+#include <sys/mman.h>
 
 #include "../dilithium_b200.h"
 
@@ -124,6 +129,18 @@ template <Params P> using SkBytes = std::array<uint8_t, P.sk_bytes()>;
 template <Params P> using SigBytes = std::array<uint8_t, P.sig_bytes()>;
 using SeedArray = std::array<uint8_t, kSeedBytes>;
 using CrhArray = std::array<uint8_t, kCrhBytes>;
+
+// DLB_SHIM_PROF=1: host-side phase times of the batch calls on stderr (where does a call's time go)
+struct ShimProf {
+  bool on = std::getenv("DLB_SHIM_PROF") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[shim] %-18s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 inline void check(int rc, const char* what) {
   if (rc != 0) throw std::runtime_error(std::string(what) + " failed: status " + std::to_string(rc));
@@ -293,6 +310,50 @@ struct AttemptResult {  // scheme.hpp:36-43
 
 namespace detail {
 
+// Result vectors of a large batch are tens to hundreds of MB of fresh memory: with 4 KB pages the
+// first touch (one page fault per 4 KB) costs more than the GPU work.  Ask for huge pages where
+// the kernel offers them on request (transparent_hugepage = madvise); a no-op elsewhere.
+inline void advise_huge(void* p, size_t bytes) {
+#ifdef MADV_HUGEPAGE
+  constexpr uintptr_t kHuge = 2u << 20;
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + kHuge - 1) & ~(kHuge - 1);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes) & ~(kHuge - 1);
+  if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+#else
+  (void)p;
+  (void)bytes;
+#endif
+}
+
+// fn(lo, hi) over [0, n) on up to `threads` host threads (the caller's included)
+template <class Fn>
+void parallel_ranges(size_t n, size_t threads, size_t min_per_thread, Fn&& fn) {
+  size_t t = std::min(threads, std::max<size_t>(1, n / std::max<size_t>(1, min_per_thread)));
+  if (t <= 1) {
+    fn(size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (size_t i = 1; i < t; ++i) pool.emplace_back([&fn, n, t, i] { fn(n * i / t, n * (i + 1) / t); });
+  fn(size_t{0}, n / t);
+  for (auto& th : pool) th.join();
+}
+
+// First touch of a fresh allocation on several threads (one write per 4 KB page): the page faults
+// -- the dominant cost of a result vector of hundreds of MB -- then run in parallel instead of inside
+// the single-threaded element construction that follows.
+inline void prefault(void* p, size_t bytes, size_t threads) {
+  auto* base = static_cast<volatile uint8_t*>(p);
+  parallel_ranges((bytes + 4095) / 4096, threads, 2048, [&](size_t lo, size_t hi) {
+    for (size_t pg = lo; pg < hi; ++pg) base[pg * 4096] = 0;
+  });
+}
+
+inline size_t copy_threads() {
+  const size_t hw = std::thread::hardware_concurrency();
+  return std::clamp<size_t>(hw / 2, 1, 8);
+}
+
 // messages of jobs[lo, hi) back to back in `flat` (pinned), offsets relative to the part
 template <class Jobs>
 void flatten_messages(const Jobs& jobs, size_t lo, size_t hi, uint8_t* flat, uint64_t* off) {
@@ -380,8 +441,8 @@ CrhArray deterministic_rho_prime(const SignPrecomp<P>& pre, const CrhArray& mu, 
   return rp;
 }
 
-// batch.hpp:159-166.  The batch is cut into parts; while the device generates part i + 1 a
-// helper thread moves part i from the pinned staging into the result vector.
+// batch.hpp:159-166.  The batch is cut into parts; while the device generates part i + 1
+// helper threads move part i from the pinned staging into the result vector.
 template <Params P>
 std::vector<std::pair<PkBytes<P>, SkBytes<P>>> batch_keygen(std::span<const SeedArray> zetas,
                                                             size_t /*workers*/ = 1,
@@ -390,7 +451,12 @@ std::vector<std::pair<PkBytes<P>, SkBytes<P>>> batch_keygen(std::span<const Seed
   const size_t n = zetas.size();
   std::vector<KeyPair> out;
   if (n == 0) return out;
+  ShimProf prof;
   out.reserve(n);
+  detail::advise_huge(out.data(), n * sizeof(KeyPair));
+  detail::prefault(out.data(), n * sizeof(KeyPair), detail::copy_threads());
+  out.resize(n);
+  prof.mark("keygen: result");
   constexpr size_t kPart = 16384;
   const size_t part = std::min(n, kPart);
   uint8_t* pk_stage[2] = {eng.out_a.get(2 * part * P.pk_bytes()), nullptr};
@@ -399,13 +465,15 @@ std::vector<std::pair<PkBytes<P>, SkBytes<P>>> batch_keygen(std::span<const Seed
   sk_stage[1] = sk_stage[0] + part * P.sk_bytes();
   uint8_t* zin = eng.in_a.get(n * kSeedBytes);
   std::memcpy(zin, zetas.data()->data(), n * kSeedBytes);
+  const size_t threads = detail::copy_threads();
   std::thread mover;
-  auto move_part = [&out](const uint8_t* pks, const uint8_t* sks, size_t cnt) {
-    for (size_t i = 0; i < cnt; ++i) {
-      KeyPair& kp = out.emplace_back();  // capacity reserved: no reallocation
-      std::memcpy(kp.first.data(), pks + i * P.pk_bytes(), P.pk_bytes());
-      std::memcpy(kp.second.data(), sks + i * P.sk_bytes(), P.sk_bytes());
-    }
+  auto move_part = [&out, threads](const uint8_t* pks, const uint8_t* sks, size_t lo, size_t cnt) {
+    detail::parallel_ranges(cnt, threads, 512, [&](size_t a, size_t b) {
+      for (size_t i = a; i < b; ++i) {
+        std::memcpy(out[lo + i].first.data(), pks + i * P.pk_bytes(), P.pk_bytes());
+        std::memcpy(out[lo + i].second.data(), sks + i * P.sk_bytes(), P.sk_bytes());
+      }
+    });
   };
   size_t pi = 0;
   for (size_t lo = 0; lo < n; lo += part, ++pi) {
@@ -414,24 +482,30 @@ std::vector<std::pair<PkBytes<P>, SkBytes<P>>> batch_keygen(std::span<const Seed
     const int rc = dlb_keygen_batch(eng.ctx(), P.level, cnt, zin + lo * kSeedBytes, pk_stage[b], sk_stage[b]);
     if (mover.joinable()) mover.join();  // part pi - 1 is in place; its buffer (b ^ 1) is free again
     check(rc, "dlb_keygen_batch");
-    mover = std::thread(move_part, pk_stage[b], sk_stage[b], cnt);
+    mover = std::thread(move_part, pk_stage[b], sk_stage[b], lo, cnt);
   }
   if (mover.joinable()) mover.join();
+  prof.mark("keygen: device+move");
   return out;
 }
 
 // batch.hpp:53-137.  rho_prime_override: nullptr (deterministic signing), or ONE rho' used
 // for every task (the reference's sign_with_precomp argument), or -- rho_prime_per_task --
 // one rho' per task.
+//
+// batch_sign_into (an extension) writes into storage the caller provides instead of returning a
+// fresh vector: with `into` in pinned memory (dlb_host_alloc) the device stores the signatures
+// there directly and no host copy is left on the path.
+namespace detail {
 template <Params P>
-std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const BatchConfig& cfg = {},
-                                    BatchStats* stats = nullptr, Engine& eng = Engine::instance(),
-                                    const CrhArray* rho_prime_override = nullptr,
-                                    std::vector<uint32_t>* attempts_out = nullptr,
-                                    std::span<const CrhArray> rho_prime_per_task = {}) {
+std::vector<SigBytes<P>> batch_sign_impl(std::span<const SignJob<P>> jobs, const BatchConfig& cfg,
+                                         BatchStats* stats, Engine& eng, const CrhArray* rho_prime_override,
+                                         std::vector<uint32_t>* attempts_out,
+                                         std::span<const CrhArray> rho_prime_per_task, SigBytes<P>* into) {
   const size_t n = jobs.size();
   std::vector<SigBytes<P>> out;
   if (n == 0) return out;
+  ShimProf prof;
   if (!rho_prime_per_task.empty() && rho_prime_per_task.size() != n)
     throw std::invalid_argument("batch_sign: one rho' per task expected");
   static_assert(sizeof(SigBytes<P>) == P.sig_bytes());
@@ -447,6 +521,7 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
     key_idx[i] = it->second;
   }
   const bool shared = keys.size() == 1;
+  prof.mark("sign: key table");
   uint8_t* skp = eng.in_a.get(keys.size() * P.sk_bytes());
   for (size_t k = 0; k < keys.size(); ++k) std::memcpy(skp + k * P.sk_bytes(), keys[k]->sk.data(), P.sk_bytes());
 
@@ -454,7 +529,7 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
   const bool logged = static_cast<bool>(cfg.trace) || static_cast<bool>(cfg.assignment_hook);
   size_t parts = (logged || cfg.psi != 0) ? 1 : std::min<size_t>(8, (n + 4095) / 4096);
   if (parts < 1) parts = 1;
-  const size_t total_msg = detail::message_bytes(jobs, 0, n);
+  const size_t total_msg = message_bytes(jobs, 0, n);
   uint8_t* flat = eng.in_b.get(total_msg + 8 * parts + 8);
   uint64_t* off = reinterpret_cast<uint64_t*>(eng.in_c.get((n + parts + 1) * 8));
   uint8_t* rp = nullptr;
@@ -464,7 +539,7 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
       std::memcpy(rp + i * kCrhBytes,
                   rho_prime_override ? rho_prime_override->data() : rho_prime_per_task[i].data(), kCrhBytes);
   }
-  uint8_t* sig_stage = eng.out_a.get(n * P.sig_bytes() + 8);
+  uint8_t* sig_stage = into ? reinterpret_cast<uint8_t*>(into) : eng.out_a.get(n * P.sig_bytes() + 8);
   uint32_t* att = reinterpret_cast<uint32_t*>(eng.out_b.get(n * 4));
   uint8_t* failed = eng.out_c.get(n);
 
@@ -472,6 +547,7 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
   if (cfg.trace) check(dlb_set_trace(eng.ctx(), cfg.trace_capacity), "dlb_set_trace");
   if (cfg.assignment_hook) check(dlb_set_assignment_log(eng.ctx(), acap), "dlb_set_assignment_log");
 
+  prof.mark("sign: staging");
   struct Part {
     size_t lo, hi;
     uint64_t ticket = 0;
@@ -483,7 +559,7 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
     ps[p].lo = n * p / parts;
     ps[p].hi = n * (p + 1) / parts;
     const size_t cnt = ps[p].hi - ps[p].lo;
-    detail::flatten_messages(jobs, ps[p].lo, ps[p].hi, flat + flat_pos, off + off_pos);
+    flatten_messages(jobs, ps[p].lo, ps[p].hi, flat + flat_pos, off + off_pos);
     rc = dlb_sign_submit(eng.ctx(), P.level, shared ? 0 : keys.size(), skp, shared ? 0 : P.sk_bytes(), cnt,
                          shared ? nullptr : key_idx.data() + ps[p].lo, flat + flat_pos, off + off_pos,
                          rp ? rp + ps[p].lo * kCrhBytes : nullptr, cfg.psi, cfg.speculate ? 1 : 0,
@@ -492,7 +568,13 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
     off_pos += cnt + 1;
     if (rc == 0) ++submitted;
   }
-  out.reserve(n);
+  prof.mark("sign: submit");
+  if (!into) {  // while the device signs: allocate the result and fault its pages in, in parallel
+    out.reserve(n);
+    advise_huge(out.data(), n * sizeof(SigBytes<P>));
+    prefault(out.data(), n * sizeof(SigBytes<P>), copy_threads());
+    prof.mark("sign: result pages");
+  }
   dlb_sign_stats total{};
   for (size_t p = 0; p < submitted; ++p) {
     dlb_sign_stats st{};
@@ -504,9 +586,11 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
     total.speculative += st.speculative;
     total.idle_slot_rounds += st.idle_slot_rounds;
     total.accepted_attempt_sum += st.accepted_attempt_sum;
+    if (into) continue;
     const auto* first = reinterpret_cast<const SigBytes<P>*>(sig_stage + ps[p].lo * P.sig_bytes());
     out.insert(out.end(), first, first + (ps[p].hi - ps[p].lo));  // while later parts still sign
   }
+  prof.mark("sign: wait+copy");
   if (cfg.trace) {
     std::vector<dlb_round_trace> recs(cfg.trace_capacity);
     const long long tot = rc == 0 ? dlb_get_trace(eng.ctx(), recs.data(), recs.size()) : 0;
@@ -542,6 +626,24 @@ std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const Batc
   if (attempts_out) attempts_out->assign(att, att + n);
   return out;
 }
+}  // namespace detail
+
+template <Params P>
+std::vector<SigBytes<P>> batch_sign(std::span<const SignJob<P>> jobs, const BatchConfig& cfg = {},
+                                    BatchStats* stats = nullptr, Engine& eng = Engine::instance(),
+                                    const CrhArray* rho_prime_override = nullptr,
+                                    std::vector<uint32_t>* attempts_out = nullptr,
+                                    std::span<const CrhArray> rho_prime_per_task = {}) {
+  return detail::batch_sign_impl<P>(jobs, cfg, stats, eng, rho_prime_override, attempts_out, rho_prime_per_task,
+                                    nullptr);
+}
+
+template <Params P>
+void batch_sign_into(std::span<const SignJob<P>> jobs, std::span<SigBytes<P>> into, const BatchConfig& cfg = {},
+                     BatchStats* stats = nullptr, Engine& eng = Engine::instance()) {
+  if (into.size() != jobs.size()) throw std::invalid_argument("batch_sign_into: one output slot per job");
+  detail::batch_sign_impl<P>(jobs, cfg, stats, eng, nullptr, nullptr, {}, into.data());
+}
 
 // batch.hpp:148-156; wrong-length pk/sig reject host-side (scheme.hpp:280-283)
 template <Params P>
@@ -574,12 +676,15 @@ std::vector<uint8_t> batch_verify(std::span<const VerifyJob<P>> jobs, size_t /*w
   uint8_t* sigs = eng.in_d.get(m * P.sig_bytes() + 8);
   uint8_t* f = eng.out_c.get(m);
   off[0] = 0;
-  for (size_t a = 0; a < m; ++a) {
-    const auto& j = jobs[live[a]];
-    std::memcpy(sigs + a * P.sig_bytes(), j.sig.data(), P.sig_bytes());
-    if (!j.message.empty()) std::memcpy(flat + off[a], j.message.data(), j.message.size());
-    off[a + 1] = off[a] + j.message.size();
-  }
+  for (size_t a = 0; a < m; ++a) off[a + 1] = off[a] + jobs[live[a]].message.size();
+  // gather the scattered job spans into the pinned staging on several host threads
+  detail::parallel_ranges(m, detail::copy_threads(), 1024, [&](size_t lo, size_t hi) {
+    for (size_t a = lo; a < hi; ++a) {
+      const auto& j = jobs[live[a]];
+      std::memcpy(sigs + a * P.sig_bytes(), j.sig.data(), P.sig_bytes());
+      if (!j.message.empty()) std::memcpy(flat + off[a], j.message.data(), j.message.size());
+    }
+  });
   if (keys.size() == 1)
     check(dlb_verify_batch(eng.ctx(), P.level, m, pks, 0, flat, off, sigs, f), "dlb_verify_batch");
   else
