@@ -199,11 +199,33 @@ __device__ __forceinline__ void ntt_inv(int32_t (&r)[8], int32_t* tile, const in
   __syncwarp();
 }
 
+// One warp copies nbytes (a multiple of 4) from a 4-byte aligned shared-memory buffer to a global
+// destination of ANY alignment with coalesced word stores (signatures are packed back to back and
+// their size is odd at levels 3 / 5).  Reads one word past the last full word of the source.
+__device__ __forceinline__ void warp_store_unaligned(uint8_t* dst, const uint32_t* src32, unsigned nbytes,
+                                                     int lane) {
+  const unsigned a = (unsigned)(reinterpret_cast<uintptr_t>(dst) & 3);
+  if (a == 0) {
+    uint32_t* g = reinterpret_cast<uint32_t*>(dst);
+    for (unsigned w = lane; w < nbytes / 4; w += 32) g[w] = src32[w];
+    return;
+  }
+  const unsigned head = 4 - a;  // bytes up to the next word boundary of the destination
+  const uint8_t* src8 = reinterpret_cast<const uint8_t*>(src32);
+  if ((unsigned)lane < head) dst[lane] = src8[lane];
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
+  const unsigned nwords = (nbytes - head) / 4;
+  for (unsigned w = lane; w < nwords; w += 32) d32[w] = __funnelshift_r(src32[w], src32[w + 1], 8 * head);
+  const unsigned done = head + 4 * nwords;
+  if ((unsigned)lane < nbytes - done) dst[done + lane] = src8[done + lane];
+}
+
 // ---- bit packing from the strided register layout -------------------------------
 // vals: tile (padded index) holding 256 raw field values; every lane packs its 8
-// consecutive coefficients into BITS bytes of `bytes` (shared scratch, BITS*32 bytes),
-// then the warp copies BITS*8 words to `gout` (4-byte aligned) with coalesced stores.
-template <int BITS>
+// consecutive coefficients into BITS bytes of `bytes` (shared scratch, BITS*32 bytes, + 4 when
+// !ALIGNED), then the warp copies BITS*8 words to `gout` with coalesced stores.  ALIGNED: gout is
+// 4-byte aligned; otherwise any alignment.
+template <int BITS, bool ALIGNED = true>
 __device__ __forceinline__ void pack_tile(const int32_t* tile, uint8_t* bytes, uint8_t* gout,
                                           int lane) {
   const int base = 8 * lane + 4 * (lane >> 2);
@@ -229,9 +251,13 @@ __device__ __forceinline__ void pack_tile(const int32_t* tile, uint8_t* bytes, u
   }
   __syncwarp();
   const uint32_t* src = reinterpret_cast<const uint32_t*>(bytes);
-  uint32_t* g = reinterpret_cast<uint32_t*>(gout);
+  if (ALIGNED) {
+    uint32_t* g = reinterpret_cast<uint32_t*>(gout);
 #pragma unroll
-  for (int w = lane; w < BITS * 8; w += 32) g[w] = src[w];
+    for (int w = lane; w < BITS * 8; w += 32) g[w] = src[w];
+  } else {
+    warp_store_unaligned(gout, src, BITS * 32, lane);
+  }
   __syncwarp();
 }
 

@@ -338,7 +338,7 @@ __device__ __forceinline__ int stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp
                                             const int2* zs, const int2* nzs, int lane,
                                             const uint8_t* ybytes, int32_t* wrows,
                                             const int8_t* next_c8, const uint64_t* ct,
-                                            const int32_t* shat, uint8_t* stage_sig,
+                                            const int32_t* shat, uint8_t* stage_sig, bool direct,
                                             const int32_t* bounds) {
   const int32_t z_bound = DBG ? bounds[0] : P::GAMMA1 - P::BETA;
   const int32_t r0_bound = DBG ? bounds[1] : P::GAMMA2 - P::BETA;
@@ -452,19 +452,28 @@ __device__ __forceinline__ int stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp
   if (DBG && fails) return 1 + (int)(__ffs(fails) - 1);
   if (weight > (unsigned)P::OMEGA) return DBG ? 4 : 1;
 
-  // accepted: c~ | z | hints into the staging slot
-  if (lane < 2 * Hashing<P>::CTW) reinterpret_cast<uint32_t*>(stage_sig)[lane] =
-      reinterpret_cast<const uint32_t*>(ct)[lane];
+  // accepted: c~ | z | hints into the staging slot -- or, for a task's next unresolved nonce
+  // (depth 0: if it is valid it IS the winner, scheduler.hpp:117), straight into the task's
+  // signature (`direct`; any alignment), so that the commit step has nothing to copy
+  if (direct) {
+    for (int b = lane; b < Hashing<P>::CT; b += 32) stage_sig[b] = reinterpret_cast<const uint8_t*>(ct)[b];
+  } else if (lane < 2 * Hashing<P>::CTW) {
+    reinterpret_cast<uint32_t*>(stage_sig)[lane] = reinterpret_cast<const uint32_t*>(ct)[lane];
+  }
 #pragma unroll 1
   for (int j = 0; j < P::L; ++j) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) ws.tile[lane + 36 * e] = P::GAMMA1 - ws.vhat[j][e][lane];
     __syncwarp();
-    pack_tile<P::Z_BITS>(ws.tile, pp.ring(pp.k), stage_sig + S::SIG_Z + j * S::Z_POLY, lane);
+    if (direct)
+      pack_tile<P::Z_BITS, false>(ws.tile, pp.ring(pp.k), stage_sig + S::SIG_Z + j * S::Z_POLY, lane);
+    else
+      pack_tile<P::Z_BITS, true>(ws.tile, pp.ring(pp.k), stage_sig + S::SIG_Z + j * S::Z_POLY, lane);
   }
   uint8_t* hint = stage_sig + S::SIG_Z + P::L * S::Z_POLY;
-  // (the padding behind the signature is cleared too: the word-wise commit copy reads it)
-  for (int b = lane; b < S::HINT + (SignSizes<P>::SIG_PAD - S::SIG); b += 32) hint[b] = 0;
+  // (staging: the padding behind the signature is cleared too, the word-wise commit copy reads it)
+  const int clear = S::HINT + (direct ? 0 : SignSizes<P>::SIG_PAD - S::SIG);
+  for (int b = lane; b < clear; b += 32) hint[b] = 0;
   __syncwarp();
   unsigned count = 0;
 #pragma unroll 1
@@ -767,11 +776,13 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       while (s < kSignThreads) {
         const int nx = grab(&sm.cursor4);
         const BatchView& v = sm.bv[sm.slot_batch[s]];
+        const bool direct = (unsigned)s < U;  // depth 0: the task's next unresolved nonce
         const int rej = stage_finish<P, DBG>(
             sm.u.a.ws[warp], pp, par, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
             wbuf + (size_t)s * Z::W_SLOT, nx < kSignThreads ? c8buf + (size_t)nx * kN : nullptr,
             ctbuf + s * CTW, v.shat + key_of(s) * ((P::L + 2 * P::K) * kN),
-            staging + (size_t)s * Z::SIG_PAD, v.bounds);
+            direct ? v.sigs + (size_t)sm.slot_task[s] * S::SIG : staging + (size_t)s * Z::SIG_PAD, direct,
+            v.bounds);
         if (lane == 0) {
           sm.slot_valid[s] = rej == 0 ? 1 : 0;
           // RejectStage of the reference (scheme.hpp:34): 0 z, 1 r0, 2 c t0, 3 hint weight; 255 accepted
@@ -845,7 +856,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
 #pragma unroll 1
       for (unsigned u = warp; u < U; u += kSignWarps) {
         const int win = sm.winner[u];
-        if (win == -1) continue;
+        if (win == -1 || win == (int)u) continue;  // open, or a depth-0 winner that S4 wrote in place
         const uint8_t* src = staging + (size_t)(win < 0 ? 0 : win) * Z::SIG_PAD;
         uint8_t* dst = sm.bv[sm.ubatch[u]].sigs + (size_t)sm.utask[u] * S::SIG;
         // word-granular, coalesced copy to a destination of any alignment (sig_bytes is
