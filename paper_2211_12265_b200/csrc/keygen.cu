@@ -15,6 +15,10 @@ namespace dlb {
 
 // Chunks alternate between two compute lanes so the one-thread-per-task hashes of one
 // chunk overlap the wide sampler / arithmetic kernels of the next (see verify.cu).
+// The one-sponge-per-task kernels (seed expansion, tr) run once over the whole call so they
+// bring enough warps to fill 148 SMs; only the stages whose scratch is large (the expanded
+// matrix, 16-56 KB per key) are cut into chunks, which alternate between two compute lanes so
+// the arithmetic of one chunk overlaps the samplers of the next.
 template <class P>
 int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uint8_t* d_sks) {
   using S = Sizes<P>;
@@ -27,14 +31,14 @@ int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uin
   const size_t cmax = c->knob_chunk;  // DLB_CHUNK at dlb_create for experiments
   if (chunk > cmax) chunk = cmax;
   if (chunk > n) chunk = n;
-  uint64_t* seeds[2];
+  uint64_t* seeds;
   int8_t* s8[2];
   int32_t* A[2];
-  const char* nm[2][3] = {{"g.seeds0", "g.s80", "g.A0"}, {"g.seeds1", "g.s81", "g.A1"}};
+  const char* nm[2][2] = {{"g.s80", "g.A0"}, {"g.s81", "g.A1"}};
+  DLB_TRY(dalloc(c, "g.seeds", n * 16, &seeds));
   for (int b = 0; b < 2; ++b) {
-    DLB_TRY(dalloc(c, nm[b][0], chunk * 16, &seeds[b]));
-    DLB_TRY(dalloc(c, nm[b][1], chunk * PV * kN, &s8[b]));
-    DLB_TRY(dalloc(c, nm[b][2], chunk * KL * kN, &A[b]));
+    DLB_TRY(dalloc(c, nm[b][0], chunk * PV * kN, &s8[b]));
+    DLB_TRY(dalloc(c, nm[b][1], chunk * KL * kN, &A[b]));
   }
   if (const int co = pipeline_carveout(c); co >= 0) {
     prefer_carveout(k_keygen_seed, co);
@@ -43,6 +47,10 @@ int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uin
     prefer_carveout(k_keygen_arith<P, 4>, co);
     prefer_carveout(k_hash_tr, co);
   }
+  k_keygen_seed<<<cdiv(n, 128), 128, 0, main>>>(
+      d_zetas, (unsigned)n, seeds,
+      Hashing<P>::MLDSA ? ((unsigned)P::K | ((unsigned)P::L << 8) | (1u << 16)) : 0u);
+  c->launches += 1;
   DLB_CUDA_CHECK(cudaEventRecord(c->ev_fork, main));
   DLB_CUDA_CHECK(cudaStreamWaitEvent(c->lane_s[0], c->ev_fork, 0));
   DLB_CUDA_CHECK(cudaStreamWaitEvent(c->lane_s[1], c->ev_fork, 0));
@@ -51,26 +59,25 @@ int keygen_dev(dlb_ctx* c, size_t n, const uint8_t* d_zetas, uint8_t* d_pks, uin
     const size_t cnt = n - lo < chunk ? n - lo : chunk;
     const int b = (int)(ci & 1);
     cudaStream_t st = c->lane_s[b];
-    const uint8_t* seedb = reinterpret_cast<const uint8_t*>(seeds[b]);
+    const uint8_t* seedb = reinterpret_cast<const uint8_t*>(seeds + lo * 16);
     uint8_t* pks = d_pks + lo * S::PK;
     uint8_t* sks = d_sks + lo * S::SK;
-    k_keygen_seed<<<cdiv(cnt, 128), 128, 0, st>>>(
-        d_zetas + lo * 32, (unsigned)cnt, seeds[b],
-        Hashing<P>::MLDSA ? ((unsigned)P::K | ((unsigned)P::L << 8) | (1u << 16)) : 0u);
     k_expand_s<P, HW><<<cdiv(cnt * PV, HW * 32), HW * 32, 0, st>>>(seedb + 32, 128,
                                                                     (unsigned)(cnt * PV), s8[b]);
     k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(seedb, 128, (unsigned)(cnt * KL),
                                                                     A[b]);
     k_keygen_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>((unsigned)cnt, seedb, s8[b], A[b], pks, sks);
-    k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, S::PK, S::PK, (unsigned)cnt, sks + 64, S::SK,
-                                              Hashing<P>::TRW);
-    c->launches += 5;
+    c->launches += 3;
     DLB_LAUNCH_CHECK();
   }
   for (int b = 0; b < 2; ++b) {
     DLB_CUDA_CHECK(cudaEventRecord(c->ev_join[b], c->lane_s[b]));
     DLB_CUDA_CHECK(cudaStreamWaitEvent(main, c->ev_join[b], 0));
   }
+  k_hash_tr<<<cdiv(n, 128), 128, 0, main>>>(d_pks, S::PK, S::PK, (unsigned)n, d_sks + 64, S::SK,
+                                            Hashing<P>::TRW);
+  c->launches += 1;
+  DLB_LAUNCH_CHECK();
   return 0;
 }
 

@@ -199,23 +199,23 @@ __device__ __forceinline__ void ntt_inv(int32_t (&r)[8], int32_t* tile, const in
   __syncwarp();
 }
 
-// One warp copies nbytes (a multiple of 4) from a 4-byte aligned shared-memory buffer to a global
-// destination of ANY alignment with coalesced word stores (signatures are packed back to back and
-// their size is odd at levels 3 / 5).  Reads one word past the last full word of the source.
+// One warp copies nbytes from a 4-byte aligned shared-memory buffer to a global destination of ANY
+// alignment with coalesced word stores (signatures are packed back to back and their size is
+// odd at levels 3 / 5; the destination may be pinned host memory, where byte-sized stores
+// would each cost a PCIe transaction).  Reads up to one word past the end of the source.
 __device__ __forceinline__ void warp_store_unaligned(uint8_t* dst, const uint32_t* src32, unsigned nbytes,
                                                      int lane) {
   const unsigned a = (unsigned)(reinterpret_cast<uintptr_t>(dst) & 3);
-  if (a == 0) {
-    uint32_t* g = reinterpret_cast<uint32_t*>(dst);
-    for (unsigned w = lane; w < nbytes / 4; w += 32) g[w] = src32[w];
-    return;
-  }
-  const unsigned head = 4 - a;  // bytes up to the next word boundary of the destination
+  const unsigned head = a ? min(4u - a, nbytes) : 0u;  // bytes up to the next word boundary
   const uint8_t* src8 = reinterpret_cast<const uint8_t*>(src32);
   if ((unsigned)lane < head) dst[lane] = src8[lane];
   uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
   const unsigned nwords = (nbytes - head) / 4;
-  for (unsigned w = lane; w < nwords; w += 32) d32[w] = __funnelshift_r(src32[w], src32[w + 1], 8 * head);
+  if (head == 0) {
+    for (unsigned w = lane; w < nwords; w += 32) d32[w] = src32[w];
+  } else {
+    for (unsigned w = lane; w < nwords; w += 32) d32[w] = __funnelshift_r(src32[w], src32[w + 1], 8 * head);
+  }
   const unsigned done = head + 4 * nwords;
   if ((unsigned)lane < nbytes - done) dst[done + lane] = src8[done + lane];
 }

@@ -293,11 +293,23 @@ static __global__ void k_hash_tr(const uint8_t* __restrict__ pk, size_t pk_strid
   {
     const uint8_t* msg = pk + (size_t)t * pk_stride;
     const size_t nblocks = pk_bytes / kRate256 + 1;
+    // packed public keys are 32 + 320 k bytes: whole 64-bit words, and 8-byte aligned whenever the
+    // array is -- then the absorb loop is plain word loads (no byte assembly, no length tests)
+    const bool aligned = ((reinterpret_cast<uintptr_t>(msg) | pk_bytes) & 7) == 0;
+    const unsigned nwords = pk_bytes / 8;
 #pragma unroll 1
     for (size_t blk = 0; blk < nblocks; ++blk) {
+      if (aligned) {
+        const uint64_t* m64 = reinterpret_cast<const uint64_t*>(msg) + blk * kWords256;
+        const unsigned left = nwords - (unsigned)(blk * kWords256);  // words from this block on
 #pragma unroll
-      for (int w = 0; w < kWords256; ++w)
-        s[w] ^= padded_word(msg, pk_bytes, blk * kRate256 + 8 * w);
+        for (int w = 0; w < kWords256; ++w)
+          s[w] ^= (unsigned)w < left ? __ldg(m64 + w) : ((unsigned)w == left ? 0x1Full : 0ull);
+      } else {
+#pragma unroll
+        for (int w = 0; w < kWords256; ++w)
+          s[w] ^= padded_word(msg, pk_bytes, blk * kRate256 + 8 * w);
+      }
       if (blk == nblocks - 1) s[kWords256 - 1] ^= 0x8000000000000000ull;
       keccak_f1600(s);
     }

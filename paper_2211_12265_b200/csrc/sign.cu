@@ -455,11 +455,13 @@ __device__ __forceinline__ int stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp
   // accepted: c~ | z | hints into the staging slot -- or, for a task's next unresolved nonce
   // (depth 0: if it is valid it IS the winner, scheduler.hpp:117), straight into the task's
   // signature (`direct`; any alignment), so that the commit step has nothing to copy
-  if (direct) {
-    for (int b = lane; b < Hashing<P>::CT; b += 32) stage_sig[b] = reinterpret_cast<const uint8_t*>(ct)[b];
-  } else if (lane < 2 * Hashing<P>::CTW) {
-    reinterpret_cast<uint32_t*>(stage_sig)[lane] = reinterpret_cast<const uint32_t*>(ct)[lane];
-  }
+  // (every piece is assembled in shared memory and leaves as whole coalesced words: the
+  // destination may be pinned host memory)
+  uint32_t* scr = reinterpret_cast<uint32_t*>(pp.ring(pp.k));  // free ring buffer, 1 KiB
+  if (lane < 2 * Hashing<P>::CTW) scr[lane] = reinterpret_cast<const uint32_t*>(ct)[lane];
+  __syncwarp();
+  warp_store_unaligned(stage_sig, scr, Hashing<P>::CT, lane);
+  __syncwarp();
 #pragma unroll 1
   for (int j = 0; j < P::L; ++j) {
 #pragma unroll
@@ -470,10 +472,12 @@ __device__ __forceinline__ int stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp
     else
       pack_tile<P::Z_BITS, true>(ws.tile, pp.ring(pp.k), stage_sig + S::SIG_Z + j * S::Z_POLY, lane);
   }
-  uint8_t* hint = stage_sig + S::SIG_Z + P::L * S::Z_POLY;
-  // (staging: the padding behind the signature is cleared too, the word-wise commit copy reads it)
-  const int clear = S::HINT + (direct ? 0 : SignSizes<P>::SIG_PAD - S::SIG);
-  for (int b = lane; b < clear; b += 32) hint[b] = 0;
+  // hint section (packing.hpp:105-118): positions ascending per polynomial, cumulative counts
+  // behind them, unused bytes zero.  (staging: the padding behind the signature is cleared
+  // too, the word-wise commit copy reads it)
+  constexpr int HWORDS = (S::HINT + (SignSizes<P>::SIG_PAD - S::SIG) + 3) / 4;
+  uint8_t* hsm = reinterpret_cast<uint8_t*>(scr);
+  for (int w = lane; w < HWORDS; w += 32) scr[w] = 0;
   __syncwarp();
   unsigned count = 0;
 #pragma unroll 1
@@ -481,11 +485,15 @@ __device__ __forceinline__ int stage_finish(SignWarpScratch<P>& ws, SlotPipe& pp
 #pragma unroll 1
     for (int e = 0; e < 8; ++e) {
       const unsigned mask = ws.hbits[i][e];
-      if ((mask >> lane) & 1) hint[count + __popc(mask & ((1u << lane) - 1))] = (uint8_t)(32 * e + lane);
+      if ((mask >> lane) & 1) hsm[count + __popc(mask & ((1u << lane) - 1))] = (uint8_t)(32 * e + lane);
       count += __popc(mask);
     }
-    if (lane == 0) hint[P::OMEGA + i] = (uint8_t)count;
+    if (lane == 0) hsm[P::OMEGA + i] = (uint8_t)count;
   }
+  __syncwarp();
+  warp_store_unaligned(stage_sig + S::SIG_Z + P::L * S::Z_POLY, scr,
+                       direct ? S::HINT : S::HINT + (SignSizes<P>::SIG_PAD - S::SIG), lane);
+  __syncwarp();
   return 0;
 }
 

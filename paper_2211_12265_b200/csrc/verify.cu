@@ -63,25 +63,22 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
   if (chunk > n) chunk = n;
   const size_t keys_cap = shared_key ? n_keys : chunk;
 
+  // The one-sponge-per-task stages (tr, mu, challenge, final hash) run once over the whole call:
+  // a chunk's worth of tasks is too few warps for 148 SMs.  Only ExpandA and the arithmetic,
+  // whose scratch is the expanded matrix (16-56 KB per key), are chunked over two lanes.
   int32_t* A[2];
-  uint8_t *tr[2], *w1buf[2], *pre_ok[2];
-  uint64_t* mu[2];
-  int8_t* c8[2];
-  const char* nm[2][6] = {{"v.A0", "v.tr0", "v.mu0", "v.c80", "v.w10", "v.ok0"},
-                          {"v.A1", "v.tr1", "v.mu1", "v.c81", "v.w11", "v.ok1"}};
-  for (int b = 0; b < 2; ++b) {
-    if (b == 1 && shared_key) {  // one expanded key serves both lanes
-      A[1] = A[0];
-      tr[1] = tr[0];
-    } else {
-      DLB_TRY(dalloc(c, nm[b][0], keys_cap * KL * kN, &A[b]));
-      DLB_TRY(dalloc(c, nm[b][1], keys_cap * Hashing<P>::TR, &tr[b]));
-    }
-    DLB_TRY(dalloc(c, nm[b][2], chunk * 8, &mu[b]));
-    DLB_TRY(dalloc(c, nm[b][3], chunk * kN, &c8[b]));
-    DLB_TRY(dalloc(c, nm[b][4], chunk * S::W1_ALL, &w1buf[b]));
-    DLB_TRY(dalloc(c, nm[b][5], chunk, &pre_ok[b]));
-  }
+  uint8_t *tr, *w1buf, *pre_ok;
+  uint64_t* mu;
+  int8_t* c8;
+  const size_t n_tr = shared_key ? n_keys : n;
+  DLB_TRY(dalloc(c, "v.A0", keys_cap * KL * kN, &A[0]));
+  if (shared_key) A[1] = A[0];  // one expanded key (table) serves both lanes
+  else DLB_TRY(dalloc(c, "v.A1", keys_cap * KL * kN, &A[1]));
+  DLB_TRY(dalloc(c, "v.tr", n_tr * Hashing<P>::TR, &tr));
+  DLB_TRY(dalloc(c, "v.mu", n * 8, &mu));
+  DLB_TRY(dalloc(c, "v.c8", n * kN, &c8));
+  DLB_TRY(dalloc(c, "v.w1", n * S::W1_ALL, &w1buf));
+  DLB_TRY(dalloc(c, "v.ok", n, &pre_ok));
   if (const int co = pipeline_carveout(c); co >= 0) {
     prefer_carveout(k_expand_a<P, HW>, co);
     prefer_carveout(k_hash_tr, co);
@@ -95,13 +92,22 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
   if (Hashing<P>::MLDSA) DLB_TRY(mldsa_prefix(c, main, &pfx, &plen));
   // (keys_expanded: a previous call of the same host-side batch already expanded this key
   // table into the context's arenas -- the host pipeline calls once per transfer chunk)
-  if (shared_key && !keys_expanded) {  // expand once on the caller's stream, before the fork
+  if (shared_key && !keys_expanded) {
     k_expand_a<P, HW><<<cdiv(n_keys * KL, HW * 32), HW * 32, 0, main>>>(d_pks, pk_stride,
                                                                         (unsigned)(n_keys * KL), A[0]);
-    k_hash_tr<<<cdiv(n_keys, 128), 128, 0, main>>>(d_pks, pk_stride, S::PK, (unsigned)n_keys, tr[0],
-                                                   Hashing<P>::TR, Hashing<P>::TRW);
-    c->launches += 2;
+    c->launches += 1;
   }
+  if (!(shared_key && keys_expanded)) {
+    k_hash_tr<<<cdiv(n_tr, 128), 128, 0, main>>>(d_pks, pk_stride, S::PK, (unsigned)n_tr, tr,
+                                                 Hashing<P>::TR, Hashing<P>::TRW);
+    c->launches += 1;
+  }
+  const size_t key_step = keyed ? 1 : (shared_key ? 0 : 1);  // 0: every task uses key 0
+  k_hash_mu<Hashing<P>::MLDSA><<<cdiv(n, 128), 128, 0, main>>>(
+      tr, key_step * Hashing<P>::TR, nullptr, 0, d_key_idx, pfx, plen, d_msgs, d_msg_off, (unsigned)n, mu,
+      nullptr);
+  k_sample_in_ball<P, HW><<<cdiv(n, HW * 32), HW * 32, 0, main>>>(d_sigs, S::SIG, (unsigned)n, c8);
+  c->launches += 2;
   DLB_CUDA_CHECK(cudaEventRecord(c->ev_fork, main));
   DLB_CUDA_CHECK(cudaStreamWaitEvent(c->lane_s[0], c->ev_fork, 0));
   DLB_CUDA_CHECK(cudaStreamWaitEvent(c->lane_s[1], c->ev_fork, 0));
@@ -112,31 +118,25 @@ int verify_dev(dlb_ctx* c, size_t n, const uint8_t* d_pks, size_t pk_stride, siz
     cudaStream_t st = c->lane_s[b];
     const uint8_t* pks = keyed ? d_pks : d_pks + lo * pk_stride;
     const uint32_t* kidx = keyed ? d_key_idx + lo : nullptr;
-    const size_t key_step = keyed ? 1 : (shared_key ? 0 : 1);  // 0: every task uses key 0
     const uint8_t* sigs = d_sigs + lo * S::SIG;
     if (!shared_key) {
       k_expand_a<P, HW><<<cdiv(cnt * KL, HW * 32), HW * 32, 0, st>>>(pks, pk_stride,
                                                                      (unsigned)(cnt * KL), A[b]);
-      k_hash_tr<<<cdiv(cnt, 128), 128, 0, st>>>(pks, pk_stride, S::PK, (unsigned)cnt, tr[b],
-                                                Hashing<P>::TR, Hashing<P>::TRW);
-      c->launches += 2;
+      c->launches += 1;
     }
-    k_hash_mu<Hashing<P>::MLDSA><<<cdiv(cnt, 128), 128, 0, st>>>(
-        tr[b], key_step * Hashing<P>::TR, nullptr, 0, kidx, pfx, plen, d_msgs, d_msg_off + lo,
-        (unsigned)cnt, mu[b], nullptr);
-    k_sample_in_ball<P, HW><<<cdiv(cnt, HW * 32), HW * 32, 0, st>>>(sigs, S::SIG, (unsigned)cnt, c8[b]);
     k_verify_arith<P, 4><<<cdiv(cnt, 4), 128, 0, st>>>(
-        (unsigned)cnt, pks, pk_stride, sigs, S::SIG, A[b], key_step * (size_t)KL * kN, kidx, c8[b],
-        w1buf[b], pre_ok[b]);
-    k_verify_final<P><<<cdiv(cnt, 128), 128, 0, st>>>((unsigned)cnt, mu[b], w1buf[b], sigs, S::SIG,
-                                                      pre_ok[b], d_flags + lo);
-    c->launches += 4;
+        (unsigned)cnt, pks, pk_stride, sigs, S::SIG, A[b], key_step * (size_t)KL * kN, kidx, c8 + lo * kN,
+        w1buf + lo * S::W1_ALL, pre_ok + lo);
+    c->launches += 1;
     DLB_LAUNCH_CHECK();
   }
   for (int b = 0; b < 2; ++b) {
     DLB_CUDA_CHECK(cudaEventRecord(c->ev_join[b], c->lane_s[b]));
     DLB_CUDA_CHECK(cudaStreamWaitEvent(main, c->ev_join[b], 0));
   }
+  k_verify_final<P><<<cdiv(n, 128), 128, 0, main>>>((unsigned)n, mu, w1buf, d_sigs, S::SIG, pre_ok, d_flags);
+  c->launches += 1;
+  DLB_LAUNCH_CHECK();
   return 0;
 }
 

@@ -64,8 +64,10 @@ if __name__ == "__main__":
     eng = Engine(0)
     pks, sks = eng.batch_keygen(level, np.arange(32, dtype=np.uint8))
     sk = sks[0]
-    run(level, 100000, 8, depth, eng, sk)
-    run(level, 10000, 10, 10, eng, sk)
-    run(level, 10000, 40, 8, eng, sk)
-    run(level, 1000, 32, 8, eng, sk)
+    nb = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+    run(level, 100000, nb, depth, eng, sk)
+    if len(sys.argv) <= 3:
+        run(level, 10000, 10, 10, eng, sk)
+        run(level, 10000, 40, 8, eng, sk)
+        run(level, 1000, 32, 8, eng, sk)
     eng.close()
