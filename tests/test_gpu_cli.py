@@ -20,7 +20,7 @@ def run(*args):
 
 @pytest.fixture(scope="module", autouse=True)
 def built():
-    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools")], check=True)
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools"), "all"], check=True)
 
 
 @pytest.mark.parametrize("level", [2, 3, 5, 65])  # 65 = ML-DSA-65 (FIPS 204 mode)
@@ -121,3 +121,21 @@ def test_bench_csv():
     assert all(l.split(",")[0] == "1" and float(l.split(",")[9]) > 0 for l in lines[1:])
     rc, out, _ = run("bench", "--level", 3, "--phi", 50, "--streams", 3, "--reps", 1)
     assert rc == 0 and [l.split(",")[7] for l in out.strip().splitlines()[1:]] == ["3", "3", "3"]
+
+
+def test_sweep_modes():
+    """tools/dilithium_cli.cpp:448-514: the three sensitivity modes in the bench CSV schema."""
+    rc, out, err = run("sweep", "--level", 2, "--phi", 512, "--reps", 1, "--psi-min", 64, "--psi-max", 512,
+                       "--psi-steps", 3, "--streams-max", 4)
+    assert rc == 0, err
+    lines = out.strip().splitlines()
+    assert lines[0] == ("schema,mode,op,level,phi,psi,workers,streams,reps,throughput_ops_s,"
+                        "mean_latency_us,attempts_mean")
+    rows = [l.split(",") for l in lines[1:]]
+    modes = [r[1] for r in rows]
+    assert modes == ["sweep-psi"] * 3 + ["sweep-batch"] * 5 + ["sweep-streams"] * 3
+    assert [r[5] for r in rows[:3]] == ["64", "288", "512"]          # psi grid
+    assert [r[4] for r in rows[3:8]] == ["32", "64", "128", "256", "512"]  # phi/16 doubling to phi
+    assert [r[7] for r in rows[8:]] == ["1", "2", "4"]               # batches in flight
+    assert all(r[0] == "1" and r[2] == "sign" and float(r[9]) > 0 and 1.5 < float(r[11]) < 12.0 for r in rows)
+    assert run("sweep", "--level", 2, "--streams-max", 64)[0] == 2

@@ -9,6 +9,8 @@
 //   verify       --level L --pk F --in MSG --sig SIG        exit 0 accept / 1 reject / 2 bad input
 //   batch-sign   --level L --sk F --out-dir D [--psi N] [--workers N] [--trace CSV] MSG...
 //   batch-verify --level L --pk F --sig-dir D [--workers N] MSG...     exit 0 iff all accept
+//   sweep        --level L [--phi N] [--reps N] [--psi-min N] [--psi-max N] [--psi-steps N] [--streams-max N]
+//                CSV rows of the modes sweep-psi / sweep-batch / sweep-streams (same schema)
 //   bench        --level L [--phi N] [--psi N] [--workers N] [--streams N] [--reps N]
 //                CSV on stdout: schema,mode,op,level,phi,psi,workers,streams,reps,
 //                               throughput_ops_s,mean_latency_us,attempts_mean
@@ -135,13 +137,15 @@ const std::map<std::string, Command>& commands() {
       {"batch-sign", {with({"--sk", "--out-dir", "--psi", "--workers", "--trace"}), {"--level", "--sk", "--out-dir"}, true}},
       {"batch-verify", {with({"--pk", "--sig-dir", "--workers"}), {"--level", "--pk", "--sig-dir"}, true}},
       {"bench", {with({"--phi", "--psi", "--workers", "--streams", "--reps", "--trace"}), {"--level"}, false}},
+      {"sweep", {with({"--phi", "--workers", "--reps", "--psi-min", "--psi-max", "--psi-steps", "--streams-max"}),
+                 {"--level"}, false}},
   };
   return table;
 }
 
 int usage(const std::string& why) {
   std::cerr << "error: " << why << "\n"
-            << "usage: dilithium_b200 <keygen|sign|verify|batch-sign|batch-verify|bench> --level {2,3,5,44,65,87} ...\n";
+            << "usage: dilithium_b200 <keygen|sign|verify|batch-sign|batch-verify|bench|sweep> --level {2,3,5,44,65,87} ...\n";
   return kBadInput;
 }
 
@@ -478,6 +482,83 @@ int cmd_bench(const Args& a) {
   });
 }
 
+// sweep: the reference tool's sensitivity study (tools/dilithium_cli.cpp:448-514)
+// with its CSV schema and its three modes.  On the GPU engine `psi` is the number of resident
+// attempt slots of the batch and `streams` the number of in-flight batches the task list is cut
+// into (dlb_sign_submit x S, dlb_sign_wait x S -- the paper's streams).  Times cover the call with
+// pinned host buffers in and out (messages up, signatures down); medians over --reps.
+int cmd_sweep(const Args& a) {
+  size_t phi, workers, reps, psi_min, psi_max, psi_steps, streams_max;
+  if (!a.number("--phi", 10000, phi) || !a.number("--workers", 1, workers) || !a.number("--reps", 5, reps) ||
+      !a.number("--psi-min", 1, psi_min) || !a.number("--psi-max", 0, psi_max) ||
+      !a.number("--psi-steps", 6, psi_steps) || !a.number("--streams-max", 8, streams_max) || phi == 0 ||
+      reps == 0)
+    return usage("sweep options must be positive numbers");
+  if (streams_max > 16) return usage("--streams-max must be at most 16 (batches in flight per engine)");
+  return with_level(a, [&](auto lv) {
+    constexpr Params P = params_of<decltype(lv)::value>();
+    Engine& eng = Engine::instance();
+    std::mt19937_64 rng(20221112);
+    SeedArray zeta;
+    for (auto& b : zeta) b = static_cast<uint8_t>(rng());
+    const auto [pk, sk] = keygen<P>(zeta);
+    (void)pk;
+    // 59-byte messages like the reference sweep (dilithium_cli.cpp:458-462), flat in pinned memory
+    constexpr size_t kMsg = 59;
+    auto* msgs = static_cast<uint8_t*>(dlb_host_alloc(phi * kMsg + 8));
+    auto* off = static_cast<uint64_t*>(dlb_host_alloc((phi + 1) * 8));
+    auto* sigs = static_cast<uint8_t*>(dlb_host_alloc(phi * P.sig_bytes() + 8));
+    auto* att = static_cast<uint32_t*>(dlb_host_alloc(phi * 4));
+    auto* skp = static_cast<uint8_t*>(dlb_host_alloc(P.sk_bytes()));
+    if (!msgs || !off || !sigs || !att || !skp) throw std::runtime_error("pinned allocation failed");
+    for (size_t i = 0; i < phi * kMsg; ++i) msgs[i] = static_cast<uint8_t>(rng());
+    for (size_t i = 0; i <= phi; ++i) off[i] = i * kMsg;
+    std::memcpy(skp, sk.data(), P.sk_bytes());
+    std::cout << "schema,mode,op,level,phi,psi,workers,streams,reps,throughput_ops_s,mean_latency_us,attempts_mean\n";
+    double attempts_mean = 0;
+    auto timed = [&](size_t n, size_t psi, size_t streams) {
+      std::vector<uint64_t> tickets(streams);
+      for (size_t s = 0; s < streams; ++s) {
+        const size_t lo = n * s / streams, hi = n * (s + 1) / streams;
+        const size_t part_psi = psi == 0 ? 0 : std::max<size_t>(1, std::min(psi, hi - lo));
+        check(dlb_sign_submit(eng.ctx(), P.level, 0, skp, 0, hi - lo, nullptr, msgs + lo * kMsg, off /* equal lengths: relative offsets */, nullptr, part_psi,
+                              1, sigs + lo * P.sig_bytes(), att + lo, nullptr, &tickets[s]),
+              "dlb_sign_submit");
+      }
+      for (size_t s = 0; s < streams; ++s) check(dlb_sign_wait(eng.ctx(), tickets[s], nullptr), "dlb_sign_wait");
+      uint64_t sum = 0;
+      for (size_t i = 0; i < n; ++i) sum += att[i];
+      attempts_mean = double(sum) / double(n);
+    };
+    auto point = [&](const char* mode, size_t n, size_t psi, size_t streams) {
+      const double sec = median_seconds(reps, [&] { timed(n, psi, streams); });
+      std::printf("1,%s,sign,%d,%zu,%zu,%zu,%zu,%zu,%.1f,%.3f,%.3f\n", mode, P.level, n, psi, workers, streams,
+                  reps, n / sec, sec / n * 1e6, attempts_mean);
+    };
+    // throughput vs psi at fixed phi
+    psi_max = std::min(psi_max == 0 ? phi : psi_max, phi);
+    psi_min = std::max<size_t>(1, std::min(psi_min, psi_max));
+    const size_t steps = std::max<size_t>(2, psi_steps);
+    for (size_t st = 0; st < steps; ++st) point("sweep-psi", phi, psi_min + (psi_max - psi_min) * st / (steps - 1), 1);
+    // throughput vs batch size at the engine's default psi
+    for (size_t batch = std::max<size_t>(1, phi / 16);; batch *= 2) {
+      if (batch >= phi) {
+        point("sweep-batch", phi, 0, 1);
+        break;
+      }
+      point("sweep-batch", batch, 0, 1);
+    }
+    // throughput vs batches in flight at full phi
+    for (size_t st = 1; st <= streams_max; st *= 2) point("sweep-streams", phi, 0, st);
+    dlb_host_free(msgs);
+    dlb_host_free(off);
+    dlb_host_free(sigs);
+    dlb_host_free(att);
+    dlb_host_free(skp);
+    return kOk;
+  });
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -494,6 +575,7 @@ int main(int argc, char** argv) {
     if (name == "verify") return cmd_verify(a);
     if (name == "batch-sign") return cmd_batch_sign(a);
     if (name == "batch-verify") return cmd_batch_verify(a);
+    if (name == "sweep") return cmd_sweep(a);
     return cmd_bench(a);
   } catch (const std::exception& e) {
     std::cerr << "error: " << e.what() << "\n";
