@@ -736,6 +736,36 @@ bool verify(std::span<const uint8_t> pk_bytes, std::span<const uint8_t> msg,
 }
 
 // ---- several GPUs of one box ------------------------------------------------------------
+// Shard g of G over an n-task batch is [n*g/G, n*(g+1)/G) -- the reference tool's partition
+// (tools/dilithium_cli.cpp:323).  Uneven n leaves shards that differ by one task; G > n leaves
+// empty shards.
+inline std::vector<size_t> shard_bounds(size_t n, size_t shards) {
+  if (shards == 0) throw std::invalid_argument("shard_bounds: no shards");
+  std::vector<size_t> b(shards + 1);
+  for (size_t g = 0; g <= shards; ++g) b[g] = n * g / shards;
+  return b;
+}
+
+// BatchStats of the shards -> BatchStats of the batch: counters add up, a shard's failed task
+// indices are rebased by the shard's first task so they index the caller's job list.
+inline BatchStats merge_shard_stats(std::span<const BatchStats> parts, std::span<const size_t> bounds) {
+  if (bounds.size() != parts.size() + 1) throw std::invalid_argument("merge_shard_stats: bounds / parts mismatch");
+  BatchStats out;
+  for (size_t g = 0; g < parts.size(); ++g) {
+    const BatchStats& s = parts[g];
+    out.rounds += s.rounds;
+    out.attempts += s.attempts;
+    out.speculative += s.speculative;
+    out.idle_slot_rounds += s.idle_slot_rounds;
+    out.accepted_attempt_sum += s.accepted_attempt_sum;
+    for (size_t t : s.failed_tasks) {
+      if (t >= bounds[g + 1] - bounds[g]) throw std::out_of_range("merge_shard_stats: failed index outside its shard");
+      out.failed_tasks.push_back(bounds[g] + t);
+    }
+  }
+  return out;
+}
+
 // The path has no exchange step: a batch is cut into contiguous ranges lo = n*g/G,
 // hi = n*(g+1)/G exactly like the reference tool's multi-engine mode
 // (tools/dilithium_cli.cpp:319-339), one Engine and one host thread per device, results
@@ -754,11 +784,7 @@ class ShardedEngine {
   }
   size_t size() const { return engines_.size(); }
   // shard boundaries of an n-task batch (the partition run() uses)
-  std::vector<size_t> partition(size_t n) const {
-    std::vector<size_t> b(engines_.size() + 1);
-    for (size_t g = 0; g <= engines_.size(); ++g) b[g] = n * g / engines_.size();
-    return b;
-  }
+  std::vector<size_t> partition(size_t n) const { return shard_bounds(n, engines_.size()); }
 
   template <Params P>
   std::vector<std::pair<PkBytes<P>, SkBytes<P>>> batch_keygen(std::span<const SeedArray> zetas) {
@@ -778,26 +804,13 @@ class ShardedEngine {
     const size_t G = engines_.size();
     std::vector<std::vector<SigBytes<P>>> parts(G);
     std::vector<BatchStats> part_stats(G);
-    std::vector<size_t> los(G, 0);
     run(jobs.size(), [&](size_t g, size_t lo, size_t hi) {
-      los[g] = lo;
       parts[g] = b200::batch_sign<P>(jobs.subspan(lo, hi - lo), cfg, &part_stats[g], *engines_[g]);
     });
     std::vector<SigBytes<P>> out;
     out.reserve(jobs.size());
     for (auto& p : parts) out.insert(out.end(), p.begin(), p.end());
-    if (stats) {
-      *stats = BatchStats{};
-      for (size_t g = 0; g < G; ++g) {
-        const BatchStats& s = part_stats[g];
-        stats->rounds += s.rounds;
-        stats->attempts += s.attempts;
-        stats->speculative += s.speculative;
-        stats->idle_slot_rounds += s.idle_slot_rounds;
-        stats->accepted_attempt_sum += s.accepted_attempt_sum;
-        for (size_t t : s.failed_tasks) stats->failed_tasks.push_back(los[g] + t);  // rebased to the batch
-      }
-    }
+    if (stats) *stats = merge_shard_stats(part_stats, partition(jobs.size()));
     return out;
   }
 
@@ -819,7 +832,7 @@ class ShardedEngine {
     std::vector<std::thread> threads;
     std::vector<std::exception_ptr> errs(G);
     for (size_t g = 0; g < G; ++g) {
-      const size_t lo = per_engine ? g : n * g / G, hi = per_engine ? g + 1 : n * (g + 1) / G;
+      const size_t lo = per_engine ? g : shard_bounds(n, G)[g], hi = per_engine ? g + 1 : shard_bounds(n, G)[g + 1];
       if (hi == lo) continue;
       threads.emplace_back([&, g, lo, hi] {
         try {

@@ -785,6 +785,8 @@ int sign_host_submit(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t
   prof.mark("arenas");
   DLB_TRY(upload("h.sk", dsk, sks, nk * ls.sk));
   DLB_TRY(upload("h.msg", dm, msgs, mbytes));
+  // the digest kernels read whole aligned words around the last message bytes (and mask them)
+  DLB_CU(cudaMemsetAsync(dm + mbytes, 0, 8, S));
   DLB_TRY(upload("h.off", doff, msg_off, (n + 1) * 8));
   if (key_idx) DLB_TRY(upload("h.kidx", dkidx, key_idx, n * 4));
   if (rho_prime) {

@@ -218,3 +218,24 @@ def test_mldsa_oracle_against_openssl_vectors(oracle, mldsa_golden, level):
                 assert ours.hex() == s["oracle_sig"] and att == s["oracle_attempts"]
             finally:
                 oracle.set_mldsa_context(b"")
+
+
+def test_reference_scheduler_commit_rule(ref):
+    """scheduler.hpp:58-136 replayed on random validity tables: whatever (phi, psi, speculate), the
+    reference's NonceScheduler accepts each task's FIRST valid attempt and executes every attempt
+    below it -- the rule the device scheduler's parity tests (assignment log, attempt counts) rely on."""
+    import numpy as np
+    rng = np.random.default_rng(58)
+    for _ in range(40):
+        phi = int(rng.integers(1, 200))
+        psi = int(rng.integers(1, 2 * phi + 1))
+        depth = 24
+        valid = (rng.random((phi, depth)) < 0.25).astype(np.uint8)
+        valid[:, -1] = 1  # every task terminates inside the table
+        for speculate in (True, False):
+            acc, executed = ref.scheduler_replay(phi, psi, 4, speculate, valid)
+            first = valid.argmax(axis=1)
+            assert np.array_equal(acc, first)
+            assert executed >= int((first + 1).sum())  # every attempt up to the accepted one ran
+            if not speculate:
+                assert executed == int((first + 1).sum())  # and without speculation nothing else
