@@ -569,10 +569,14 @@ std::vector<SigBytes<P>> batch_sign_impl(std::span<const SignJob<P>> jobs, const
     if (rc == 0) ++submitted;
   }
   prof.mark("sign: submit");
-  if (!into) {  // while the device signs: allocate the result and fault its pages in, in parallel
+  if (!into) {  // while the device signs: allocate the result, fault its pages in (in parallel), size it
     out.reserve(n);
     advise_huge(out.data(), n * sizeof(SigBytes<P>));
     prefault(out.data(), n * sizeof(SigBytes<P>), copy_threads());
+    // up to 64 MB the vector is sized now (its zero fill hides behind the device) and finished
+    // parts are copied in by several threads; beyond, one appending pass per part is cheaper than
+    // a zero fill plus a copy
+    if (n * sizeof(SigBytes<P>) <= (size_t{64} << 20)) out.resize(n);
     prof.mark("sign: result pages");
   }
   dlb_sign_stats total{};
@@ -587,8 +591,16 @@ std::vector<SigBytes<P>> batch_sign_impl(std::span<const SignJob<P>> jobs, const
     total.idle_slot_rounds += st.idle_slot_rounds;
     total.accepted_attempt_sum += st.accepted_attempt_sum;
     if (into) continue;
-    const auto* first = reinterpret_cast<const SigBytes<P>*>(sig_stage + ps[p].lo * P.sig_bytes());
-    out.insert(out.end(), first, first + (ps[p].hi - ps[p].lo));  // while later parts still sign
+    // finished part: pinned staging -> result vector on several threads, while later parts still sign
+    const size_t lo = ps[p].lo, cnt = ps[p].hi - ps[p].lo;
+    if (out.size() == n) {
+      parallel_ranges(cnt, copy_threads(), 512, [&](size_t a, size_t b) {
+        std::memcpy(out[lo + a].data(), sig_stage + (lo + a) * P.sig_bytes(), (b - a) * P.sig_bytes());
+      });
+    } else {
+      const auto* first = reinterpret_cast<const SigBytes<P>*>(sig_stage + lo * P.sig_bytes());
+      out.insert(out.end(), first, first + cnt);
+    }
   }
   prof.mark("sign: wait+copy");
   if (cfg.trace) {
