@@ -57,8 +57,9 @@ typedef struct dlb_sign_stats {
 
 /* Library / device ------------------------------------------------------------------ */
 
-/* Creates an engine on CUDA device `device`.  max_batch is a sizing hint (0 = grow on
- * demand).  Replaces the per-call WorkerPool + MemoryPool construction of
+/* Creates an engine on CUDA device `device`.  max_batch is a sizing hint: 0 = everything grows
+ * on demand; > 0 = the signing state and the per-task arenas of that many tasks are built here
+ * instead of inside the first call.  Replaces the per-call WorkerPool + MemoryPool construction of
  * batch.hpp:62-67 with a context that is built once and reused. */
 int dlb_create(dlb_ctx** out, int device, size_t max_batch);
 void dlb_destroy(dlb_ctx* ctx);

@@ -208,6 +208,23 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
     return rc;
   }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  // max_batch > 0: the caller knows its batch size -- build the signing state (ring, lanes, flags)
+  // and the size-dependent I/O arenas of the first arena set now instead of inside the first call
+  if (max_batch) {
+    unsigned t;
+    cudaStream_t pub;
+    int rc2 = sign_reserve(c, &t, &pub);  // creates the state; the ticket itself is not consumed
+    void* p = nullptr;
+    if (rc2 == 0) rc2 = c->dbuf(c->slot_name(0, "io.off"), (max_batch + 1) * 8, &p);
+    if (rc2 == 0) rc2 = c->dbuf(c->slot_name(0, "io.att"), max_batch * 4, &p);
+    if (rc2 == 0) rc2 = c->dbuf(c->slot_name(0, "io.fail"), max_batch, &p);
+    if (rc2 == 0) rc2 = c->dbuf(c->slot_name(0, "s.mu"), max_batch * 64, &p);
+    if (rc2 == 0) rc2 = c->dbuf(c->slot_name(0, "s.rp"), max_batch * 64, &p);
+    if (rc2 != 0) {
+      dlb_destroy(c);
+      return rc2;
+    }
+  }
   *out = c;
   return 0;
 }
