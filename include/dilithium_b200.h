@@ -38,7 +38,7 @@ extern "C" {
 #define DLB_E_LEVEL (-2)
 #define DLB_E_KEY (-3)
 #define DLB_E_NOMEM (-4)
-#define DLB_E_BUSY (-5)     /* 16 signing batches already in flight: wait for the oldest first */
+#define DLB_E_BUSY (-5)     /* the batch submitted 16 tickets ago is still un-waited: wait for it first */
 #define DLB_E_INTERNAL (-6) /* a submitted batch was never completed (device fault) */
 
 typedef struct dlb_ctx dlb_ctx;
@@ -183,7 +183,9 @@ int dlb_verify_batch_keyed(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t
  * The paper keeps several batches in flight per GPU (the reference
  * tool's engines, tools/dilithium_cli.cpp:309-345).  dlb_sign_submit enqueues a batch and
  * returns at once with a ticket; dlb_sign_wait blocks until that batch is complete and fills
- * the outputs.  Up to 16 batches may be in flight per context (DLB_E_BUSY beyond).  The device
+ * the outputs.  Tickets are numbered consecutively (synchronous sign calls take one too) and the
+ * engine keeps 16 consecutive tickets: a submission returns DLB_E_BUSY while the batch submitted 16
+ * tickets earlier has not been waited for.  The device
  * scheduler is shared: CTAs that run out of tasks of one batch claim tasks of the next
  * submitted batches (of the same level) before they speculate, so the rejection-loop tail of a
  * batch overlaps the body of its successors.  Output bytes never depend on what else is in

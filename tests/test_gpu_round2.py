@@ -202,3 +202,56 @@ def test_key_cache_across_calls(oracle, monkeypatch):
         assert [sigs[i].tobytes() for i in range(6)] == want[2]
     finally:
         e.close()
+
+
+def test_in_flight_stress_random_pipeline(eng):
+    """A long random pipeline: 240 batches of random size (1 .. 30,000), level and key -- 40 shared
+    keys per level, more than the 32-entry key cache holds, plus per-task-key batches -- submitted
+    with a randomly varying number of tickets in flight and waited in random order.  Every
+    signature and attempt count must equal what the same batch gives when it runs alone."""
+    rs = np.random.default_rng(977)
+    levels = (2, 3, 5, 44)
+    keys = {lv: eng.batch_keygen(lv, rs.integers(0, 256, (40, 32), dtype=np.uint8)) for lv in levels}
+    pool = {}
+
+    def make(lv):
+        n = int(rs.choice([1, 7, 100, 900, 4000, 12000, 30000], p=[.1, .1, .2, .25, .2, .1, .05]))
+        per_task = n <= 40 and rs.random() < 0.3
+        k = None if per_task else int(rs.integers(0, 40))
+        lens = rs.integers(0, 90, n)
+        off = np.zeros(n + 1, np.uint64)
+        off[1:] = np.cumsum(lens)
+        flat = rs.integers(0, 256, int(off[-1]) + 1, dtype=np.uint8)
+        sk = keys[lv][1][:n] if per_task else keys[lv][1][k]
+        return lv, sk, flat, off
+
+    inflight, checked = [], 0
+    for it in range(240):
+        lv = int(rs.choice(levels, p=[.55, .2, .15, .1]))
+        job = make(lv)
+        want = eng.batch_sign(job[0], job[1], (job[2], job[3]), return_info=True) if it % 3 == 0 else None
+        depth = int(rs.integers(1, 13))
+        newest = max([h["ticket"] for h, _, _ in inflight], default=0) + (2 if want is not None else 1)
+        # (the ring holds 16 consecutive tickets: whatever was submitted 16 tickets ago must have
+        # been waited for; the synchronous call above consumed a ticket as well)
+        while len(inflight) >= depth or (inflight and newest - min(h["ticket"] for h, _, _ in inflight) >= 15):
+            old = min(range(len(inflight)), key=lambda i: inflight[i][0]["ticket"])
+            j = old if newest - inflight[old][0]["ticket"] >= 15 else int(rs.integers(0, len(inflight)))
+            h, jb, w = inflight.pop(j)
+            sigs, att, failed, st = eng.sign_wait(h)
+            assert not failed.any() and st["accepted_attempt_sum"] == int(att.sum())
+            if w is not None:
+                assert np.array_equal(sigs, w[0]) and np.array_equal(att, w[1])
+                checked += 1
+            else:  # every signature at least verifies under its key
+                pk = keys[jb[0]][0]
+                kk = pk[:len(att)] if jb[1].ndim == 2 else pk[[i for i in range(40) if np.array_equal(keys[jb[0]][1][i], jb[1])][0]]
+                assert eng.batch_verify(jb[0], kk, (jb[2], jb[3]), sigs).all()
+        inflight.append((eng.sign_submit(job[0], job[1], (job[2], job[3])), job, want))
+    for h, jb, w in inflight:
+        sigs, att, failed, _ = eng.sign_wait(h)
+        assert not failed.any()
+        if w is not None:
+            assert np.array_equal(sigs, w[0]) and np.array_equal(att, w[1])
+            checked += 1
+    assert checked >= 60
