@@ -200,6 +200,9 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
   if (const char* v = getenv("DLB_PIPE_CHUNK")) c->knob_pipe_chunk = (size_t)atol(v);
   if (const char* v = getenv("DLB_SIGN_PAD_SMEM")) c->knob_sign_pad_smem = (size_t)atol(v);
   if (const char* v = getenv("DLB_CARVEOUT")) c->knob_carveout = atoi(v);
+  if (const char* v = getenv("DLB_BOOST_THR")) c->knob_boost_thr = (unsigned)atoi(v);
+  if (const char* v = getenv("DLB_BOOST_DEPTH")) c->knob_boost_depth = (unsigned)atoi(v);
+  if (c->knob_boost_depth < 1 || c->knob_boost_depth > 8) c->knob_boost_depth = 4;
   if (const char* v = getenv("DLB_SIGN_OCC")) c->knob_sign_occ = (unsigned)atoi(v);
   if (const char* v = getenv("DLB_KEY_CACHE")) c->knob_key_cache = (size_t)atol(v);
   const int rc = create_resources(c);

@@ -144,6 +144,7 @@ struct dlb_ctx {
   // input / output / per-batch arenas come in sets; a ticket holds the lowest free set from
   // submission to wait, so a pipeline of depth d only ever touches (and warms) d sets
   bool set_busy[dlb::kRing] = {};
+  bool slot_launched[dlb::kRing] = {};   // sign_ev1[slot] has been recorded at least once
   int cur_set = 0;                       // set reserved for the submission in progress
   int sign_occ[12] = {};                 // resident CTAs per SM of k_sign_persistent<level, DBG>
   size_t sign_smem[12] = {};
@@ -156,6 +157,10 @@ struct dlb_ctx {
   unsigned dbg_max_attempt = 0;          // stage tests: smaller nonce space (0 = the scheme's)
   // tuning knobs, read from the environment once at dlb_create (profiles/: the sweeps)
   unsigned knob_spec_depth = 8;
+  // straggler boost (DLB_BOOST_THR failed attempts, 0 = off; DLB_BOOST_DEPTH extra nonces per round).
+  // Off by default: measured 54 -> 42 ms batch latency in a deep pipeline for -0.6 % throughput
+  // (profiles/r02_summary.md section 2)
+  unsigned knob_boost_thr = 0, knob_boost_depth = 4;
   size_t knob_chunk = 65536;      // keygen / verify device chunk (tasks)
   size_t knob_pipe_chunk = 8192;  // host transfer pipeline chunk (tasks)
   size_t knob_sign_pad_smem = 0;  // occupancy experiments

@@ -84,9 +84,11 @@ __global__ void __launch_bounds__(WARPS * 32)
 // ---- device-side scheduler state -----------------------------------------------------
 //
 // Batches in flight.  A submitted batch is described by one SignBatch in a device ring
-// (slot = ticket % kRing).  The scheduler kernel launched for ticket T serves tickets
-// T .. T + window - 1: its CTAs refill their open-task tables from ANY published batch of
-// that window before they speculate (the reference's pass 1 before pass 2,
+// (slot = ticket % kRing).  A CTA of the scheduler kernel launched for ticket T serves T and a
+// window of eight tickets that starts at the oldest younger batch with unclaimed tasks when the
+// CTA became resident (a kernel may wait a long time for residency behind older ones; anchoring
+// the window at T would hand it batches that were finished long ago): it refills its open-task
+// table from ANY published batch of that window before it speculates (the reference's pass 1 before pass 2,
 // scheduler.hpp:58-92, extended across batches -- the paper's in-flight batches,
 // PAPER.md:710-721), so the tail of one batch overlaps the body of the next ones.  Kernels of
 // consecutive tickets run on kLanes stream lanes with one scratch set each; a CTA never
@@ -110,6 +112,7 @@ struct BatchView {
   uint8_t* dbg_stage;
   int32_t bounds[3];
   unsigned plen;
+  unsigned ticket1, pad1;
   const uint8_t* sk_base;
   const uint8_t* msgs;
   const uint64_t* msg_off;
@@ -126,6 +129,8 @@ struct SignArgs {             // one scheduler-kernel instance
   unsigned slots;             // attempt slots a CTA fills with speculation (<= 128): small batches are
                               // spread over more CTAs with fewer slots each to cut round latency
   int single_round;           // stage-test mode: exactly one round, then fail open tasks
+  unsigned boost_thr;         // a task past this many failed attempts is a straggler (0 = no boost)
+  unsigned boost_depth;       // extra nonces a straggler runs per round while work is queued
   uint32_t* trace;            // nullable: per-round records of 8 words (dlb_round_trace)
   unsigned trace_cap;
   uint32_t* alog;             // nullable: per executed attempt 4 words (dlb_assignment)
@@ -182,7 +187,9 @@ struct SignSmem {
   unsigned bcnt[kWindow];          // open tasks held per batch
   unsigned bfin[kWindow];          // tasks of each batch finished in the current round
   unsigned seen;                   // bit i: bv[i] loaded
+  unsigned first;                  // window position i >= 1 is ticket first + i - 1 (position 0: own)
   unsigned U, Uold, span, need_hash;
+  unsigned B;                      // tasks (table front) that share the slots behind the first U
   unsigned cursor2, cursor4;  // next unclaimed slot of stages S2 / S4 (warps pull slots)
   unsigned r_on, r_spec;      // this round's assigned / speculative slots (trace)
   unsigned rounds;            // rounds this CTA has run
@@ -521,6 +528,20 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
     sm.rounds = 0;
   }
   if (tid < kWindow) sm.bcnt[tid] = sm.bfin[tid] = 0;
+  if (warp == 0) {
+    // Window anchor: the OLDEST younger batch that still has unclaimed tasks (a batch whose own
+    // kernel is still waiting for residency must not be left to it alone), else the first ticket
+    // that has not been published yet.  gate = ticket + 1 of the batch in a ring slot.
+    unsigned g1 = 0, cand = 0xFFFFFFFFu;
+    if (lane < kRing) {
+      const SignBatch* g = a.ring + lane;
+      g1 = ld_acquire(&g->gate);
+      if (g1 > a.ticket + 1u && ld_relaxed(&g->head) < g->n) cand = g1 - 1u;
+    }
+    g1 = __reduce_max_sync(0xffffffffu, g1);    // newest published ticket + 1 (>= own + 1)
+    cand = __reduce_min_sync(0xffffffffu, cand);
+    if (lane == 0) sm.first = cand != 0xFFFFFFFFu ? cand : max(g1, a.ticket + 1u);
+  }
   __syncthreads();
 
   while (true) {
@@ -536,12 +557,27 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
         sm.Uold = U;
         sm.need_hash = 0;
       }
-      if (U < (unsigned)kSignThreads && !(a.single_round && sm.rounds > 0)) {
+      // Stragglers.  With work queued every slot runs a first attempt, so a task deep in its
+      // rejection loop advances one nonce per full-length round and its batch completes long
+      // after its siblings (a pipeline of bounded depth then stalls on it).  The table is ordered
+      // by age; the tasks at its front that are past boost_thr failed attempts keep boost_depth
+      // slots each free of new work and run that many extra nonces per round -- a few percent of the
+      // slots (0.765^16 = 1.4 % of the tasks are that deep) for half the tail.
+      unsigned n_s = 0;
+      if (a.boost_thr && U) {
+        const bool deep = (unsigned)lane < U && sm.unext[lane] >= a.boost_thr && sm.bv[sm.ubatch[lane]].spec_depth > 0;
+        const unsigned m = __ballot_sync(0xffffffffu, deep);
+        n_s = m == 0xffffffffu ? 32u : (unsigned)__ffs(~m) - 1u;  // length of the leading run
+        n_s = min(n_s, 32u / a.boost_depth);
+      }
+      const unsigned cap = (unsigned)kSignThreads - n_s * a.boost_depth;
+      if (U < cap && !(a.single_round && sm.rounds > 0)) {
         bool avail = false;
         if ((unsigned)lane < a.window) {
-          SignBatch* g = a.ring + ((a.ticket + lane) % kRing);
+          const unsigned ticket = lane == 0 ? a.ticket : sm.first + (unsigned)lane - 1u;
+          SignBatch* g = a.ring + (ticket % kRing);
           bool seen = (sm.seen >> lane) & 1u;
-          if (!seen && ld_acquire(&g->gate) == a.ticket + lane + 1u && g->level == P::LEVEL &&
+          if (!seen && ld_acquire(&g->gate) == ticket + 1u && g->level == P::LEVEL &&
               (lane == 0 || !g->exclusive)) {
             BatchView& v = sm.bv[lane];
             v.n = g->n;
@@ -564,6 +600,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
             v.bounds[1] = g->bounds[1];
             v.bounds[2] = g->bounds[2];
             v.plen = g->plen;
+            v.ticket1 = ticket + 1u;
             v.sk_base = g->sk_base;
             v.msgs = g->msgs;
             v.msg_off = g->msg_off;
@@ -577,11 +614,11 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
           if (seen) avail = ld_relaxed(&g->head) < sm.bv[lane].n && sm.bcnt[lane] < sm.bv[lane].tcap;
         }
         unsigned m = __ballot_sync(0xffffffffu, avail);
-        while (m && U < (unsigned)kSignThreads) {
+        while (m && U < cap) {
           const int i = __ffs(m) - 1;
           m &= m - 1;
           const BatchView& v = sm.bv[i];
-          const unsigned want = min(v.tcap - sm.bcnt[i], (unsigned)kSignThreads - U);
+          const unsigned want = min(v.tcap - sm.bcnt[i], cap - U);
           unsigned base = 0, got = 0;
           if (lane == 0) {
             base = atomicAdd(&v.g->head, want);
@@ -606,10 +643,14 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
         }
         if (lane == 0) sm.U = U;
       }
+      // the table is full up to the cap: the spare slots belong to the stragglers; otherwise (queues
+      // dry) every open task shares them breadth first, the reference's pass 2
+      if (lane == 0) sm.B = (n_s && U >= cap) ? n_s : U;
     }
     __syncthreads();
     const unsigned U = sm.U;
     if (U == 0) break;
+    const unsigned B = sm.B;
 
     // ---- S0: mu = H(tr || M), rho' = H(K || mu) of the tasks just claimed (scheme.hpp:240-248)
     if (sm.need_hash) {
@@ -629,16 +670,22 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       __syncthreads();
     }
 
-    // ---- schedule: slot s -> open task s % U, depth s / U (scheduler.hpp:58-92) ------
+    // ---- schedule (scheduler.hpp:58-92): pass 1 = slot u runs open task u's next nonce; pass 2 =
+    // the slots behind the table run further nonces, breadth first over the first B tasks --------
     // Depth 0 (pass 1) always runs.  Speculative depths (pass 2) only use the first a.slots
     // slots and only exist when the queues could not fill the table, because the refill above
     // comes first.
     {
-      const unsigned u = tid % U, depth = tid / U;
+      // slots [0, U): depth 0 of every open task; slot U + j: task j mod B at depth 1 + j div B
+      const unsigned j = (unsigned)tid >= U ? (unsigned)tid - U : 0u;
+      const unsigned u = (unsigned)tid < U ? (unsigned)tid : j % B;
+      const unsigned depth = (unsigned)tid < U ? 0u : 1u + j / B;
       const unsigned bi = sm.ubatch[u];
       const BatchView& v = sm.bv[bi];
       const unsigned att = sm.unext[u] + depth;
-      const bool on = (depth == 0 || ((unsigned)tid < a.slots && depth <= v.spec_depth)) &&
+      const bool boosted = B != U;  // spare slots reserved for stragglers, not the kernel's pass-2 budget
+      const bool on = (depth == 0 || (boosted ? depth <= min(a.boost_depth, v.spec_depth)
+                                              : ((unsigned)tid < a.slots && depth <= v.spec_depth))) &&
                       att <= v.max_attempt;
       const unsigned task = sm.utask[u];
       sm.slot_task[tid] = on ? task : kNoSlot;
@@ -813,7 +860,8 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       const BatchView& v = sm.bv[bi];
       int win = -1;
       unsigned ran = 0;
-      for (unsigned s = tid; s < (unsigned)kSignThreads; s += U) {
+      for (unsigned s = tid; s < (unsigned)kSignThreads; s = s < U ? U + s : s + B) {
+        if (s >= U && (unsigned)tid >= B) break;  // only the first B tasks own slots behind the table
         if (sm.slot_task[s] == kNoSlot) break;
         ++ran;
         if (sm.slot_valid[s]) {
@@ -907,7 +955,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
         if (old + f == v.n) {
           atomicMax(&v.g->t_last_exit, now);
           __threadfence_system();
-          *v.g->host_flag = a.ticket + tid + 1u;
+          *v.g->host_flag = v.ticket1;
         }
       }
       if (tid == 0) {
@@ -1098,6 +1146,12 @@ int sign_reserve(dlb_ctx* c, unsigned* ticket, cudaStream_t* pub) {
   DLB_TRY(sign_state_init(c));
   const unsigned t = c->next_ticket;
   if (c->tickets[t % kRing].active) return DLB_E_BUSY;  // kRing batches in flight: wait for the oldest first
+  // A ring slot is rewritten only when the scheduler kernel of the ticket that used it last
+  // (16 tickets ago) has exited.  By induction every kernel with an older ticket has exited too,
+  // and only those can hold a cached view of that slot's previous batch (a CTA's window starts
+  // at or behind its own ticket): no resident CTA can mistake the new batch's work queue for
+  // the old one's.  In a steady flow that kernel retired several tickets ago.
+  if (c->slot_launched[t % kRing]) DLB_CUDA_CHECK(cudaEventSynchronize(c->sign_ev1[t % kRing]));
   *ticket = t;
   *pub = c->sign_pub;
   cudaStream_t* lane = pub;
@@ -1263,6 +1317,8 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   a.window = h.exclusive ? 1u : (unsigned)kWindow;
   a.slots = (unsigned)slots_per;
   a.single_round = io.single_round;
+  a.boost_thr = io.single_round ? 0u : c->knob_boost_thr;
+  a.boost_depth = c->knob_boost_depth ? c->knob_boost_depth : 1u;
   a.log = c->d_log;
   if (c->trace_cap && !io.single_round) {
     DLB_TRY(dalloc(c, "s.trace", c->trace_cap * 8, &a.trace));
@@ -1288,6 +1344,7 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   cudaEventRecord(c->sign_ev0[slot], lane);
   k_sign_persistent<P, DBG><<<(unsigned)grid, kSignThreads, smem_bytes, lane>>>(a);
   cudaEventRecord(c->sign_ev1[slot], lane);
+  c->slot_launched[slot] = true;
   cudaEventRecord(c->lane_done[ln], lane);
   c->lane_used[ln] = true;
   c->launches += 1;
@@ -1340,7 +1397,13 @@ int sign_wait(dlb_ctx* c, unsigned ticket, dlb_sign_stats* stats, bool drain) {
         if (e == cudaErrorNotReady) idle = false;
         else if (e != cudaSuccess) return -1000 - (int)e;
       }
-      if (idle && *flag != ticket + 1u) return DLB_E_INTERNAL;
+      if (idle && *flag != ticket + 1u) {
+        SignBatch hq;  // what the device thinks of the batch, for the bug report
+        if (cudaMemcpy(&hq, c->d_ring + slot, sizeof hq, cudaMemcpyDeviceToHost) == cudaSuccess)
+          fprintf(stderr, "dilithium-b200: ticket %u never completed: n %u head %u done %u gate %u failed %llu\n",
+                  ticket, hq.n, hq.head, hq.done, hq.gate, hq.failed);
+        return DLB_E_INTERNAL;
+      }
     }
 #if defined(__x86_64__)
     __builtin_ia32_pause();

@@ -7,7 +7,7 @@
 namespace dlb {
 
 constexpr int kRing = 16;    // batch descriptors per context = tickets that may be in flight
-constexpr int kWindow = 8;   // batches one scheduler kernel may serve (its own and the next 7)
+constexpr int kWindow = 9;   // batches one scheduler CTA may serve: its kernel's own and eight more (see sign.cu)
 constexpr int kLanes = 4;    // stream lanes / scratch sets; the kernel of ticket T runs on lane T % kLanes
 
 struct SignBatch {

@@ -31,7 +31,8 @@ def run(depth_now, steps_now, show=False):
 
     def wait(t):
         st = SignStats()
-        assert lib.dlb_sign_wait(ctx, t, C.byref(st)) == 0
+        rc = lib.dlb_sign_wait(ctx, t, C.byref(st))
+        assert rc == 0, "dlb_sign_wait: %d" % rc
         stats.append(st)
     for i in range(steps_now):
         if len(inflight) >= depth_now:
