@@ -38,7 +38,7 @@ extern "C" {
 #define DLB_E_LEVEL (-2)
 #define DLB_E_KEY (-3)
 #define DLB_E_NOMEM (-4)
-#define DLB_E_BUSY (-5)     /* the batch submitted 16 tickets ago is still un-waited: wait for it first */
+#define DLB_E_BUSY (-5)     /* the batch submitted 32 tickets ago is still un-waited: wait for it first */
 #define DLB_E_INTERNAL (-6) /* a submitted batch was never completed (device fault) */
 
 typedef struct dlb_ctx dlb_ctx;
@@ -110,7 +110,8 @@ long long dlb_get_assignment_log(dlb_ctx* ctx, dlb_assignment* out, size_t max_r
 
 /* FIPS 204 context string for the ML-DSA levels (44 / 65 / 87): signing and verification
  * hash M' = 0 || len || ctx || M.  len <= 255; the default is the empty string.  Sticky per
- * context until changed; ignored by the round-3 levels. */
+ * context until changed; ignored by the round-3 levels.  DLB_E_BUSY while signing batches are in
+ * flight (they hash their tasks with the current string). */
 int dlb_set_mldsa_context(dlb_ctx* ctx, const uint8_t* context_string, size_t len);
 
 /* Several GPUs of one box: the transport limit is host memory and PCIe, so the host thread that
@@ -184,7 +185,7 @@ int dlb_verify_batch_keyed(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t
  * tool's engines, tools/dilithium_cli.cpp:309-345).  dlb_sign_submit enqueues a batch and
  * returns at once with a ticket; dlb_sign_wait blocks until that batch is complete and fills
  * the outputs.  Tickets are numbered consecutively (synchronous sign calls take one too) and the
- * engine keeps 16 consecutive tickets: a submission returns DLB_E_BUSY while the batch submitted 16
+ * engine keeps 32 consecutive tickets: a submission returns DLB_E_BUSY while the batch submitted 32
  * tickets earlier has not been waited for.  The device
  * scheduler is shared: CTAs that run out of tasks of one batch claim tasks of the next
  * submitted batches (of the same level) before they speculate, so the rejection-loop tail of a

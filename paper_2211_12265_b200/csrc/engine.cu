@@ -332,6 +332,8 @@ long long dlb_get_trace(dlb_ctx* c, dlb_round_trace* out, size_t max_records) {
 
 int dlb_set_mldsa_context(dlb_ctx* c, const uint8_t* ctx_bytes, size_t len) {
   if (!c || len > 255 || (len && !ctx_bytes)) return DLB_E_ARG;  // FIPS 204: |ctx| <= 255
+  for (int r = 0; r < kRing; ++r)  // batches in flight hash their tasks with the current string
+    if (c->tickets[r].active) return DLB_E_BUSY;
   c->mldsa_pfx[0] = 0;
   c->mldsa_pfx[1] = (uint8_t)len;
   if (len) memcpy(c->mldsa_pfx + 2, ctx_bytes, len);

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 //
 // Batches in flight.  A submitted batch is described by one SignBatch in a device ring
 // (slot = ticket % kRing).  A CTA of the scheduler kernel launched for ticket T serves T and a
-// window of eight tickets that starts at the oldest younger batch with unclaimed tasks when the
+// window of 24 tickets that starts at the oldest younger batch with unclaimed tasks when the
 // CTA became resident (a kernel may wait a long time for residency behind older ones; anchoring
 // the window at T would hand it batches that were finished long ago): it refills its open-task
 // table from ANY published batch of that window before it speculates (the reference's pass 1 before pass 2,
@@ -96,9 +96,12 @@ __global__ void __launch_bounds__(WARPS * 32)
 // unclaimed tasks.  Completion is per batch (SignBatch::done reaching n raises a flag in
 // mapped host memory), not per kernel.
 
-// what a CTA keeps of a batch it serves (window position i <-> ticket own + i)
+// what a CTA keeps in shared memory of a batch it serves (window position i): the fields the
+// stages read per slot.  Everything else (output arrays of the commit step, the inputs of the
+// digest stage, test hooks) is read from the descriptor itself when needed -- immutable, and
+// fetched behind the acquire that made the batch visible.
 struct BatchView {
-  unsigned n, tcap, max_attempt, spec_depth, key_stride, pad;
+  unsigned n, tcap, max_attempt, spec_depth, key_stride, ticket1;
   const uint64_t* mu;
   const uint64_t* rho_prime;
   const uint32_t* kappa0;
@@ -106,20 +109,7 @@ struct BatchView {
   const int32_t* shat;
   const uint32_t* key_idx;
   uint8_t* sigs;
-  uint32_t* attempts_out;
-  uint8_t* failed_out;
-  uint8_t* dbg_ctilde;
-  uint8_t* dbg_stage;
-  int32_t bounds[3];
-  unsigned plen;
-  unsigned ticket1, pad1;
-  const uint8_t* sk_base;
-  const uint8_t* msgs;
-  const uint64_t* msg_off;
-  const uint8_t* pfx;
-  uint64_t* mu_w;
-  uint64_t* rp_w;
-  SignBatch* g;  // the descriptor in the ring (mutable counters)
+  SignBatch* g;  // the descriptor in the ring (cold fields, mutable counters)
 };
 
 struct SignArgs {             // one scheduler-kernel instance
@@ -577,7 +567,9 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
           const unsigned ticket = lane == 0 ? a.ticket : sm.first + (unsigned)lane - 1u;
           SignBatch* g = a.ring + (ticket % kRing);
           bool seen = (sm.seen >> lane) & 1u;
-          if (!seen && ld_acquire(&g->gate) == ticket + 1u && g->level == P::LEVEL &&
+          // (a CTA never looks kRing - 1 or more tickets past its own: that slot may be its own batch's)
+          if (!seen && ticket - a.ticket <= (unsigned)kRing - 2u && ld_acquire(&g->gate) == ticket + 1u &&
+              g->level == P::LEVEL &&
               (lane == 0 || !g->exclusive)) {
             BatchView& v = sm.bv[lane];
             v.n = g->n;
@@ -585,6 +577,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
             v.max_attempt = g->max_attempt;
             v.spec_depth = g->spec_depth;
             v.key_stride = g->key_stride;
+            v.ticket1 = ticket + 1u;
             v.mu = g->mu;
             v.rho_prime = g->rho_prime;
             v.kappa0 = g->kappa0;
@@ -592,21 +585,6 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
             v.shat = g->shat;
             v.key_idx = g->key_idx;
             v.sigs = g->sigs;
-            v.attempts_out = g->attempts_out;
-            v.failed_out = g->failed_out;
-            v.dbg_ctilde = g->dbg_ctilde;
-            v.dbg_stage = g->dbg_stage;
-            v.bounds[0] = g->bounds[0];
-            v.bounds[1] = g->bounds[1];
-            v.bounds[2] = g->bounds[2];
-            v.plen = g->plen;
-            v.ticket1 = ticket + 1u;
-            v.sk_base = g->sk_base;
-            v.msgs = g->msgs;
-            v.msg_off = g->msg_off;
-            v.pfx = g->pfx;
-            v.mu_w = g->mu_w;
-            v.rp_w = g->rp_w;
             v.g = g;
             atomicOr(&sm.seen, 1u << lane);
             seen = true;
@@ -629,7 +607,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
               atomicMin(&v.g->t_first_start, now);
               atomicMax(&v.g->t_last_start, now);
               sm.bcnt[i] += got;
-              if (v.msg_off) sm.need_hash = 1;
+              if (v.g->msg_off) sm.need_hash = 1;
             }
           }
           base = __shfl_sync(0xffffffffu, base, 0);
@@ -656,15 +634,18 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
     if (sm.need_hash) {
       if ((unsigned)tid >= sm.Uold && (unsigned)tid < U) {
         const BatchView& v = sm.bv[sm.ubatch[tid]];
-        if (v.msg_off) {
+        const SignBatch* g = v.g;
+        const uint64_t* msg_off = g->msg_off;
+        if (msg_off) {
           const unsigned task = sm.utask[tid];
           const size_t kt = v.key_idx ? (size_t)ld_weak(v.key_idx + task) : (size_t)task * v.key_stride;
-          const uint8_t* sk = v.sk_base + kt * S::SK;
-          const uint64_t m0 = ld_weak(v.msg_off + task), m1 = ld_weak(v.msg_off + task + 1);
+          const uint8_t* sk = g->sk_base + kt * S::SK;
+          const uint64_t m0 = ld_weak(msg_off + task), m1 = ld_weak(msg_off + task + 1);
+          uint64_t* rp_w = g->rp_w;
           hash_mu_task<Hashing<P>::MLDSA, false>(
               reinterpret_cast<const uint64_t*>(sk + 64), reinterpret_cast<const uint64_t*>(sk + 32),
-              v.pfx, v.plen, v.msgs + m0, (size_t)(m1 - m0), v.mu_w + (size_t)task * 8,
-              v.rp_w ? v.rp_w + (size_t)task * 8 : nullptr);
+              g->pfx, g->plen, g->msgs + m0, (size_t)(m1 - m0), g->mu_w + (size_t)task * 8,
+              rp_w ? rp_w + (size_t)task * 8 : nullptr);
         }
       }
       __syncthreads();
@@ -837,11 +818,11 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
             wbuf + (size_t)s * Z::W_SLOT, nx < kSignThreads ? c8buf + (size_t)nx * kN : nullptr,
             ctbuf + s * CTW, v.shat + key_of(s) * ((P::L + 2 * P::K) * kN),
             direct ? v.sigs + (size_t)sm.slot_task[s] * S::SIG : staging + (size_t)s * Z::SIG_PAD, direct,
-            v.bounds);
+            DBG ? v.g->bounds : nullptr);
         if (lane == 0) {
           sm.slot_valid[s] = rej == 0 ? 1 : 0;
           // RejectStage of the reference (scheme.hpp:34): 0 z, 1 r0, 2 c t0, 3 hint weight; 255 accepted
-          if (DBG && v.dbg_stage) v.dbg_stage[sm.slot_task[s]] = rej ? (uint8_t)(rej - 1) : (uint8_t)255;
+          if (DBG && v.g->dbg_stage) v.g->dbg_stage[sm.slot_task[s]] = rej ? (uint8_t)(rej - 1) : (uint8_t)255;
         }
         s = nx;
         par ^= 1;
@@ -869,22 +850,23 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
           break;
         }
       }
-      if (v.dbg_ctilde) {
+      const SignBatch* g = v.g;
+      if (uint8_t* dbg_ct = g->dbg_ctilde) {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(ctbuf + tid * CTW);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(v.dbg_ctilde + (size_t)task * Hashing<P>::CT);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(dbg_ct + (size_t)task * Hashing<P>::CT);
         for (int w = 0; w < 2 * CTW; ++w) dst[w] = src[w];
       }
       if (win >= 0) {
         const unsigned ordinal = sm.slot_attempt[win] + 1;
-        if (v.attempts_out) v.attempts_out[task] = ordinal;
-        if (v.failed_out) v.failed_out[task] = 0;
+        if (uint32_t* ao = g->attempts_out) ao[task] = ordinal;
+        if (uint8_t* fo = g->failed_out) fo[task] = 0;
         atomicAdd(&v.g->accepted_sum, (unsigned long long)ordinal);
       } else {
         next += ran;
         if (next > v.max_attempt || a.single_round) {
           win = -2;  // nonce space exhausted (scheduler.hpp:122-128)
-          if (v.attempts_out) v.attempts_out[task] = 0;
-          if (v.failed_out) v.failed_out[task] = 1;
+          if (uint32_t* ao = g->attempts_out) ao[task] = 0;
+          if (uint8_t* fo = g->failed_out) fo[task] = 1;
           atomicAdd(&v.g->failed, 1ull);
         }
       }

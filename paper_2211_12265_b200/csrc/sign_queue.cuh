@@ -6,8 +6,8 @@
 
 namespace dlb {
 
-constexpr int kRing = 16;    // batch descriptors per context = tickets that may be in flight
-constexpr int kWindow = 9;   // batches one scheduler CTA may serve: its kernel's own and eight more (see sign.cu)
+constexpr int kRing = 32;    // batch descriptors per context = consecutive tickets that may be in flight
+constexpr int kWindow = 25;  // batches one scheduler CTA may serve: its kernel's own and 24 more (see sign.cu)
 constexpr int kLanes = 4;    // stream lanes / scratch sets; the kernel of ticket T runs on lane T % kLanes
 
 struct SignBatch {

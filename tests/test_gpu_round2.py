@@ -131,7 +131,7 @@ def test_nonce_space_exhaustion_reports_failed_tasks(eng, oracle, level):
 
 def test_batches_in_flight_mixed_levels_and_keys(eng, oracle):
     """dlb_sign_submit / dlb_sign_wait: sixteen batches of different sizes, levels, keys and key
-    modes in flight at once, waited out of order -- every byte as if each had run alone."""
+    modes (plus sixteen single-task batches, filling the ring of 32) in flight at once, waited out of order -- every byte as if each had run alone."""
     rng = mt19937_64(31415)
     shapes = [(2, 3000, "shared"), (3, 700, "shared"), (2, 1, "shared"), (5, 900, "per_task"),
               (2, 5000, "table"), (2, 64, "shared"), (3, 2000, "table"), (44, 800, "shared"),
@@ -154,8 +154,11 @@ def test_batches_in_flight_mixed_levels_and_keys(eng, oracle):
                                     return_info=True))
     handles = [eng.sign_submit(level, sks[0] if mode == "shared" else sks, (flat, off), key_idx=kidx)
                for level, n, mode, sks, flat, off, kidx in jobs]
-    with pytest.raises(Exception):  # the ring is full: a seventeenth submission is refused
+    extra = [eng.sign_submit(2, jobs[2][3][0], (jobs[2][4], jobs[2][5])) for _ in range(16)]
+    with pytest.raises(Exception):  # the ring holds 32 consecutive tickets: the 33rd submission is refused
         eng.sign_submit(2, jobs[0][3][0], (jobs[0][4], jobs[0][5]))
+    for h in extra[::-1]:
+        assert np.array_equal(eng.sign_wait(h)[0], alone[2][0])
     order = [7, 0, 15, 3, 8, 1, 2, 12, 4, 5, 6, 9, 10, 11, 13, 14]
     for j in order:
         sigs, att, failed, st = eng.sign_wait(handles[j])
@@ -230,13 +233,13 @@ def test_in_flight_stress_random_pipeline(eng):
         lv = int(rs.choice(levels, p=[.55, .2, .15, .1]))
         job = make(lv)
         want = eng.batch_sign(job[0], job[1], (job[2], job[3]), return_info=True) if it % 3 == 0 else None
-        depth = int(rs.integers(1, 13))
+        depth = int(rs.integers(1, 25))
         newest = max([h["ticket"] for h, _, _ in inflight], default=0) + (2 if want is not None else 1)
-        # (the ring holds 16 consecutive tickets: whatever was submitted 16 tickets ago must have
+        # (the ring holds 32 consecutive tickets: whatever was submitted 32 tickets ago must have
         # been waited for; the synchronous call above consumed a ticket as well)
-        while len(inflight) >= depth or (inflight and newest - min(h["ticket"] for h, _, _ in inflight) >= 15):
+        while len(inflight) >= depth or (inflight and newest - min(h["ticket"] for h, _, _ in inflight) >= 31):
             old = min(range(len(inflight)), key=lambda i: inflight[i][0]["ticket"])
-            j = old if newest - inflight[old][0]["ticket"] >= 15 else int(rs.integers(0, len(inflight)))
+            j = old if newest - inflight[old][0]["ticket"] >= 31 else int(rs.integers(0, len(inflight)))
             h, jb, w = inflight.pop(j)
             sigs, att, failed, st = eng.sign_wait(h)
             assert not failed.any() and st["accepted_attempt_sum"] == int(att.sum())
