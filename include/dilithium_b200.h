@@ -113,6 +113,13 @@ long long dlb_get_assignment_log(dlb_ctx* ctx, dlb_assignment* out, size_t max_r
  * context until changed; ignored by the round-3 levels.  DLB_E_BUSY while signing batches are in
  * flight (they hash their tasks with the current string). */
 int dlb_set_mldsa_context(dlb_ctx* ctx, const uint8_t* context_string, size_t len);
+/* HashML-DSA (FIPS 204 Alg. 4 / 5, the pre-hash variant): with a hash OID set (the DER encoding,
+ * 11 bytes for the SHA-2 / SHA-3 / SHAKE identifiers of the standard, at most 16) signing and
+ * verification hash M' = 1 || len || ctx || OID || m, where the "message" m each task passes is the
+ * digest PH(M) the caller computed with that hash.  oid_len == 0 returns to pure ML-DSA
+ * (dlb_set_mldsa_context).  Sticky per context; DLB_E_BUSY while signing batches are in flight. */
+int dlb_set_mldsa_prehash(dlb_ctx* ctx, const uint8_t* context_string, size_t len, const uint8_t* oid,
+                          size_t oid_len);
 
 /* Several GPUs of one box: the transport limit is host memory and PCIe, so the host thread that
  * drives a GPU -- and the pinned staging it allocates -- should live on that GPU's NUMA node.

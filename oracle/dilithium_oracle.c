@@ -657,19 +657,29 @@ int orc_sign_attempt_bounded(int level, const uint8_t* sk, const uint8_t mu[64],
 /* FIPS 204 context string (ML-DSA levels only): M' = 0 || len || ctx || M */
 static uint8_t g_ctx[255];
 static size_t g_ctx_len = 0;
+static uint8_t g_oid[16];
+static size_t g_oid_len = 0; /* > 0: HashML-DSA, FIPS 204 Alg. 4 / 5 (messages are digests PH(M)) */
 int orc_set_mldsa_context(const uint8_t* ctx, size_t len) {
   if (len > 255) return -1;
   if (len) memcpy(g_ctx, ctx, len);
   g_ctx_len = len;
+  g_oid_len = 0;
+  return 0;
+}
+int orc_set_mldsa_prehash(const uint8_t* ctx, size_t len, const uint8_t* oid, size_t oid_len) {
+  if (orc_set_mldsa_context(ctx, len) != 0 || oid_len > 16) return -1;
+  if (oid_len) memcpy(g_oid, oid, oid_len);
+  g_oid_len = oid_len;
   return 0;
 }
 static void mldsa_mu(uint8_t mu[64], const uint8_t tr[64], const uint8_t* msg, size_t msglen) {
   xof_t x;
-  const uint8_t pfx[2] = {0, (uint8_t)g_ctx_len};
+  const uint8_t pfx[2] = {(uint8_t)(g_oid_len ? 1 : 0), (uint8_t)g_ctx_len};
   xof_init(&x, 136);
   xof_absorb(&x, tr, 64);
   xof_absorb(&x, pfx, 2);
   xof_absorb(&x, g_ctx, g_ctx_len);
+  xof_absorb(&x, g_oid, g_oid_len);
   xof_absorb(&x, msg, msglen);
   xof_squeeze(&x, mu, 64);
 }

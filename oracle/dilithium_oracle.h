@@ -67,6 +67,8 @@ int32_t orc_use_hint(int h, int32_t r, int32_t gamma2);
 /* FIPS 204 context string used by sign / verify at levels 44 / 65 / 87 (len <= 255; default
  * empty; process-wide, not thread-safe -- tests only) */
 int orc_set_mldsa_context(const uint8_t* ctx, size_t len);
+/* HashML-DSA (FIPS 204 Alg. 4 / 5): M' = 1 || len || ctx || OID || PH(M); messages are digests */
+int orc_set_mldsa_prehash(const uint8_t* ctx, size_t len, const uint8_t* oid, size_t oid_len);
 
 /* scheme.hpp:68-104 */
 int orc_keygen(int level, const uint8_t zeta[32], uint8_t* pk, uint8_t* sk);

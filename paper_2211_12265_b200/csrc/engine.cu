@@ -342,6 +342,20 @@ int dlb_set_mldsa_context(dlb_ctx* c, const uint8_t* ctx_bytes, size_t len) {
   return 0;
 }
 
+int dlb_set_mldsa_prehash(dlb_ctx* c, const uint8_t* ctx_bytes, size_t len, const uint8_t* oid, size_t oid_len) {
+  if (!c || len > 255 || (len && !ctx_bytes) || oid_len > 16 || (oid_len && !oid)) return DLB_E_ARG;
+  if (oid_len == 0) return dlb_set_mldsa_context(c, ctx_bytes, len);
+  for (int r = 0; r < kRing; ++r)
+    if (c->tickets[r].active) return DLB_E_BUSY;
+  c->mldsa_pfx[0] = 1;  // FIPS 204 Alg. 4 / 5: M' = 1 || |ctx| || ctx || OID || PH(M)
+  c->mldsa_pfx[1] = (uint8_t)len;
+  if (len) memcpy(c->mldsa_pfx + 2, ctx_bytes, len);
+  memcpy(c->mldsa_pfx + 2 + len, oid, oid_len);
+  c->mldsa_plen = 2 + (unsigned)len + (unsigned)oid_len;
+  c->mldsa_pfx_dirty = true;
+  return 0;
+}
+
 namespace {
 
 // "/sys/bus/pci/devices/<domain:bus:dev.fn>/<leaf>" of a CUDA device, first line

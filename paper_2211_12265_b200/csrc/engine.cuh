@@ -118,7 +118,7 @@ struct dlb_ctx {
   unsigned long long trace_count = 0;  // records the last sign call produced
   // FIPS 204 message prefix 0 || |ctx| || ctx (2..257 bytes) for the ML-DSA levels: host copy
   // and its device mirror; the default is the empty context string
-  uint8_t mldsa_pfx[264] = {0, 0};
+  uint8_t mldsa_pfx[288] = {0, 0};       // + an 11-byte hash OID in the pre-hash variant (HashML-DSA)
   unsigned mldsa_plen = 2;
   uint8_t* d_mldsa_pfx = nullptr;
   bool mldsa_pfx_dirty = true;

@@ -61,6 +61,7 @@ def load_library():
         "dlb_measure_int32_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "dlb_measure_imad_hi_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "dlb_set_mldsa_context": (C.c_int, [vp, _u8p, sz]),
+        "dlb_set_mldsa_prehash": (C.c_int, [vp, _u8p, sz, _u8p, sz]),
         "dlb_set_trace": (C.c_int, [vp, sz]),
         "dlb_get_trace": (C.c_longlong, [vp, vp, sz]),
         "dlb_bind_thread_to_device": (C.c_int, [C.c_int]),
@@ -118,7 +119,7 @@ EXPORTED_SYMBOLS = [
     "dlb_dbg_sample_in_ball", "dlb_dbg_rounding", "dlb_dbg_ntt", "dlb_dbg_sign_attempt",
     "dlb_dbg_sign_attempt_bounded", "dlb_dbg_set_max_attempt", "dlb_set_assignment_log",
     "dlb_get_assignment_log", "dlb_sign_submit", "dlb_sign_submit_dev", "dlb_sign_wait",
-    "dlb_bind_thread_to_device", "dlb_device_numa_node",
+    "dlb_bind_thread_to_device", "dlb_device_numa_node", "dlb_set_mldsa_prehash",
 ]
 
 
@@ -229,6 +230,15 @@ class Engine:
         buf = np.frombuffer(bytes(context), np.uint8)
         self._chk(self.lib.dlb_set_mldsa_context(self.ctx, buf.ctypes.data_as(_u8p) if len(buf) else None,
                                                  len(buf)), "dlb_set_mldsa_context")
+
+    def set_mldsa_prehash(self, oid=b"", context=b""):
+        """HashML-DSA (FIPS 204 Alg. 4 / 5): with a hash OID (DER bytes) the messages passed to sign /
+        verify are the digests PH(M); an empty OID returns to pure ML-DSA."""
+        cb = np.frombuffer(bytes(context), np.uint8)
+        ob = np.frombuffer(bytes(oid), np.uint8)
+        self._chk(self.lib.dlb_set_mldsa_prehash(self.ctx, cb.ctypes.data_as(_u8p) if len(cb) else None, len(cb),
+                                                 ob.ctypes.data_as(_u8p) if len(ob) else None, len(ob)),
+                  "dlb_set_mldsa_prehash")
 
     # ---- batch.hpp:159-166
     def batch_keygen(self, level, zetas):

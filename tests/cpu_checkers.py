@@ -251,6 +251,13 @@ class Oracle(_Checker):
     prefix = "orc_"
 
 
+    def set_mldsa_prehash(self, oid=b"", ctx=b""):
+        """HashML-DSA mode of the oracle (FIPS 204 Alg. 4 / 5); an empty OID returns to pure ML-DSA."""
+        fn = self.lib.orc_set_mldsa_prehash
+        fn.restype, fn.argtypes = C.c_int, [_u8p, C.c_size_t, _u8p, C.c_size_t]
+        assert fn(_p(bytes(ctx)) if ctx else None, len(ctx), _p(bytes(oid)) if oid else None, len(oid)) == 0
+
+
 class RefStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in
                 ("rounds", "attempts", "speculative", "idle_slot_rounds", "accepted_attempt_sum",

@@ -134,3 +134,39 @@ def test_context_strings_match_oracle(eng, oracle, level):
     finally:
         eng.set_mldsa_context(b"")
         oracle.set_mldsa_context(b"")
+
+
+def test_hash_mldsa_prehash_mode(oracle):
+    """HashML-DSA (FIPS 204 Alg. 4 / 5): M' = 1 || |ctx| || ctx || OID || PH(M).  With the SHA-512 and
+    SHAKE256 OIDs set, signatures over caller-computed digests equal the oracle's pre-hash mode byte
+    for byte, verify, differ from pure ML-DSA over the same bytes, and are rejected by it."""
+    import hashlib
+    from paper_2211_12265_b200 import Engine
+    oids = {"sha512": bytes.fromhex("0609608648016503040203"),     # 2.16.840.1.101.3.4.2.3
+            "shake256": bytes.fromhex("060960864801650304020C")}   # 2.16.840.1.101.3.4.2.12
+    eng = Engine(0)
+    try:
+        for level in (44, 65, 87):
+            pks, sks = eng.batch_keygen(level, np.arange(32, dtype=np.uint8))
+            msgs = [bytes([i]) * (3 * i + 1) for i in range(24)]
+            for name, oid in oids.items():
+                dig = [hashlib.sha512(m).digest() if name == "sha512" else hashlib.shake_256(m).digest(64) for m in msgs]
+                ctx = b"prehash ctx" if name == "sha512" else b""
+                eng.set_mldsa_prehash(oid, ctx)
+                oracle.set_mldsa_prehash(oid, ctx)
+                sigs = eng.batch_sign(level, sks[0], dig)
+                for i in range(len(dig)):
+                    assert sigs[i].tobytes() == oracle.sign(level, sks[0].tobytes(), dig[i])[0]
+                assert eng.batch_verify(level, pks[0], dig, sigs).all()
+                for i in (0, 7):
+                    assert oracle.verify(level, pks[0].tobytes(), dig[i], sigs[i].tobytes()) == 1
+                eng.set_mldsa_prehash(b"", ctx)     # pure ML-DSA over the same bytes: other signatures
+                oracle.set_mldsa_prehash(b"", ctx)
+                pure = eng.batch_sign(level, sks[0], dig)
+                assert not np.array_equal(pure, sigs)
+                assert not eng.batch_verify(level, pks[0], dig, sigs).any()
+        with pytest.raises(Exception):
+            eng.set_mldsa_prehash(bytes(17))
+    finally:
+        oracle.set_mldsa_prehash(b"", b"")
+        eng.close()
