@@ -130,9 +130,13 @@ template <Params P> using SigBytes = std::array<uint8_t, P.sig_bytes()>;
 using SeedArray = std::array<uint8_t, kSeedBytes>;
 using CrhArray = std::array<uint8_t, kCrhBytes>;
 
-// DLB_SHIM_PROF=1: host-side phase times of the batch calls on stderr (where does a call's time go)
+// DLB_SHIM_PROF=1 (read once per process): host-side phase times of the batch calls on stderr
+inline bool shim_prof_enabled() {
+  static const bool on = std::getenv("DLB_SHIM_PROF") != nullptr;
+  return on;
+}
 struct ShimProf {
-  bool on = std::getenv("DLB_SHIM_PROF") != nullptr;
+  bool on = shim_prof_enabled();
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   void mark(const char* what) {
     if (!on) return;

@@ -204,6 +204,7 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
   if (const char* v = getenv("DLB_BOOST_DEPTH")) c->knob_boost_depth = (unsigned)atoi(v);
   if (c->knob_boost_depth < 1 || c->knob_boost_depth > 8) c->knob_boost_depth = 4;
   if (const char* v = getenv("DLB_SIGN_OCC")) c->knob_sign_occ = (unsigned)atoi(v);
+  c->knob_submit_prof = getenv("DLB_SUBMIT_PROF") != nullptr;
   if (const char* v = getenv("DLB_KEY_CACHE")) c->knob_key_cache = (size_t)atol(v);
   const int rc = create_resources(c);
   if (rc != 0) {
@@ -784,7 +785,7 @@ int sign_host_submit(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t
   if (msg_off[0] != 0 || !msg_off_ok(msgs, msg_off, n)) return DLB_E_ARG;
   cudaSetDevice(c->device);
   OwnStream own(c);
-  PhaseProf prof;
+  PhaseProf prof(c->knob_submit_prof);
   unsigned t;
   cudaStream_t S;
   DLB_TRY(sign_reserve(c, &t, &S));

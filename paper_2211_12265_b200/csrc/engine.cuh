@@ -165,6 +165,7 @@ struct dlb_ctx {
   size_t knob_pipe_chunk = 8192;  // host transfer pipeline chunk (tasks)
   size_t knob_sign_pad_smem = 0;  // occupancy experiments
   int knob_carveout = -1;
+  bool knob_submit_prof = false;  // DLB_SUBMIT_PROF: host-side phase times of every submission on stderr
   unsigned knob_sign_occ = 0;     // resident scheduler CTAs per SM (DLB_SIGN_OCC; 0 = what fits)
 
   cudaStream_t s() const { return ext ? ext : stream; }
@@ -225,7 +226,7 @@ struct dlb_ctx {
 
 namespace dlb {
 
-// host-side phase timer for the submission path (DLB_SUBMIT_PROF=1 prints to stderr)
+// host-side phase timer for the submission path (DLB_SUBMIT_PROF=1 at dlb_create: prints to stderr)
 struct PhaseProf {
   bool on;
   double t0;
@@ -234,7 +235,7 @@ struct PhaseProf {
     clock_gettime(CLOCK_MONOTONIC, &ts);
     return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
   }
-  PhaseProf() : on(getenv("DLB_SUBMIT_PROF") != nullptr), t0(on ? now() : 0) {}
+  explicit PhaseProf(bool enabled) : on(enabled), t0(on ? now() : 0) {}
   void mark(const char* what) {
     if (!on) return;
     const double t = now();

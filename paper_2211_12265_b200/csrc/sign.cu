@@ -536,7 +536,8 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
 
   while (true) {
     // ---- refill from the device work queues of the batches in this kernel's window ------
-    // Warp 0: lane i looks at ticket own + i.  A batch becomes visible through an acquire
+    // Warp 0: lane 0 looks at the kernel's own ticket, lane i >= 1 at ticket first + i - 1.  A batch
+    // becomes visible through an acquire
     // load of its gate word (the host writes it after the descriptor and all inputs are in
     // place; the acquire also drops stale L1 lines of whatever occupied those arenas before).
     // Tasks are claimed oldest batch first, up to tcap per batch and 128 per CTA.
@@ -1159,7 +1160,7 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   // distinct keys to precompute: the key table, one key per task, or one shared key
   const size_t nk = io.d_key_idx ? io.n_keys : (io.sk_stride ? n : 1);
 
-  PhaseProf prof;
+  PhaseProf prof(c->knob_submit_prof);
   int32_t *A = nullptr, *shat = nullptr;
   uint64_t *mu, *rp;
   // a shared key is looked up in (or added to) the cross-call cache: a hit needs no per-key kernels
