@@ -568,8 +568,11 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
           const unsigned ticket = lane == 0 ? a.ticket : sm.first + (unsigned)lane - 1u;
           SignBatch* g = a.ring + (ticket % kRing);
           bool seen = (sm.seen >> lane) & 1u;
-          // (a CTA never looks kRing - 1 or more tickets past its own: that slot may be its own batch's)
-          if (!seen && ticket - a.ticket <= (unsigned)kRing - 2u && ld_acquire(&g->gate) == ticket + 1u &&
+          // A CTA serves at most kRing / 2 tickets past its kernel's own: the kernel of ticket T has
+          // then certainly exited when ticket T + kRing wants its ring slot (sign_reserve waits for
+          // exactly that), however late its CTAs became resident.  A CTA that starts with nothing in
+          // reach exits at once and lets the next kernel of its lane in.
+          if (!seen && ticket - a.ticket <= (unsigned)kRing / 2u && ld_acquire(&g->gate) == ticket + 1u &&
               g->level == P::LEVEL &&
               (lane == 0 || !g->exclusive)) {
             BatchView& v = sm.bv[lane];
@@ -592,6 +595,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
           }
           if (seen) avail = ld_relaxed(&g->head) < sm.bv[lane].n && sm.bcnt[lane] < sm.bv[lane].tcap;
         }
+        __syncwarp();  // the views written above are read by every lane below
         unsigned m = __ballot_sync(0xffffffffu, avail);
         while (m && U < cap) {
           const int i = __ffs(m) - 1;
@@ -620,6 +624,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
           }
           U += got;
         }
+        __syncwarp();
         if (lane == 0) sm.U = U;
       }
       // the table is full up to the cap: the spare slots belong to the stragglers; otherwise (queues
@@ -1312,15 +1317,33 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
     a.alog_cap = (unsigned)(c->alog_cap > 0xFFFFFFFFu ? 0xFFFFFFFFu : c->alog_cap);
   }
   if (a.trace || a.alog) DLB_CUDA_CHECK(cudaMemsetAsync(c->d_log, 0, sizeof(SignLog), st));
-  // one scratch set per lane, sized for the full resident grid so it never moves under a
-  // running kernel of the same lane
+  // One scratch set per lane, sized for the full resident grid so it never moves under a
+  // running kernel of the same lane.  All lanes are sized together: growing an arena frees the
+  // old one, which waits for every kernel on the device, so a lane left at a smaller parameter
+  // set's size would stall a later submission in the middle of a flow (which lane a ticket gets
+  // depends on when earlier kernels retire).  This way the first ticket of a larger set pays once.
   const size_t slots = grid_max * kSignThreads;
-  DLB_TRY(dalloc(c, c->lane_name(ln, "s.y"), slots * Z::Y_SLOT + 16, &a.ybytes));
-  DLB_TRY(dalloc(c, c->lane_name(ln, "s.w"), slots * Z::W_SLOT, &a.wbuf));
-  DLB_TRY(dalloc(c, c->lane_name(ln, "s.w1"), slots * S::W1_ALL, &a.w1buf));
-  DLB_TRY(dalloc(c, c->lane_name(ln, "s.ct"), slots * Hashing<P>::CTW, &a.ctbuf));
-  DLB_TRY(dalloc(c, c->lane_name(ln, "s.c8"), slots * kN, &a.c8buf));
-  DLB_TRY(dalloc(c, c->lane_name(ln, "s.stage"), slots * Z::SIG_PAD, &a.staging));
+  for (int l = 0; l < kLanes; ++l) {
+    uint8_t* yb;
+    int32_t* wb;
+    uint8_t *w1b, *stg;
+    int8_t* c8b;
+    uint64_t* ctb;
+    DLB_TRY(dalloc(c, c->lane_name(l, "s.y"), slots * Z::Y_SLOT + 16, &yb));
+    DLB_TRY(dalloc(c, c->lane_name(l, "s.w"), slots * Z::W_SLOT, &wb));
+    DLB_TRY(dalloc(c, c->lane_name(l, "s.w1"), slots * S::W1_ALL, &w1b));
+    DLB_TRY(dalloc(c, c->lane_name(l, "s.ct"), slots * Hashing<P>::CTW, &ctb));
+    DLB_TRY(dalloc(c, c->lane_name(l, "s.c8"), slots * kN, &c8b));
+    DLB_TRY(dalloc(c, c->lane_name(l, "s.stage"), slots * Z::SIG_PAD, &stg));
+    if (l == ln) {
+      a.ybytes = yb;
+      a.wbuf = wb;
+      a.w1buf = w1b;
+      a.ctbuf = ctb;
+      a.c8buf = c8b;
+      a.staging = stg;
+    }
+  }
   prof.mark(" scratch");
   DLB_CUDA_CHECK(cudaEventRecord(c->sign_pubd, st));
   DLB_CUDA_CHECK(cudaStreamWaitEvent(lane, c->sign_pubd, 0));
