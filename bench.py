@@ -6,7 +6,7 @@ prints ONE JSON line on rank 0.  A step is one pass of the hot path over one bat
 synthetic input on every GPU: ONE batch of 100,000 Dilithium2 sign tasks (the task count of
 the paper's headline shape, 10 in-flight batches of 10,000), one shared key,
 32-byte messages, deterministic signing (BASELINE.json configs[1]).  Steps are submitted through
-dlb_sign_submit[_dev] / dlb_sign_wait with up to --depth (8) steps in flight, the way the paper
+dlb_sign_submit[_dev] / dlb_sign_wait with up to --depth (16) steps in flight, the way the paper
 keeps batches in flight; every step is a separate batch with its own output buffers.
 
   value     whole-job signatures/s with inputs resident in HBM (CUDA events around K steps)
@@ -855,7 +855,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tasks", type=int, default=100000, help="tasks per GPU per step")
-    ap.add_argument("--depth", type=int, default=8, help="steps (batches) in flight")
+    ap.add_argument("--depth", type=int, default=16, help="steps (batches) in flight")
     ap.add_argument("--no-shim", action="store_true", help="skip the C++ shim leg (tools/bench_shim)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-levels", action="store_true", help="skip the Dilithium3/5 extras")

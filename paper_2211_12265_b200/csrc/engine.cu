@@ -168,6 +168,7 @@ static int create_resources(dlb_ctx* c) {
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
   DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+  DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stats, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) {
     DLB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->lane_s[b], cudaStreamNonBlocking));
     DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join[b], cudaEventDisableTiming));
@@ -206,6 +207,7 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
   if (const char* v = getenv("DLB_SIGN_OCC")) c->knob_sign_occ = (unsigned)atoi(v);
   c->knob_submit_prof = getenv("DLB_SUBMIT_PROF") != nullptr;
   if (const char* v = getenv("DLB_KEY_CACHE")) c->knob_key_cache = (size_t)atol(v);
+  if (const char* v = getenv("DLB_ZERO_COPY_MAX")) c->knob_zero_copy_max = (size_t)atoll(v);
   const int rc = create_resources(c);
   if (rc != 0) {
     dlb_destroy(c);  // tolerates the handles that were never created
@@ -273,6 +275,7 @@ void dlb_destroy(dlb_ctx* c) {
       if (c->sign_evs[r]) cudaEventDestroy(c->sign_evs[r]);
       if (c->sign_ev0[r]) cudaEventDestroy(c->sign_ev0[r]);
       if (c->sign_ev1[r]) cudaEventDestroy(c->sign_ev1[r]);
+      if (c->sign_cpy[r]) cudaEventDestroy(c->sign_cpy[r]);
     }
     if (c->sign_dep) cudaEventDestroy(c->sign_dep);
     if (c->sign_pubd) cudaEventDestroy(c->sign_pubd);
@@ -297,6 +300,7 @@ void dlb_destroy(dlb_ctx* c) {
   st(c->stream);
   st(c->copy_in);
   st(c->copy_out);
+  st(c->copy_stats);
   delete c;
 }
 
@@ -797,7 +801,11 @@ int sign_host_submit(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t
   uint64_t* doff;
   uint32_t *datt, *dkidx = nullptr;
   if (key_idx) DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.kidx"), n, &dkidx));
-  uint8_t* zero_copy = static_cast<uint8_t*>(pinned_alias(sigs));  // pinned: write in place
+  // Pinned result buffer: signatures are written in place by the kernel's commit step (no copy to
+  // wait for).  DLB_ZERO_COPY_MAX sends batches above a size through device memory and a copy at
+  // wait time instead; measured slower at every size (profiles/r02_summary.md), so off by default.
+  uint8_t* const pinned_sigs = static_cast<uint8_t*>(pinned_alias(sigs));
+  uint8_t* zero_copy = n * ls.sig <= c->knob_zero_copy_max ? pinned_sigs : nullptr;
   DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.sk"), nk * ls.sk, &dsk));
   DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.msg"), mbytes + 8, &dm));
   DLB_TRY(dalloc(c, c->slot_name(c->cur_set, "io.off"), n + 1, &doff));
@@ -867,6 +875,7 @@ int sign_host_submit(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t
     tk.d_failed = dfail;
   }
   tk.zero_host = sigs;
+  tk.host_pinned = pinned_sigs && (!attempts || pinned_alias(attempts)) && (!failed || pinned_alias(failed));
   *ticket_out = (uint64_t)t + 1;
   return 0;
 }

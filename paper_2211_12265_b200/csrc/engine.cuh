@@ -49,6 +49,8 @@ struct SignTicket {
   // the caller's signature buffer, cleared when the key turns out malformed
   uint8_t* zero_host = nullptr;
   uint8_t* zero_dev = nullptr;
+  bool copy_issued = false;  // the result copies are already queued on copy_out (sign_cpy[slot] follows them)
+  bool host_pinned = false;  // the caller's result buffers are page-locked: the copies are asynchronous
 };
 
 // Per-key signing state kept across calls (SignPrecomp, scheme.hpp:26-32,106-125): the expanded
@@ -105,6 +107,7 @@ struct dlb_ctx {
   cudaStream_t stream = nullptr;      // engine-owned compute stream
   cudaStream_t copy_in = nullptr;     // H2D stream
   cudaStream_t copy_out = nullptr;    // D2H stream
+  cudaStream_t copy_stats = nullptr;  // D2H of a finished batch's counters (never behind a bulk copy)
   cudaStream_t ext = nullptr;         // caller's stream for *_dev calls (optional)
   cudaStream_t lane_s[2] = {};        // two compute lanes: consecutive chunks overlap
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {};
@@ -138,13 +141,13 @@ struct dlb_ctx {
   cudaStream_t sign_pub = nullptr;       // publication stream: copies and per-key kernels, never a scheduler kernel
   cudaEvent_t sign_pubd = nullptr;       // batch published (the lane's kernel launch waits for it)
   // per ring slot: start of the batch's device work, start / end of its scheduler kernel
-  cudaEvent_t sign_evs[dlb::kRing] = {}, sign_ev0[dlb::kRing] = {}, sign_ev1[dlb::kRing] = {}, sign_dep = nullptr;
+  cudaEvent_t sign_evs[dlb::kRing] = {}, sign_ev0[dlb::kRing] = {}, sign_ev1[dlb::kRing] = {}, sign_cpy[dlb::kRing] = {},
+              sign_dep = nullptr;
   dlb::SignTicket tickets[dlb::kRing];
   unsigned next_ticket = 0;
   // input / output / per-batch arenas come in sets; a ticket holds the lowest free set from
   // submission to wait, so a pipeline of depth d only ever touches (and warms) d sets
   bool set_busy[dlb::kRing] = {};
-  bool slot_launched[dlb::kRing] = {};   // sign_ev1[slot] has been recorded at least once
   int cur_set = 0;                       // set reserved for the submission in progress
   int sign_occ[12] = {};                 // resident CTAs per SM of k_sign_persistent<level, DBG>
   size_t sign_smem[12] = {};
@@ -154,6 +157,10 @@ struct dlb_ctx {
   std::vector<dlb::KeyCacheEntry> key_cache;
   unsigned long long key_cache_clock = 0, key_cache_hits = 0, key_cache_misses = 0;
   size_t knob_key_cache = 32;            // entries; 0 disables (DLB_KEY_CACHE)
+  size_t knob_zero_copy_max = ~(size_t)0; // signatures go straight into a pinned caller buffer up to this many
+                                         // bytes per batch, through device memory + a copy at wait time above
+                                         // (DLB_ZERO_COPY_MAX; in place is faster at every size measured,
+                                         // profiles/r02_summary.md)
   unsigned dbg_max_attempt = 0;          // stage tests: smaller nonce space (0 = the scheme's)
   // tuning knobs, read from the environment once at dlb_create (profiles/: the sweeps)
   unsigned knob_spec_depth = 8;

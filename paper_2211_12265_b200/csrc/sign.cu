@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(WARPS * 32)
 // digest stage, test hooks) is read from the descriptor itself when needed -- immutable, and
 // fetched behind the acquire that made the batch visible.
 struct BatchView {
-  unsigned n, tcap, max_attempt, spec_depth, key_stride, ticket1;
+  unsigned n, tcap, max_attempt, spec_depth, key_stride, ticket1;  // ticket1 = gate value the view was loaded for
+  int level;
+  unsigned exclusive;
   const uint64_t* mu;
   const uint64_t* rho_prime;
   const uint32_t* kappa0;
@@ -115,7 +117,7 @@ struct BatchView {
 struct SignArgs {             // one scheduler-kernel instance
   SignBatch* ring;            // kRing descriptors
   unsigned ticket;            // own ticket
-  unsigned window;            // tickets served: ticket .. ticket + window - 1
+  unsigned window;            // 1: the kernel serves its own batch only (stage tests); else every batch in flight
   unsigned slots;             // attempt slots a CTA fills with speculation (<= 128): small batches are
                               // spread over more CTAs with fewer slots each to cut round latency
   int single_round;           // stage-test mode: exactly one round, then fail open tasks
@@ -173,11 +175,9 @@ struct SignSmem {
   uint8_t slot_valid[kSignThreads];
   int32_t winner[kSignThreads];    // per open task: winning slot, -1 none, -2 failed
   uint32_t warp_sums[kSignWarps];
-  BatchView bv[kWindow];           // descriptors of the batches this CTA has seen published
-  unsigned bcnt[kWindow];          // open tasks held per batch
-  unsigned bfin[kWindow];          // tasks of each batch finished in the current round
-  unsigned seen;                   // bit i: bv[i] loaded
-  unsigned first;                  // window position i >= 1 is ticket first + i - 1 (position 0: own)
+  BatchView bv[kRing];             // descriptor of the batch last seen published in each ring slot
+  unsigned bcnt[kRing];            // open tasks held per batch
+  unsigned bfin[kRing];            // tasks of each batch finished in the current round
   unsigned U, Uold, span, need_hash;
   unsigned B;                      // tasks (table front) that share the slots behind the first U
   unsigned cursor2, cursor4;  // next unclaimed slot of stages S2 / S4 (warps pull slots)
@@ -514,33 +514,23 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
   load_twiddles(sm.zs, sm.nzs);
   if (tid == 0) {
     sm.U = 0;
-    sm.seen = 0;
     sm.rounds = 0;
   }
-  if (tid < kWindow) sm.bcnt[tid] = sm.bfin[tid] = 0;
-  if (warp == 0) {
-    // Window anchor: the OLDEST younger batch that still has unclaimed tasks (a batch whose own
-    // kernel is still waiting for residency must not be left to it alone), else the first ticket
-    // that has not been published yet.  gate = ticket + 1 of the batch in a ring slot.
-    unsigned g1 = 0, cand = 0xFFFFFFFFu;
-    if (lane < kRing) {
-      const SignBatch* g = a.ring + lane;
-      g1 = ld_acquire(&g->gate);
-      if (g1 > a.ticket + 1u && ld_relaxed(&g->head) < g->n) cand = g1 - 1u;
-    }
-    g1 = __reduce_max_sync(0xffffffffu, g1);    // newest published ticket + 1 (>= own + 1)
-    cand = __reduce_min_sync(0xffffffffu, cand);
-    if (lane == 0) sm.first = cand != 0xFFFFFFFFu ? cand : max(g1, a.ticket + 1u);
+  if (tid < kRing) {
+    sm.bcnt[tid] = sm.bfin[tid] = 0;
+    sm.bv[tid].ticket1 = 0;
   }
   __syncthreads();
 
   while (true) {
-    // ---- refill from the device work queues of the batches in this kernel's window ------
-    // Warp 0: lane 0 looks at the kernel's own ticket, lane i >= 1 at ticket first + i - 1.  A batch
-    // becomes visible through an acquire
-    // load of its gate word (the host writes it after the descriptor and all inputs are in
-    // place; the acquire also drops stale L1 lines of whatever occupied those arenas before).
-    // Tasks are claimed oldest batch first, up to tcap per batch and 128 per CTA.
+    // ---- refill from the device work queues of the batches in flight -----------------------
+    // Warp 0, lane p looks at ring slot p.  A batch becomes visible through an acquire load of
+    // its gate word (the host writes it after the descriptor and all inputs are in place; the
+    // acquire also drops stale L1 lines of whatever occupied those arenas before).  Tasks are
+    // claimed oldest ticket first, up to tcap open tasks per batch and 128 per CTA, with a
+    // compare-and-swap on the batch's 64-bit queue word (ticket + 1 : next task): a claim can
+    // only ever succeed against the batch the view was loaded for, so a CTA may outlive its own
+    // batch for as long as work keeps arriving and ring slots are reused under it.
     if (warp == 0) {
       unsigned U = sm.U;
       if (lane == 0) {
@@ -563,25 +553,23 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       }
       const unsigned cap = (unsigned)kSignThreads - n_s * a.boost_depth;
       if (U < cap && !(a.single_round && sm.rounds > 0)) {
-        bool avail = false;
-        if ((unsigned)lane < a.window) {
-          const unsigned ticket = lane == 0 ? a.ticket : sm.first + (unsigned)lane - 1u;
-          SignBatch* g = a.ring + (ticket % kRing);
-          bool seen = (sm.seen >> lane) & 1u;
-          // A CTA serves at most kRing / 2 tickets past its kernel's own: the kernel of ticket T has
-          // then certainly exited when ticket T + kRing wants its ring slot (sign_reserve waits for
-          // exactly that), however late its CTAs became resident.  A CTA that starts with nothing in
-          // reach exits at once and lets the next kernel of its lane in.
-          if (!seen && ticket - a.ticket <= (unsigned)kRing / 2u && ld_acquire(&g->gate) == ticket + 1u &&
-              g->level == P::LEVEL &&
-              (lane == 0 || !g->exclusive)) {
-            BatchView& v = sm.bv[lane];
+        // a.window == 1 (stage tests): only the kernel's own batch
+        unsigned tk = 0xFFFFFFFFu, blocked = 0xFFFFFFFFu;
+        if (a.window > 1u || (unsigned)lane == a.ticket % kRing) {
+          SignBatch* g = a.ring + lane;
+          const unsigned g1 = ld_acquire(&g->gate);
+          BatchView& v = sm.bv[lane];
+          const bool own = g1 == a.ticket + 1u;
+          if (g1 != 0 && v.ticket1 != g1 && sm.bcnt[lane] == 0) {
+            // (a view is only replaced when none of the previous occupant's tasks is open here,
+            // which its completion -- the precondition of the slot's reuse -- implies)
             v.n = g->n;
             v.tcap = g->tcap;
             v.max_attempt = g->max_attempt;
             v.spec_depth = g->spec_depth;
             v.key_stride = g->key_stride;
-            v.ticket1 = ticket + 1u;
+            v.level = g->level;
+            v.exclusive = g->exclusive;
             v.mu = g->mu;
             v.rho_prime = g->rho_prime;
             v.kappa0 = g->kappa0;
@@ -590,22 +578,47 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
             v.key_idx = g->key_idx;
             v.sigs = g->sigs;
             v.g = g;
-            atomicOr(&sm.seen, 1u << lane);
-            seen = true;
+            v.ticket1 = g1;
           }
-          if (seen) avail = ld_relaxed(&g->head) < sm.bv[lane].n && sm.bcnt[lane] < sm.bv[lane].tcap;
+          if (g1 != 0 && v.ticket1 == g1) {
+            const unsigned long long q = ld_relaxed(&g->head);
+            const bool open = (unsigned)(q >> 32) == g1 && (unsigned)q < v.n;
+            if (open) {
+              if (v.level == P::LEVEL && (own || (!v.exclusive && a.window > 1u))) {
+                if (sm.bcnt[lane] < v.tcap) tk = g1 - 1u;
+              } else {
+                blocked = g1 - 1u;  // unclaimed work this kernel cannot serve
+              }
+            }
+          }
         }
         __syncwarp();  // the views written above are read by every lane below
-        unsigned m = __ballot_sync(0xffffffffu, avail);
-        while (m && U < cap) {
-          const int i = __ffs(m) - 1;
-          m &= m - 1;
+        // First come, first served across parameter sets: nothing younger than the oldest batch
+        // this kernel cannot serve is claimed (its own kernel gets the SMs as these CTAs retire),
+        // except the kernel's own batch, which it always serves -- no batch is left without a
+        // kernel that will take it.
+        blocked = __reduce_min_sync(0xffffffffu, blocked);
+        if (tk != 0xFFFFFFFFu && tk > blocked && tk != a.ticket) tk = 0xFFFFFFFFu;
+        while (U < cap) {
+          const unsigned best = __reduce_min_sync(0xffffffffu, tk);
+          if (best == 0xFFFFFFFFu) break;
+          const int i = (int)(best % kRing);
+          if (lane == i) tk = 0xFFFFFFFFu;
           const BatchView& v = sm.bv[i];
           const unsigned want = min(v.tcap - sm.bcnt[i], cap - U);
           unsigned base = 0, got = 0;
           if (lane == 0) {
-            base = atomicAdd(&v.g->head, want);
-            if (base < v.n) got = min(want, v.n - base);
+            unsigned long long q = ld_relaxed(&v.g->head);
+            while ((unsigned)(q >> 32) == v.ticket1 && (unsigned)q < v.n) {
+              const unsigned take = min(want, v.n - (unsigned)q);
+              const unsigned long long old = atomicCAS(&v.g->head, q, q + take);
+              if (old == q) {
+                base = (unsigned)q;
+                got = take;
+                break;
+              }
+              q = old;
+            }
             if (got) {
               unsigned long long now;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
@@ -701,7 +714,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       const unsigned n_on = __syncthreads_count(on);
       const unsigned n_spec = __syncthreads_count(on && depth > 0);
       if (warp == 0) {  // a round counts for every batch present; idle slots go to the oldest
-        const bool present = lane < kWindow && sm.bcnt[lane] > 0;
+        const bool present = sm.bcnt[lane] > 0;
         const unsigned pm = __ballot_sync(0xffffffffu, present);
         if (present) {
           atomicAdd(&sm.bv[lane].g->rounds, 1ull);
@@ -930,7 +943,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       }
       // per-batch completion: everything this CTA wrote for the finished tasks is made
       // visible system-wide before `done` moves; whoever completes the batch raises its flag
-      if (tid < kWindow && sm.bfin[tid]) {
+      if (tid < kRing && sm.bfin[tid]) {
         const unsigned f = sm.bfin[tid];
         sm.bfin[tid] = 0;
         sm.bcnt[tid] -= f;
@@ -1002,6 +1015,7 @@ int sign_state_init(dlb_ctx* c) {
     DLB_CUDA_CHECK(cudaEventCreate(&c->sign_evs[r]));
     DLB_CUDA_CHECK(cudaEventCreate(&c->sign_ev0[r]));
     DLB_CUDA_CHECK(cudaEventCreate(&c->sign_ev1[r]));
+    DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->sign_cpy[r], cudaEventDisableTiming));
   }
   DLB_CUDA_CHECK(cudaEventCreateWithFlags(&c->sign_dep, cudaEventDisableTiming));
   c->sign_ready = true;
@@ -1134,12 +1148,10 @@ int sign_reserve(dlb_ctx* c, unsigned* ticket, cudaStream_t* pub) {
   DLB_TRY(sign_state_init(c));
   const unsigned t = c->next_ticket;
   if (c->tickets[t % kRing].active) return DLB_E_BUSY;  // kRing batches in flight: wait for the oldest first
-  // A ring slot is rewritten only when the scheduler kernel of the ticket that used it last
-  // (16 tickets ago) has exited.  By induction every kernel with an older ticket has exited too,
-  // and only those can hold a cached view of that slot's previous batch (a CTA's window starts
-  // at or behind its own ticket): no resident CTA can mistake the new batch's work queue for
-  // the old one's.  In a steady flow that kernel retired several tickets ago.
-  if (c->slot_launched[t % kRing]) DLB_CUDA_CHECK(cudaEventSynchronize(c->sign_ev1[t % kRing]));
+  // The ring slot of a completed ticket may be rewritten while scheduler CTAs that once served it
+  // are still resident: their view of the slot is tagged with the old ticket, and a claim is a
+  // compare-and-swap against the slot's (ticket + 1 : next task) word, so it can only succeed
+  // against the batch the view was loaded for.
   *ticket = t;
   *pub = c->sign_pub;
   cudaStream_t* lane = pub;
@@ -1257,6 +1269,7 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   h.level = P::LEVEL;
   h.exclusive = (io.single_round || DBG) ? 1u : 0u;
   h.ticket1 = ticket + 1u;
+  h.head = (unsigned long long)(ticket + 1u) << 32;  // queue word: ticket + 1 : next unclaimed task
   h.mu = io.d_mu_in ? io.d_mu_in : mu;
   h.rho_prime = io.d_rho_prime ? reinterpret_cast<const uint64_t*>(io.d_rho_prime) : rp;
   h.kappa0 = io.d_kappa0;
@@ -1302,7 +1315,7 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   memset(&a, 0, sizeof a);
   a.ring = c->d_ring;
   a.ticket = ticket;
-  a.window = h.exclusive ? 1u : (unsigned)kWindow;
+  a.window = h.exclusive ? 1u : (unsigned)kRing;
   a.slots = (unsigned)slots_per;
   a.single_round = io.single_round;
   a.boost_thr = io.single_round ? 0u : c->knob_boost_thr;
@@ -1350,7 +1363,6 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   cudaEventRecord(c->sign_ev0[slot], lane);
   k_sign_persistent<P, DBG><<<(unsigned)grid, kSignThreads, smem_bytes, lane>>>(a);
   cudaEventRecord(c->sign_ev1[slot], lane);
-  c->slot_launched[slot] = true;
   cudaEventRecord(c->lane_done[ln], lane);
   c->lane_used[ln] = true;
   c->launches += 1;
@@ -1375,6 +1387,20 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
 template <class P>
 int sign_submit(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   return io.dbg_bounds ? sign_submit_t<P, true>(c, ticket, io) : sign_submit_t<P, false>(c, ticket, io);
+}
+
+// Queues the device -> host copies of a completed batch's results (those not written in place)
+// on the copy-out stream; sign_cpy[slot] follows them.
+static int sign_copy_out(dlb_ctx* c, int slot) {
+  SignTicket& tk = c->tickets[slot];
+  if (tk.copy_issued) return 0;
+  cudaStream_t co = c->copy_out;
+  if (tk.h_sigs) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_sigs, tk.d_sigs, tk.n * tk.sig_bytes, cudaMemcpyDeviceToHost, co));
+  if (tk.h_att) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_att, tk.d_att, tk.n * 4, cudaMemcpyDeviceToHost, co));
+  if (tk.h_failed) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_failed, tk.d_failed, tk.n, cudaMemcpyDeviceToHost, co));
+  DLB_CUDA_CHECK(cudaEventRecord(c->sign_cpy[slot], co));
+  tk.copy_issued = true;
+  return 0;
 }
 
 // Blocks until the batch of `ticket` is complete (its flag in mapped host memory), then
@@ -1406,8 +1432,8 @@ int sign_wait(dlb_ctx* c, unsigned ticket, dlb_sign_stats* stats, bool drain) {
       if (idle && *flag != ticket + 1u) {
         SignBatch hq;  // what the device thinks of the batch, for the bug report
         if (cudaMemcpy(&hq, c->d_ring + slot, sizeof hq, cudaMemcpyDeviceToHost) == cudaSuccess)
-          fprintf(stderr, "dilithium-b200: ticket %u never completed: n %u head %u done %u gate %u failed %llu\n",
-                  ticket, hq.n, hq.head, hq.done, hq.gate, hq.failed);
+          fprintf(stderr, "dilithium-b200: ticket %u never completed: n %u queue %u:%u done %u gate %u failed %llu\n",
+                  ticket, hq.n, (unsigned)(hq.head >> 32), (unsigned)hq.head, hq.done, hq.gate, hq.failed);
         return DLB_E_INTERNAL;
       }
     }
@@ -1422,15 +1448,22 @@ int sign_wait(dlb_ctx* c, unsigned ticket, dlb_sign_stats* stats, bool drain) {
     cudaEventElapsedTime(&c->last_ms, c->sign_evs[slot], c->sign_ev1[slot]);
   }
   SignBatch hq;
-  cudaStream_t co = c->copy_out;
-  DLB_CUDA_CHECK(cudaMemcpyAsync(&hq, c->d_ring + slot, sizeof hq, cudaMemcpyDeviceToHost, co));
+  DLB_TRY(sign_copy_out(c, slot));
+  // Other batches that have completed meanwhile: queue their result copies behind this one now, so
+  // the copy engine works through them while the caller handles this batch (only when the copies
+  // are asynchronous; a pageable destination would block here).
+  for (unsigned k = 1; k < (unsigned)kRing; ++k) {
+    const int s2 = (int)((ticket + k) % kRing);
+    const SignTicket& t2 = c->tickets[s2];
+    if (t2.active && t2.host_pinned && !t2.copy_issued && c->h_flags[s2] == t2.ticket + 1u)
+      DLB_TRY(sign_copy_out(c, s2));
+  }
+  DLB_CUDA_CHECK(cudaEventSynchronize(c->sign_cpy[slot]));
+  DLB_CUDA_CHECK(cudaMemcpyAsync(&hq, c->d_ring + slot, sizeof hq, cudaMemcpyDeviceToHost, c->copy_stats));
   SignLog hl{};
   if (tk.had_trace || tk.had_alog)
-    DLB_CUDA_CHECK(cudaMemcpyAsync(&hl, c->d_log, sizeof hl, cudaMemcpyDeviceToHost, co));
-  if (tk.h_sigs) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_sigs, tk.d_sigs, tk.n * tk.sig_bytes, cudaMemcpyDeviceToHost, co));
-  if (tk.h_att) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_att, tk.d_att, tk.n * 4, cudaMemcpyDeviceToHost, co));
-  if (tk.h_failed) DLB_CUDA_CHECK(cudaMemcpyAsync(tk.h_failed, tk.d_failed, tk.n, cudaMemcpyDeviceToHost, co));
-  DLB_CUDA_CHECK(cudaStreamSynchronize(co));
+    DLB_CUDA_CHECK(cudaMemcpyAsync(&hl, c->d_log, sizeof hl, cudaMemcpyDeviceToHost, c->copy_stats));
+  DLB_CUDA_CHECK(cudaStreamSynchronize(c->copy_stats));
   if (stats) {
     stats->rounds = hq.rounds;
     stats->attempts = hq.attempts;

@@ -7,7 +7,6 @@
 namespace dlb {
 
 constexpr int kRing = 32;    // batch descriptors per context = consecutive tickets that may be in flight
-constexpr int kWindow = 25;  // batches one scheduler CTA may serve: its kernel's own and 24 more (see sign.cu)
 constexpr int kLanes = 4;    // stream lanes / scratch sets; the kernel of ticket T runs on lane T % kLanes
 
 struct SignBatch {
@@ -45,10 +44,10 @@ struct SignBatch {
   unsigned pad0;
   volatile unsigned* host_flag;  // mapped pinned word: set to ticket + 1 when done == n
   // ---- mutable (device atomics)
-  unsigned head;              // next unclaimed task (the device work queue of this batch)
+  unsigned long long head;    // the device work queue of this batch: (ticket + 1) << 32 | next unclaimed
+                              // task; claimed by compare-and-swap, so a stale view can never claim
   unsigned done;              // committed tasks
   unsigned key_bad;           // some secret key failed the eta range check
-  unsigned pad1;
   unsigned long long rounds, attempts, speculative, idle_slots, accepted_sum, failed;
   // %globaltimer, ns: first / last claim of a task, first / last commit of a task
   unsigned long long t_first_start, t_last_start, t_first_exit, t_last_exit;
