@@ -84,19 +84,26 @@ __global__ void __launch_bounds__(WARPS * 32)
 // ---- device-side scheduler state -----------------------------------------------------
 //
 // Batches in flight.  A submitted batch is described by one SignBatch in a device ring
-// (slot = ticket % kRing).  A CTA of the scheduler kernel launched for ticket T serves T and a
-// window of 24 tickets that starts at the oldest younger batch with unclaimed tasks when the
-// CTA became resident (a kernel may wait a long time for residency behind older ones; anchoring
-// the window at T would hand it batches that were finished long ago): it refills its open-task
-// table from ANY published batch of that window before it speculates (the reference's pass 1 before pass 2,
-// scheduler.hpp:58-92, extended across batches -- the paper's in-flight batches,
-// PAPER.md:710-721), so the tail of one batch overlaps the body of the next ones.  Kernels of
-// consecutive tickets run on kLanes stream lanes with one scratch set each; a CTA never
-// waits for anything, it exits when its table is empty and no batch of its window has
-// unclaimed tasks.  Completion is per batch (SignBatch::done reaching n raises a flag in
-// mapped host memory), not per kernel.
+// (slot = ticket % kRing).  Every scheduler CTA, whichever ticket its kernel was launched for,
+// serves every published batch of its parameter set: lane p of warp 0 watches ring slot p, and
+// the CTA refills its open-task table from ANY batch with unclaimed tasks, oldest ticket first,
+// before it speculates (the reference's pass 1 before pass 2, scheduler.hpp:58-92, extended
+// across batches -- the paper's in-flight batches), so the tail of one batch
+// overlaps the body of the next ones and, while work keeps arriving, every slot runs a first
+// attempt.  A view of a ring slot is tagged with the gate value (ticket + 1) it was loaded for
+// and tasks are claimed by compare-and-swap on the batch's (ticket + 1 : next task) word, so a
+// view that outlived its batch can never claim from the slot's next occupant: CTAs may stay
+// resident for as long as the flow lasts, and a slot is reused as soon as its ticket was waited
+// for.  One kernel is still launched per ticket (kLanes stream lanes, one scratch set each): it
+// provides the CTAs when none are resident and always serves its own batch, so no batch is ever
+// without a kernel that will take it.  Batches of another parameter set (or stage tests, which
+// only their own kernel serves) are honoured first come first served: a CTA claims nothing
+// younger than the oldest batch it cannot serve, retires when its table is empty, and that
+// batch's own kernel gets the SMs.  A CTA never waits for anything; it exits when its table is
+// empty and nothing it may serve has unclaimed tasks.  Completion is per batch (SignBatch::done
+// reaching n raises a flag in mapped host memory), not per kernel.
 
-// what a CTA keeps in shared memory of a batch it serves (window position i): the fields the
+// what a CTA keeps in shared memory of the batch in ring slot i: the fields the
 // stages read per slot.  Everything else (output arrays of the commit step, the inputs of the
 // digest stage, test hooks) is read from the descriptor itself when needed -- immutable, and
 // fetched behind the acquire that made the batch visible.
@@ -168,7 +175,7 @@ struct SignSmem {
   } u;
   uint32_t utask[kSignThreads];    // open tasks of this CTA (compact): task id within its batch
   uint32_t unext[kSignThreads];    // their next unresolved attempt ordinal
-  uint8_t ubatch[kSignThreads];    // their batch: window position (ticket - own ticket)
+  uint8_t ubatch[kSignThreads];    // their batch: ring slot (ticket % kRing)
   uint32_t slot_task[kSignThreads];     // task id or kNoSlot
   uint32_t slot_attempt[kSignThreads];
   uint8_t slot_batch[kSignThreads];

@@ -7,7 +7,7 @@
 namespace dlb {
 
 constexpr int kRing = 32;    // batch descriptors per context = consecutive tickets that may be in flight
-constexpr int kLanes = 4;    // stream lanes / scratch sets; the kernel of ticket T runs on lane T % kLanes
+constexpr int kLanes = 4;    // stream lanes / scratch sets; a ticket's kernel takes the lowest idle lane, else T % kLanes
 
 struct SignBatch {
   // ---- immutable once published (copied into shared memory by every CTA that serves it)

@@ -258,3 +258,34 @@ def test_in_flight_stress_random_pipeline(eng):
             assert np.array_equal(sigs, w[0]) and np.array_equal(att, w[1])
             checked += 1
     assert checked >= 60
+
+
+def test_steady_flow_reuses_ring_slots_under_resident_ctas(eng, oracle):
+    """A steady flow of equal batches, 24 in flight, over four turns of the 32-slot ring: the
+    scheduler CTAs stay resident across batches (their views of a ring slot are re-tagged when the
+    slot gets its next ticket; claims are compare-and-swaps against the slot's ticket), so every
+    batch must still give the bytes of a synchronous call, a stage test (an exclusive batch of
+    another kernel) in the middle of the flow included."""
+    rs = np.random.default_rng(4242)
+    level, n, depth, batches = 2, 20000, 24, 130
+    pks, sks = eng.batch_keygen(level, rs.integers(0, 256, (1, 32), dtype=np.uint8))
+    flat = rs.integers(0, 256, n * 32, dtype=np.uint8)
+    off = np.arange(n + 1, dtype=np.uint64) * 32
+    want, want_att, _, _ = eng.batch_sign(level, sks[0], (flat, off), return_info=True)
+    for i in range(0, n, n // 5):
+        assert want[i].tobytes() == oracle.sign(level, sks[0].tobytes(), flat[32 * i:32 * i + 32].tobytes())[0]
+    mus = rs.integers(0, 256, (8, 64), dtype=np.uint8)
+    inflight = []
+    for b in range(batches):
+        if len(inflight) >= depth:
+            sigs, att, failed, st = eng.sign_wait(inflight.pop(0))
+            assert not failed.any() and np.array_equal(sigs, want) and np.array_equal(att, want_att)
+            assert st["accepted_attempt_sum"] == int(want_att.sum()) and st["attempts"] >= st["accepted_attempt_sum"]
+        if b == 70:  # one round of the bounds-injected kernel while 23 batches are in flight
+            acc, stage, _, _, _ = eng.dbg_sign_attempt_bounded(level, sks[0], mus, mus[::-1].copy(),
+                                                                np.zeros(8, np.uint32), 1, 1000, 1000)
+            assert not acc.any() and (stage == 0).all()
+        inflight.append(eng.sign_submit(level, sks[0], (flat, off)))
+    for h in inflight:
+        sigs, att, failed, st = eng.sign_wait(h)
+        assert not failed.any() and np.array_equal(sigs, want) and np.array_equal(att, want_att)
