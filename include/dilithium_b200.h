@@ -196,8 +196,12 @@ int dlb_verify_batch_keyed(dlb_ctx* ctx, int level, size_t n_keys, const uint8_t
  * tickets earlier has not been waited for.  The device
  * scheduler is shared: CTAs that run out of tasks of one batch claim tasks of the next
  * submitted batches (of the same level) before they speculate, so the rejection-loop tail of a
- * batch overlaps the body of its successors.  Output bytes never depend on what else is in
- * flight.  Arguments as dlb_sign_batch / dlb_sign_batch_keyed (key_idx == NULL: sk_stride 0 =
+ * batch overlaps the body of its successors.  Batches of different levels are served first come
+ * first served.  Throughput grows with the work in flight until the scheduler's queues never run
+ * dry: a batch's unluckiest task needs ~45 rounds, so a batch completes 55-100 ms after it was
+ * submitted, and a steady stream wants about that much work in flight (100,000-task batches: 16;
+ * measured 14.7 M sign/s against 14.3 at 8 and 10.6 one at a time).  Output bytes never depend
+ * on what else is in flight.  Arguments as dlb_sign_batch / dlb_sign_batch_keyed (key_idx == NULL: sk_stride 0 =
  * one shared key, else one key per task; key_idx != NULL: a table of n_keys keys, sk_stride
  * = sk_bytes).  All input and output buffers must stay valid until the wait returns; a
  * signature buffer in pinned memory (dlb_host_alloc) is written in place by the device.
