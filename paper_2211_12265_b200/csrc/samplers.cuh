@@ -25,14 +25,13 @@ __device__ __forceinline__ uint64_t load_u64_unaligned(const uint8_t* p) {
 // out[p][256] int32 in [0,q).  rho of key n at rho_base + n*rho_stride.
 constexpr int kExpandAStageStride = 57;  // 56 candidates per block, odd stride
 
-template <class P, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    k_expand_a(const uint8_t* __restrict__ rho_base, size_t rho_stride, unsigned n_streams,
-               int32_t* __restrict__ out) {
-  __shared__ int32_t stage[WARPS][32][kExpandAStageStride];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned p0 = (blockIdx.x * WARPS + warp) * 32;
-  if (p0 >= n_streams) return;  // whole warp idle
+// One warp, 32 consecutive streams starting at p0 (the warp-uniform first stream); stage = the
+// warp's [32][kExpandAStageStride] shared-memory rows.  NC = false inside the persistent signing
+// kernel (keys published after the kernel started are read with coherent loads).
+template <class P, bool NC>
+__device__ __forceinline__ void expand_a_warp(const uint8_t* __restrict__ rho_base, size_t rho_stride,
+                                              unsigned p0, unsigned n_streams, int32_t* __restrict__ out,
+                                              int32_t (*stage)[kExpandAStageStride], int lane) {
   const unsigned p = p0 + lane;
   const bool active = p < n_streams;
   constexpr int KL = P::K * P::L;
@@ -44,13 +43,14 @@ __global__ void __launch_bounds__(WARPS * 32)
     const unsigned i = r / P::L, j = r % P::L;
     const uint8_t* rho = rho_base + (size_t)key * rho_stride;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) s[w] = load_u64_unaligned(rho + 8 * w);
+    for (int w = 0; w < 4; ++w)
+      s[w] = (uint64_t)load_u32_unaligned<NC>(rho + 8 * w) | ((uint64_t)load_u32_unaligned<NC>(rho + 8 * w + 4) << 32);
     // nonce (i<<8)|j little-endian, then the 0x1F suffix; 0x80 closes the 168-byte block
     s[4] = (uint64_t)j | ((uint64_t)i << 8) | ((uint64_t)0x1F << 16);
     s[20] = 0x8000000000000000ull;
   }
   unsigned ctr = active ? 0u : (unsigned)kN;
-  int32_t* row = stage[warp][lane];
+  int32_t* row = stage[lane];
 
   while (true) {
     keccak_f1600(s);
@@ -76,12 +76,23 @@ __global__ void __launch_bounds__(WARPS * 32)
       const unsigned base = __shfl_sync(kFullMask, ctr, src);
       const unsigned cnt = min(ns, (unsigned)kN - base);
       int32_t* dst = out + (size_t)(p0 + src) * kN + base;
-      for (unsigned idx = lane; idx < cnt; idx += 32) dst[idx] = stage[warp][src][idx];
+      for (unsigned idx = lane; idx < cnt; idx += 32) dst[idx] = stage[src][idx];
     }
     ctr = min((unsigned)kN, ctr + n);
     __syncwarp();
     if (__all_sync(kFullMask, ctr >= (unsigned)kN)) break;
   }
+}
+
+template <class P, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    k_expand_a(const uint8_t* __restrict__ rho_base, size_t rho_stride, unsigned n_streams,
+               int32_t* __restrict__ out) {
+  __shared__ int32_t stage[WARPS][32][kExpandAStageStride];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned p0 = (blockIdx.x * WARPS + warp) * 32;
+  if (p0 >= n_streams) return;  // whole warp idle
+  expand_a_warp<P, true>(rho_base, rho_stride, p0, n_streams, out, stage[warp], lane);
 }
 
 // --------------------------------------------------------------------- ExpandS

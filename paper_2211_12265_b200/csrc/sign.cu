@@ -39,23 +39,17 @@ constexpr int kSignThreads = 128;          // threads = attempt slots per CTA
 constexpr int kSignWarps = kSignThreads / 32;
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 constexpr int kChunkBytes = 1024;  // cp.async landing buffer: one packed polynomial
+constexpr int kPrepKeys = 16;       // keys a scheduler CTA precomputes per claim
 
 // ---- per-key precomputation -----------------------------------------------------------
 // One warp per (key, polynomial): s1 (L), s2 (K), t0 (K) unpacked from the secret key,
 // range-checked (packing.hpp:79-86), transformed; stored reduced, natural order.
-template <class P, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    k_sign_unpack(unsigned n_keys, const uint8_t* __restrict__ sks, size_t sk_stride,
-                  int32_t* __restrict__ shat, unsigned* __restrict__ key_bad) {
+template <class P, bool NC>
+__device__ __forceinline__ void sign_unpack_poly(unsigned id, const uint8_t* __restrict__ sks, size_t sk_stride,
+                                                 int32_t* __restrict__ shat, unsigned* __restrict__ key_bad,
+                                                 int32_t* tile, const int2* zs, int lane) {
   using S = Sizes<P>;
   constexpr int PV = P::L + 2 * P::K;
-  __shared__ __align__(16) int2 zs[256], nzs[256];
-  __shared__ __align__(16) int32_t tiles[WARPS][kTileWords];
-  load_twiddles(zs, nzs);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned id = blockIdx.x * WARPS + warp;
-  if (id >= n_keys * PV) return;
   const unsigned key = id / PV, p = id % PV;
   const uint8_t* sk = sks + (size_t)key * sk_stride;
   int32_t r[8];
@@ -64,7 +58,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     const uint8_t* src = sk + S::SK_S1 + p * S::ETA_POLY;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const uint32_t raw = load_bits(src, (lane + 32 * e) * P::ETA_BITS, P::ETA_BITS);
+      const uint32_t raw = load_bits_t<NC>(src, (lane + 32 * e) * P::ETA_BITS, P::ETA_BITS);
       bad = bad || raw > 2u * P::ETA;
       r[e] = P::ETA - (int32_t)raw;
     }
@@ -72,13 +66,28 @@ __global__ void __launch_bounds__(WARPS * 32)
     const uint8_t* src = sk + S::SK_T0 + (p - P::L - P::K) * S::T0_POLY;
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      r[e] = 4096 - (int32_t)load_bits(src, (lane + 32 * e) * 13, 13);
+      r[e] = 4096 - (int32_t)load_bits_t<NC>(src, (lane + 32 * e) * 13, 13);
   }
-  ntt_fwd(r, tiles[warp], zs, lane);
+  ntt_fwd(r, tile, zs, lane);
   int4* dst = reinterpret_cast<int4*>(shat + (size_t)id * kN) + 2 * lane;
   dst[0] = make_int4(reduce32(r[0]), reduce32(r[1]), reduce32(r[2]), reduce32(r[3]));
   dst[1] = make_int4(reduce32(r[4]), reduce32(r[5]), reduce32(r[6]), reduce32(r[7]));
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(key_bad, 1u);
+}
+
+template <class P, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    k_sign_unpack(unsigned n_keys, const uint8_t* __restrict__ sks, size_t sk_stride,
+                  int32_t* __restrict__ shat, unsigned* __restrict__ key_bad) {
+  constexpr int PV = P::L + 2 * P::K;
+  __shared__ __align__(16) int2 zs[256], nzs[256];
+  __shared__ __align__(16) int32_t tiles[WARPS][kTileWords];
+  load_twiddles(zs, nzs);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned id = blockIdx.x * WARPS + warp;
+  if (id >= n_keys * PV) return;
+  sign_unpack_poly<P, true>(id, sks, sk_stride, shat, key_bad, tiles[warp], zs, lane);
 }
 
 // ---- device-side scheduler state -----------------------------------------------------
@@ -111,6 +120,8 @@ struct BatchView {
   unsigned n, tcap, max_attempt, spec_depth, key_stride, ticket1;  // ticket1 = gate value the view was loaded for
   int level;
   unsigned exclusive;
+  unsigned prep_n;   // keys the scheduler precomputes for this batch (0: none)
+  unsigned prep_ok;  // ... and they have all been seen done (behind an acquire)
   const uint64_t* mu;
   const uint64_t* rho_prime;
   const uint32_t* kappa0;
@@ -190,6 +201,8 @@ struct SignSmem {
   unsigned cursor2, cursor4;  // next unclaimed slot of stages S2 / S4 (warps pull slots)
   unsigned r_on, r_spec;      // this round's assigned / speculative slots (trace)
   unsigned rounds;            // rounds this CTA has run
+  unsigned prep_slot, prep_k0, prep_cnt;  // keys to precompute before this round (prep_cnt 0: none)
+  unsigned prep_wait;         // a servable batch's precomputation is in other CTAs' hands
 };
 
 // ---- asynchronous scratch prefetch ----------------------------------------------------
@@ -544,6 +557,8 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
         sm.span = 0;
         sm.Uold = U;
         sm.need_hash = 0;
+        sm.prep_cnt = 0;
+        sm.prep_wait = 0;
       }
       // Stragglers.  With work queued every slot runs a first attempt, so a task deep in its
       // rejection loop advances one nonce per full-length round and its batch completes long
@@ -561,7 +576,8 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       const unsigned cap = (unsigned)kSignThreads - n_s * a.boost_depth;
       if (U < cap && !(a.single_round && sm.rounds > 0)) {
         // a.window == 1 (stage tests): only the kernel's own batch
-        unsigned tk = 0xFFFFFFFFu, blocked = 0xFFFFFFFFu;
+        unsigned tk = 0xFFFFFFFFu, blocked = 0xFFFFFFFFu, ptk = 0xFFFFFFFFu;
+        bool pwait = false;
         if (a.window > 1u || (unsigned)lane == a.ticket % kRing) {
           SignBatch* g = a.ring + lane;
           const unsigned g1 = ld_acquire(&g->gate);
@@ -577,6 +593,8 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
             v.key_stride = g->key_stride;
             v.level = g->level;
             v.exclusive = g->exclusive;
+            v.prep_n = g->prep_n;
+            v.prep_ok = 0;
             v.mu = g->mu;
             v.rho_prime = g->rho_prime;
             v.kappa0 = g->kappa0;
@@ -588,11 +606,27 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
             v.ticket1 = g1;
           }
           if (g1 != 0 && v.ticket1 == g1) {
+            const bool mine = v.level == P::LEVEL && (own || (!v.exclusive && a.window > 1u));
+            bool ready = true;
+#ifndef DLB_AB_NO_PREP  // (A/B switch: the scheduler without its precomputation code; shared cached keys only)
+            if (v.prep_n && !v.prep_ok) {  // keys still being precomputed (by scheduler CTAs, below)
+              if (ld_acquire(&g->prep_done) >= v.prep_n) {
+                v.prep_ok = 1;
+              } else {
+                ready = false;
+                const unsigned long long pq = ld_relaxed(&g->prep_q);
+                if (mine && (unsigned)(pq >> 32) == g1) {
+                  if ((unsigned)pq < v.prep_n) ptk = g1 - 1u;
+                  else pwait = true;
+                }
+              }
+            }
+#endif
             const unsigned long long q = ld_relaxed(&g->head);
             const bool open = (unsigned)(q >> 32) == g1 && (unsigned)q < v.n;
             if (open) {
-              if (v.level == P::LEVEL && (own || (!v.exclusive && a.window > 1u))) {
-                if (sm.bcnt[lane] < v.tcap) tk = g1 - 1u;
+              if (mine) {
+                if (ready && sm.bcnt[lane] < v.tcap) tk = g1 - 1u;
               } else {
                 blocked = g1 - 1u;  // unclaimed work this kernel cannot serve
               }
@@ -644,6 +678,31 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
           }
           U += got;
         }
+        // Per-key precomputation of a batch whose keys are not cached: a run of keys is claimed
+        // like tasks are and expanded by this CTA before the round (the precomputation of the next
+        // batches thus overlaps the signing of the current ones; a separate kernel could not become
+        // resident beside the scheduler grid).  Oldest batch first.
+        ptk = __reduce_min_sync(0xffffffffu, ptk);
+        pwait = __any_sync(0xffffffffu, pwait);
+        if (lane == 0) {
+          sm.prep_wait = pwait ? 1u : 0u;
+          if (ptk != 0xFFFFFFFFu) {
+            const BatchView& v = sm.bv[ptk % kRing];
+            unsigned long long q = ld_relaxed(&v.g->prep_q);
+            while ((unsigned)(q >> 32) == v.ticket1 && (unsigned)q < v.prep_n) {
+              const unsigned take = min((unsigned)kPrepKeys, v.prep_n - (unsigned)q);
+              const unsigned long long old = atomicCAS(&v.g->prep_q, q, q + take);
+              if (old == q) {
+                sm.prep_slot = ptk % kRing;
+                sm.prep_k0 = (unsigned)q;
+                sm.prep_cnt = take;
+                break;
+              }
+              q = old;
+            }
+            if (!sm.prep_cnt) sm.prep_wait = 1u;  // lost the race for the last keys: they are in hand
+          }
+        }
         __syncwarp();
         if (lane == 0) sm.U = U;
       }
@@ -653,7 +712,43 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
     }
     __syncthreads();
     const unsigned U = sm.U;
-    if (U == 0) break;
+    const unsigned prep_cnt = sm.prep_cnt, prep_wait = sm.prep_wait;
+#ifndef DLB_AB_NO_PREP
+    if (prep_cnt) {
+      // ExpandA (sampling.hpp:42-56; one sponge per matrix polynomial, 32 streams per warp pass)
+      // and the secret vectors (scheme.hpp:106-125; one warp per polynomial) of keys
+      // [prep_k0, prep_k0 + prep_cnt) of the batch in ring slot prep_slot.  The stage buffers of
+      // the round are free here and lend their shared memory.
+      constexpr int KL = P::K * P::L, PV = P::L + 2 * P::K;
+      const BatchView& v = sm.bv[sm.prep_slot];
+      SignBatch* g = v.g;
+      const unsigned k0 = sm.prep_k0, cnt = prep_cnt;
+      const uint8_t* sks = g->prep_sks;
+      const size_t stride = g->prep_stride;
+      static_assert(sizeof(sm.u) >= sizeof(int32_t) * kSignWarps * 32 * kExpandAStageStride, "ExpandA staging fits the stage buffers");
+      auto stage = reinterpret_cast<int32_t(*)[32][kExpandAStageStride]>(&sm.u);
+      const unsigned send = (k0 + cnt) * KL;
+      for (unsigned p0 = k0 * KL + (unsigned)warp * 32u; p0 < send; p0 += (unsigned)kSignThreads)
+        expand_a_warp<P, false>(sks, stride, p0, send, const_cast<int32_t*>(v.A), stage[warp], lane);
+      __syncthreads();
+      for (unsigned id = k0 * PV + (unsigned)warp; id < (k0 + cnt) * PV; id += (unsigned)kSignWarps)
+        sign_unpack_poly<P, false>(id, sks, stride, const_cast<int32_t*>(v.shat), &g->key_bad,
+                                   sm.u.a.ws[warp].tile, sm.zs, lane);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&g->prep_done, cnt);
+      }
+    }
+#endif
+    if (U == 0) {
+      if (!prep_cnt && !prep_wait) break;
+      // look again: the batch may be claimable now, or its last keys are being expanded by other
+      // CTAs and its tasks follow shortly.  (Barrier: warp 0 rewrites the refill's shared words.)
+      if (!prep_cnt) __nanosleep(2000);
+      __syncthreads();
+      continue;
+    }
     const unsigned B = sm.B;
 
     // ---- S0: mu = H(tr || M), rho' = H(K || mu) of the tasks just claimed (scheme.hpp:240-248)
@@ -985,11 +1080,12 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
 // ---- host side ---------------------------------------------------------------------
 //
 // Submission and completion are separate (dlb_sign_submit / dlb_sign_wait); the synchronous
-// entry points are submit + wait.  Everything a submission needs is enqueued on the stream lane
-// of its ticket: inputs, the descriptor body, the per-key and per-task precomputation, the
-// gate word that publishes the batch to running scheduler kernels, and the batch's own
-// scheduler kernel.  The precompute kernels use one-warp CTAs so they fit beside a fully
-// resident scheduler grid (114 registers x 512 threads leave one warp's worth per SM).
+// entry points are submit + wait.  A submission enqueues its inputs, the descriptor body and
+// the gate word that publishes the batch on the publication stream, and the batch's own scheduler
+// kernel on a stream lane.  Per-key precomputation: a shared key comes from the cross-call cache
+// (a miss runs the two one-warp-CTA kernels once); key tables and per-task keys are expanded by
+// the scheduler CTAs themselves (SignBatch::prep_*), because no other kernel can become resident
+// beside a scheduler grid: 4 CTAs x 128 threads x 128 registers fill the register file.
 
 namespace {
 
@@ -1148,7 +1244,7 @@ KeyCacheEntry* key_cache_get(dlb_ctx* c, const uint8_t* hk, const uint8_t* dsk, 
 
 }  // namespace
 
-// Everything that publishes a batch (input copies, descriptor, per-key kernels of uncached keys,
+// Everything that publishes a batch (input copies, descriptor, the kernels of a key-cache miss,
 // gate) goes through one publication stream that never holds a scheduler kernel, so it cannot
 // queue up behind a running one; the scheduler kernel of the ticket then goes to its lane.
 int sign_reserve(dlb_ctx* c, unsigned* ticket, cudaStream_t* pub) {
@@ -1298,6 +1394,12 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
     h.rp_w = io.d_rho_prime ? nullptr : rp;
   }
   h.host_flag = c->d_flags + slot;
+  if (!cached) {
+    h.prep_sks = io.d_sks;
+    h.prep_stride = (unsigned)io.sk_stride;
+    h.prep_n = (unsigned)nk;
+    h.prep_q = (unsigned long long)(ticket + 1u) << 32;
+  }
   h.t_first_start = h.t_first_exit = ~0ull;
   h.gate = ticket + 1u;
   SignBatch* g = c->d_ring + slot;
@@ -1306,13 +1408,8 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
   DLB_CUDA_CHECK(cudaMemcpyAsync(g, &h, offsetof(SignBatch, gate), cudaMemcpyHostToDevice, st));
 
   prof.mark(" body copy");
-  // per-key precomputation (scheme.hpp:106-125), unless the shared key came from the cache
-  if (!cached) {
-    k_expand_a<P, 1><<<cdiv(nk * KL, 32), 32, 0, st>>>(io.d_sks, io.sk_stride, (unsigned)(nk * KL), A);
-    k_sign_unpack<P, 1><<<(unsigned)(nk * PV), 32, 0, st>>>((unsigned)nk, io.d_sks, io.sk_stride, shat,
-                                                           &g->key_bad);
-    c->launches += 2;
-  }
+  // per-key precomputation (scheme.hpp:106-125), unless the shared key came from the cache: done
+  // by the scheduler CTAs themselves (prep_* in the descriptor), nothing to launch
   prof.mark(" prep launches");
   // publish: running scheduler kernels of earlier tickets may start claiming tasks now
   DLB_CUDA_CHECK(cudaMemcpyAsync(&g->gate, &h.gate, sizeof(unsigned), cudaMemcpyHostToDevice, st));

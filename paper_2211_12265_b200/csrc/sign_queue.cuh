@@ -43,9 +43,18 @@ struct SignBatch {
   int32_t bounds[3];          // DBG kernel: z, r0, c*t0 norm bounds (scheme.hpp:133-138)
   unsigned pad0;
   volatile unsigned* host_flag;  // mapped pinned word: set to ticket + 1 when done == n
+  // per-key precomputation done by the scheduler itself (keys that are not in the cross-call cache:
+  // key tables, one key per task): prep_n keys at prep_sks + k * prep_stride -> A, shat above.  The
+  // batch's tasks become claimable when prep_done == prep_n.
+  const uint8_t* prep_sks;
+  unsigned prep_stride;
+  unsigned prep_n;
   // ---- mutable (device atomics)
   unsigned long long head;    // the device work queue of this batch: (ticket + 1) << 32 | next unclaimed
                               // task; claimed by compare-and-swap, so a stale view can never claim
+  unsigned long long prep_q;  // (ticket + 1) << 32 | next key to precompute, claimed like `head`
+  unsigned prep_done;         // keys precomputed
+  unsigned pad1;
   unsigned done;              // committed tasks
   unsigned key_bad;           // some secret key failed the eta range check
   unsigned long long rounds, attempts, speculative, idle_slots, accepted_sum, failed;
