@@ -106,7 +106,7 @@ class MultiEngine:
         if errs:
             raise errs[0]
 
-    def batch_sign(self, level, sks, flat, off, chunk=65536, return_info=False, depth=4):
+    def batch_sign(self, level, sks, flat, off, chunk=65536, return_info=False, depth=16):
         """Every engine streams its shard as chunks in flight (sign_submit / sign_wait)."""
         from .engine import LEVELS
         n = len(off) - 1
