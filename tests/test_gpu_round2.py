@@ -289,3 +289,56 @@ def test_steady_flow_reuses_ring_slots_under_resident_ctas(eng, oracle):
     for h in inflight:
         sigs, att, failed, st = eng.sign_wait(h)
         assert not failed.any() and np.array_equal(sigs, want) and np.array_equal(att, want_att)
+
+
+def test_staged_result_copies_option(oracle, monkeypatch):
+    """DLB_ZERO_COPY_MAX=0: signatures for a pinned caller buffer go through device memory and are
+    copied at wait time (copies of batches that completed meanwhile are queued behind the waited
+    one); bytes are those of the default in-place path and of the oracle.  Straight through the
+    C ABI with every result buffer pinned."""
+    import ctypes as C
+    from paper_2211_12265_b200 import Engine
+    from paper_2211_12265_b200.engine import LEVELS, SignStats
+    level, n, batches = 3, 700, 6
+    sgb = LEVELS[level][4]
+    rs = np.random.default_rng(99)
+    flats = [rs.integers(0, 256, n * 24, dtype=np.uint8) for _ in range(batches)]
+    off = np.arange(n + 1, dtype=np.uint64) * 24
+    vp = C.c_void_p
+    got = {}
+    for knob in ("0", None):
+        if knob is None:
+            monkeypatch.delenv("DLB_ZERO_COPY_MAX", raising=False)
+        else:
+            monkeypatch.setenv("DLB_ZERO_COPY_MAX", knob)
+        e = Engine(0)
+        try:
+            pks, sks = e.batch_keygen(level, np.arange(32, dtype=np.uint8))
+            sk = np.ascontiguousarray(sks[0])
+
+            def pinned(nbytes, dtype):
+                p = e.lib.dlb_host_alloc(nbytes)
+                assert p
+                return p, np.frombuffer((C.c_uint8 * nbytes).from_address(p), dtype)
+
+            bufs = [(pinned(n * sgb, np.uint8), pinned(n * 4, np.uint32), pinned(n, np.uint8)) for _ in range(batches)]
+            tickets = []
+            for b in range(batches):
+                (ps, _), (pa, _), (pf, _) = bufs[b]
+                t = C.c_uint64(0)
+                assert e.lib.dlb_sign_submit(e.ctx, level, 0, vp(sk.ctypes.data), 0, n, None, vp(flats[b].ctypes.data),
+                                             vp(off.ctypes.data), None, 0, 1, vp(ps), vp(pa), vp(pf), C.byref(t)) == 0
+                tickets.append(t.value)
+            for b in (3, 0, 5, 1, 2, 4):
+                st = SignStats()
+                assert e.lib.dlb_sign_wait(e.ctx, tickets[b], C.byref(st)) == 0
+                assert not bufs[b][2][1].any() and st.accepted_attempt_sum == int(bufs[b][1][1].sum())
+            got[knob] = [bufs[b][0][1].reshape(n, sgb).copy() for b in range(batches)]
+            for trio in bufs:
+                for p, _ in trio:
+                    e.lib.dlb_host_free(p)
+        finally:
+            e.close()
+    for b in range(batches):
+        assert np.array_equal(got["0"][b], got[None][b])
+        assert got["0"][b][7].tobytes() == oracle.sign(level, sks[0].tobytes(), flats[b][7 * 24:8 * 24].tobytes())[0]
