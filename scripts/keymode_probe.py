@@ -59,6 +59,14 @@ modes = [("one shared key", 0, 0, None)]
 for T in (16, 1024):
     modes.append(("table of %d keys" % T, T, skb, torch.from_numpy(rng.integers(0, T, n).astype(np.uint32)).to(dev)))
 modes.append(("one key per task", 0, skb, None))
+if os.environ.get("ONLY"):  # e.g. ONLY="one key per task" ONCE=1 under ncu: one synchronous batch of that mode
+    modes = [m for m in modes if m[0] == os.environ["ONLY"]]
+if os.environ.get("ONCE"):
+    for name, nk, stride, kidx in modes:
+        depth = 1
+        run(nk, stride, kidx, 2)
+    eng.close()
+    sys.exit(0)
 for name, nk, stride, kidx in modes:
     for d_, steps in ((1, 6), (depth, 32)):
         depth_saved = depth
