@@ -69,14 +69,18 @@ __device__ __forceinline__ void expand_a_warp(const uint8_t* __restrict__ rho_ba
         n += t < (uint32_t)kQ;
       }
     }
+    // copy-out: row src holds cnt <= 56 accepted values that go to coefficients [base, base + cnt)
+    // of stream p0 + src -- one shuffle of the packed (cnt, base) per row, two predicated copies
+    const unsigned desc = min(n, (unsigned)kN - ctr) | (ctr << 8);
+    int32_t* obase = out + (size_t)p0 * kN + lane;
     __syncwarp();
-#pragma unroll 1
+#pragma unroll 8
     for (int src = 0; src < 32; ++src) {
-      const unsigned ns = __shfl_sync(kFullMask, n, src);
-      const unsigned base = __shfl_sync(kFullMask, ctr, src);
-      const unsigned cnt = min(ns, (unsigned)kN - base);
-      int32_t* dst = out + (size_t)(p0 + src) * kN + base;
-      for (unsigned idx = lane; idx < cnt; idx += 32) dst[idx] = stage[src][idx];
+      const unsigned d = __shfl_sync(kFullMask, desc, src);
+      const unsigned cnt = d & 0xFFu;
+      int32_t* dst = obase + src * kN + (d >> 8);
+      if ((unsigned)lane < cnt) dst[0] = stage[src][lane];
+      if ((unsigned)lane + 32u < cnt) dst[32] = stage[src][lane + 32];
     }
     ctr = min((unsigned)kN, ctr + n);
     __syncwarp();

@@ -2,6 +2,8 @@
 scheduler-equivalence criterion (tests/acceptance.cpp:186-244), injected norm bounds and reject
 stages (tests/test_scheme.cpp:147-174), nonce-space exhaustion (scheduler.hpp:52,122-128),
 batches in flight (tools/dilithium_cli.cpp:309-345), the cross-call key cache."""
+import os
+
 import numpy as np
 import pytest
 
@@ -229,7 +231,8 @@ def test_in_flight_stress_random_pipeline(eng):
         return lv, sk, flat, off
 
     inflight, checked = [], 0
-    for it in range(240):
+    iters = int(os.environ.get("DLB_STRESS_ITERS", "240"))  # a longer soak: DLB_STRESS_ITERS=3000
+    for it in range(iters):
         lv = int(rs.choice(levels, p=[.55, .2, .15, .1]))
         job = make(lv)
         want = eng.batch_sign(job[0], job[1], (job[2], job[3]), return_info=True) if it % 3 == 0 else None
