@@ -22,6 +22,43 @@ __device__ __constant__ const uint64_t kKeccakRC[24] = {
     0x8000000000008002ull, 0x8000000000000080ull, 0x000000000000800aull, 0x800000008000000aull,
     0x8000000080008081ull, 0x8000000000008080ull, 0x0000000080000001ull, 0x8000000080008008ull};
 
+// Rotations on the fma pipe.  A 64-bit rotate is two funnel shifts on the alu pipe, the pipe every
+// other instruction of the permutation (LOP3) needs as well; the fma pipe idles.  hi:lo rotated
+// left by r < 32 is {hi * 2^r + (lo >> (32 - r)), lo * 2^r + (hi >> (32 - r))}: two IMAD.WIDE by
+// 2^r give all four terms ({x >> (32 - r), x << r} = x * 2^r as 64 bits), two more IMADs (or one
+// IMAD and one LOP3) put them together.  The multipliers come from the constant bank, which keeps
+// ptxas from turning the multiplies back into shifts.  DLB_KECCAK_FMA_ROT = how many of the 29
+// rotations of a round go that way (0: none).
+#ifndef DLB_KECCAK_FMA_ROT
+#define DLB_KECCAK_FMA_ROT 0
+#endif
+__device__ __constant__ uint32_t kRotMul[33] = {
+    1u << 0,  1u << 1,  1u << 2,  1u << 3,  1u << 4,  1u << 5,  1u << 6,  1u << 7,  1u << 8,  1u << 9,  1u << 10,
+    1u << 11, 1u << 12, 1u << 13, 1u << 14, 1u << 15, 1u << 16, 1u << 17, 1u << 18, 1u << 19, 1u << 20, 1u << 21,
+    1u << 22, 1u << 23, 1u << 24, 1u << 25, 1u << 26, 1u << 27, 1u << 28, 1u << 29, 1u << 30, 1u << 31, 1u};
+
+template <int R>
+__device__ __forceinline__ uint64_t rotl64_fma(uint64_t x) {
+  static_assert(R % 32 != 0, "plain moves otherwise");
+  uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  if (R > 32) {
+    const uint32_t t = lo;
+    lo = hi;
+    hi = t;
+  }
+  const uint32_t p = kRotMul[R & 31], one = kRotMul[32];
+  uint32_t alo, ahi, blo, bhi, nlo, nhi;
+  asm("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %2, %3;\n\tmov.b64 {%0, %1}, w;\n\t}" : "=r"(alo), "=r"(ahi) : "r"(lo), "r"(p));
+  asm("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %2, %3;\n\tmov.b64 {%0, %1}, w;\n\t}" : "=r"(blo), "=r"(bhi) : "r"(hi), "r"(p));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(nlo) : "r"(alo), "r"(one), "r"(bhi));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(nhi) : "r"(blo), "r"(one), "r"(ahi));
+  return ((uint64_t)nhi << 32) | nlo;
+}
+
+// rotation number IDX (0..28) of a round: on the fma pipe if IDX < DLB_KECCAK_FMA_ROT
+template <int R, int IDX>
+__device__ __forceinline__ uint64_t rotl64_sel(uint64_t x);
+
 template <int R>
 __device__ __forceinline__ uint64_t rotl64(uint64_t x) {
   if (R == 0) return x;
@@ -40,41 +77,52 @@ __device__ __forceinline__ uint64_t rotl64(uint64_t x) {
   return ((uint64_t)nhi << 32) | nlo;
 }
 
+template <int R, int IDX>
+__device__ __forceinline__ uint64_t rotl64_sel(uint64_t x) {
+  if constexpr (R % 32 != 0 && IDX < DLB_KECCAK_FMA_ROT) return rotl64_fma<R>(x);
+  else return rotl64<R>(x);
+}
+
 __device__ __forceinline__ void keccak_round(uint64_t (&s)[25], uint64_t rc) {
   uint64_t c[5], r[5], b[25];
 #pragma unroll
   for (int x = 0; x < 5; ++x) c[x] = s[x] ^ s[x + 5] ^ s[x + 10] ^ s[x + 15] ^ s[x + 20];
-#pragma unroll
-  for (int x = 0; x < 5; ++x) r[x] = rotl64<1>(c[x]);
+  {
+  r[0] = rotl64_sel<1, 24>(c[0]);
+  r[1] = rotl64_sel<1, 25>(c[1]);
+  r[2] = rotl64_sel<1, 26>(c[2]);
+  r[3] = rotl64_sel<1, 27>(c[3]);
+  r[4] = rotl64_sel<1, 28>(c[4]);
+  }
   // theta + rho + pi: b[y + 5*((2x+3y)%5)] = rotl(s[x+5y] ^ d[x], rho[x+5y]) with
   // d[x] = c[x-1] ^ rotl(c[x+1], 1) folded into the same three-input XOR (one LOP3 per
   // 32-bit half instead of forming d first: 10 instructions fewer per round)
 #define DLB_TH(i, x) (s[i] ^ c[((x) + 4) % 5] ^ r[((x) + 1) % 5])
   b[0] = rotl64<0>(DLB_TH(0, 0));
-  b[10] = rotl64<1>(DLB_TH(1, 1));
-  b[20] = rotl64<62>(DLB_TH(2, 2));
-  b[5] = rotl64<28>(DLB_TH(3, 3));
-  b[15] = rotl64<27>(DLB_TH(4, 4));
-  b[16] = rotl64<36>(DLB_TH(5, 0));
-  b[1] = rotl64<44>(DLB_TH(6, 1));
-  b[11] = rotl64<6>(DLB_TH(7, 2));
-  b[21] = rotl64<55>(DLB_TH(8, 3));
-  b[6] = rotl64<20>(DLB_TH(9, 4));
-  b[7] = rotl64<3>(DLB_TH(10, 0));
-  b[17] = rotl64<10>(DLB_TH(11, 1));
-  b[2] = rotl64<43>(DLB_TH(12, 2));
-  b[12] = rotl64<25>(DLB_TH(13, 3));
-  b[22] = rotl64<39>(DLB_TH(14, 4));
-  b[23] = rotl64<41>(DLB_TH(15, 0));
-  b[8] = rotl64<45>(DLB_TH(16, 1));
-  b[18] = rotl64<15>(DLB_TH(17, 2));
-  b[3] = rotl64<21>(DLB_TH(18, 3));
-  b[13] = rotl64<8>(DLB_TH(19, 4));
-  b[14] = rotl64<18>(DLB_TH(20, 0));
-  b[24] = rotl64<2>(DLB_TH(21, 1));
-  b[9] = rotl64<61>(DLB_TH(22, 2));
-  b[19] = rotl64<56>(DLB_TH(23, 3));
-  b[4] = rotl64<14>(DLB_TH(24, 4));
+  b[10] = rotl64_sel<1, 0>(DLB_TH(1, 1));
+  b[20] = rotl64_sel<62, 1>(DLB_TH(2, 2));
+  b[5] = rotl64_sel<28, 2>(DLB_TH(3, 3));
+  b[15] = rotl64_sel<27, 3>(DLB_TH(4, 4));
+  b[16] = rotl64_sel<36, 4>(DLB_TH(5, 0));
+  b[1] = rotl64_sel<44, 5>(DLB_TH(6, 1));
+  b[11] = rotl64_sel<6, 6>(DLB_TH(7, 2));
+  b[21] = rotl64_sel<55, 7>(DLB_TH(8, 3));
+  b[6] = rotl64_sel<20, 8>(DLB_TH(9, 4));
+  b[7] = rotl64_sel<3, 9>(DLB_TH(10, 0));
+  b[17] = rotl64_sel<10, 10>(DLB_TH(11, 1));
+  b[2] = rotl64_sel<43, 11>(DLB_TH(12, 2));
+  b[12] = rotl64_sel<25, 12>(DLB_TH(13, 3));
+  b[22] = rotl64_sel<39, 13>(DLB_TH(14, 4));
+  b[23] = rotl64_sel<41, 14>(DLB_TH(15, 0));
+  b[8] = rotl64_sel<45, 15>(DLB_TH(16, 1));
+  b[18] = rotl64_sel<15, 16>(DLB_TH(17, 2));
+  b[3] = rotl64_sel<21, 17>(DLB_TH(18, 3));
+  b[13] = rotl64_sel<8, 18>(DLB_TH(19, 4));
+  b[14] = rotl64_sel<18, 19>(DLB_TH(20, 0));
+  b[24] = rotl64_sel<2, 20>(DLB_TH(21, 1));
+  b[9] = rotl64_sel<61, 21>(DLB_TH(22, 2));
+  b[19] = rotl64_sel<56, 22>(DLB_TH(23, 3));
+  b[4] = rotl64_sel<14, 23>(DLB_TH(24, 4));
 #undef DLB_TH
   // chi
 #pragma unroll
