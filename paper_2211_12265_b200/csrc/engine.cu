@@ -207,6 +207,7 @@ int dlb_create(dlb_ctx** out, int device, size_t max_batch) {
   if (const char* v = getenv("DLB_SIGN_OCC")) c->knob_sign_occ = (unsigned)atoi(v);
   c->knob_submit_prof = getenv("DLB_SUBMIT_PROF") != nullptr;
   if (const char* v = getenv("DLB_KEY_CACHE")) c->knob_key_cache = (size_t)atol(v);
+  if (const char* v = getenv("DLB_HOST_STAGE")) c->knob_host_stage = atoi(v) != 0;
   if (const char* v = getenv("DLB_ZERO_COPY_MAX")) c->knob_zero_copy_max = (size_t)atoll(v);
   const int rc = create_resources(c);
   if (rc != 0) {
@@ -852,6 +853,7 @@ int sign_host_submit(dlb_ctx* c, int level, size_t n, const uint8_t* sks, size_t
   io.psi = psi;
   io.speculate = speculate;
   io.d_sigs = dsig;
+  io.host_out = zero_copy != nullptr;
   io.d_attempts = datt;
   io.d_failed = dfail;
   c->launches = 0;

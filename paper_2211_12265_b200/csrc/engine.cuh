@@ -72,6 +72,7 @@ struct SignIo {
   const uint8_t* d_sks = nullptr;
   const uint8_t* h_sks = nullptr;         // nullable: host copy of the keys (shared key: cache lookup)
   size_t sk_stride = 0, n_keys = 0;
+  bool host_out = false;  // d_sigs is mapped host memory
   const uint32_t* d_key_idx = nullptr;
   const uint8_t* d_msgs = nullptr;
   const uint64_t* d_msg_off = nullptr;
@@ -157,6 +158,8 @@ struct dlb_ctx {
   std::vector<dlb::KeyCacheEntry> key_cache;
   unsigned long long key_cache_clock = 0, key_cache_hits = 0, key_cache_misses = 0;
   size_t knob_key_cache = 32;            // entries; 0 disables (DLB_KEY_CACHE)
+  bool knob_host_stage = false;          // signatures for a pinned caller buffer leave the kernel as whole rows from
+                                         // the staging buffer instead of field by field (DLB_HOST_STAGE)
   size_t knob_zero_copy_max = ~(size_t)0; // signatures go straight into a pinned caller buffer up to this many
                                          // bytes per batch, through device memory + a copy at wait time above
                                          // (DLB_ZERO_COPY_MAX; in place is faster at every size measured,

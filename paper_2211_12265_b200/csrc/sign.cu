@@ -120,6 +120,7 @@ struct BatchView {
   unsigned n, tcap, max_attempt, spec_depth, key_stride, ticket1;  // ticket1 = gate value the view was loaded for
   int level;
   unsigned exclusive;
+  unsigned stage_out;  // never write a signature in place (host-mapped output, DLB_HOST_STAGE)
   unsigned prep_n;   // keys the scheduler precomputes for this batch (0: none)
   unsigned prep_ok;  // ... and they have all been seen done (behind an acquire)
   const uint64_t* mu;
@@ -594,6 +595,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
             v.level = g->level;
             v.exclusive = g->exclusive;
             v.prep_n = g->prep_n;
+            v.stage_out = g->stage_out;
             v.prep_ok = 0;
             v.mu = g->mu;
             v.rho_prime = g->rho_prime;
@@ -933,7 +935,7 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
       while (s < kSignThreads) {
         const int nx = grab(&sm.cursor4);
         const BatchView& v = sm.bv[sm.slot_batch[s]];
-        const bool direct = (unsigned)s < U;  // depth 0: the task's next unresolved nonce
+        const bool direct = (unsigned)s < U && !v.stage_out;  // depth 0: the task's next unresolved nonce
         const int rej = stage_finish<P, DBG>(
             sm.u.a.ws[warp], pp, par, sm.zs, sm.nzs, lane, ybytes + (size_t)s * Z::Y_SLOT,
             wbuf + (size_t)s * Z::W_SLOT, nx < kSignThreads ? c8buf + (size_t)nx * kN : nullptr,
@@ -1015,7 +1017,8 @@ __global__ void __launch_bounds__(kSignThreads, (P::LEVEL == 2 || P::LEVEL == 44
 #pragma unroll 1
       for (unsigned u = warp; u < U; u += kSignWarps) {
         const int win = sm.winner[u];
-        if (win == -1 || win == (int)u) continue;  // open, or a depth-0 winner that S4 wrote in place
+        // open, or a depth-0 winner that S4 wrote in place
+        if (win == -1 || (win == (int)u && !sm.bv[sm.ubatch[u]].stage_out)) continue;
         const uint8_t* src = staging + (size_t)(win < 0 ? 0 : win) * Z::SIG_PAD;
         uint8_t* dst = sm.bv[sm.ubatch[u]].sigs + (size_t)sm.utask[u] * S::SIG;
         // word-granular, coalesced copy to a destination of any alignment (sig_bytes is
@@ -1394,6 +1397,7 @@ static int sign_submit_t(dlb_ctx* c, unsigned ticket, const SignIo& io) {
     h.rp_w = io.d_rho_prime ? nullptr : rp;
   }
   h.host_flag = c->d_flags + slot;
+  h.stage_out = io.host_out && c->knob_host_stage ? 1u : 0u;
   if (!cached) {
     h.prep_sks = io.d_sks;
     h.prep_stride = (unsigned)io.sk_stride;

@@ -49,6 +49,8 @@ struct SignBatch {
   const uint8_t* prep_sks;
   unsigned prep_stride;
   unsigned prep_n;
+  unsigned stage_out;         // signatures always go through the staging buffer and one whole-row copy (DLB_HOST_STAGE)
+  unsigned pad4;
   // ---- mutable (device atomics)
   unsigned long long head;    // the device work queue of this batch: (ticket + 1) << 32 | next unclaimed
                               // task; claimed by compare-and-swap, so a stale view can never claim
