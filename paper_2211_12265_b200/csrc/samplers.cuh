@@ -134,6 +134,12 @@ __global__ void __launch_bounds__(WARPS * 32)
     keccak_f1600(s);
 #pragma unroll
     for (int w = 0; w < kWords256; ++w) {
+#ifndef DLB_EXPAND_S_NO_EARLY_EXIT
+      // The last block of a stream is mostly surplus (eta = 2: 256 of the first 272 nibbles are
+      // accepted on average, the second block supplies the last few): stop at the first word
+      // pair by which every lane of the warp is full.
+      if (w > 0 && (w & 1) == 0 && __all_sync(kFullMask, ctr >= (unsigned)kN)) break;
+#endif
       const uint64_t v = s[w];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
