@@ -7,6 +7,24 @@
 #pragma once
 #include "ntt.cuh"
 
+// Matrix loads in flight per thread in the arithmetic kernels' accumulation loops (2 x 16 bytes
+// per unrolled iteration).  These kernels stream every task's matrix from HBM (22 KB per
+// Dilithium2 key, 3.4 TB/s while they run); four iterations in flight measured +0.4 / +1.9 /
+// +3.9 % keygen throughput at Dilithium2 / 3 / 5 against one, eight no better
+// (profiles/r02_arith_unroll_ab.txt).
+// k_verify_arith at L = 4 is the exception: fully unrolled it needs 86 registers instead of 64,
+// loses three resident CTAs per SM and 3 % (28.8 -> 27.9 M verify/s), so it keeps one iteration.
+#ifndef DLB_ARITH_J_UNROLL
+#define DLB_ARITH_J_UNROLL 4
+#endif
+#ifndef DLB_VERIFY_J_UNROLL
+#define DLB_VERIFY_J_UNROLL (P::L > 4 ? DLB_ARITH_J_UNROLL : 1)
+#endif
+#define DLB_PRAGMA_(x) _Pragma(#x)
+#define DLB_PRAGMA(x) DLB_PRAGMA_(x)
+#define DLB_ARITH_J_PRAGMA DLB_PRAGMA(unroll DLB_ARITH_J_UNROLL)
+#define DLB_VERIFY_J_PRAGMA DLB_PRAGMA(unroll DLB_VERIFY_J_UNROLL)
+
 namespace dlb {
 
 // per-warp shared scratch
@@ -113,7 +131,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     int64_t acc64[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) acc64[m] = mac_wide(0, -ch[m], reduce32(r[m]));
-#pragma unroll 1
+    DLB_VERIFY_J_PRAGMA
     for (int j = 0; j < P::L; ++j) {
       const int4* ap = reinterpret_cast<const int4*>(tA + (size_t)(i * P::L + j) * kN) + 2 * lane;
       const int4 a0 = __ldg(ap), a1 = __ldg(ap + 1);
@@ -190,7 +208,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     int64_t acc64[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) acc64[m] = 0;
-#pragma unroll 1
+    DLB_ARITH_J_PRAGMA
     for (int j = 0; j < P::L; ++j) {
       const int4* ap = reinterpret_cast<const int4*>(tA + (size_t)(i * P::L + j) * kN) + 2 * lane;
       const int4 a0 = __ldg(ap), a1 = __ldg(ap + 1);
