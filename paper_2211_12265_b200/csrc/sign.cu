@@ -32,6 +32,14 @@
 #endif
 namespace dlb {
 
+// matrix-row iterations in flight in S2's accumulation loop (A/B knob: with one key per task the
+// matrix streams from HBM; profiles/r02_summary.md section 2)
+#ifndef DLB_SIGN_J_UNROLL
+#define DLB_SIGN_J_UNROLL 1
+#endif
+#define DLB_SIGN_PRAGMA_(x) _Pragma(#x)
+#define DLB_SIGN_PRAGMA(x) DLB_SIGN_PRAGMA_(x)
+#define DLB_SIGN_J_PRAGMA DLB_SIGN_PRAGMA(unroll DLB_SIGN_J_UNROLL)
 #ifndef DLB_SIGN_MINB
 #define DLB_SIGN_MINB 4  // resident CTAs per SM: 5 (96 regs) was measured slower -- it squeezes L1 to ~10 KB
 #endif
@@ -294,7 +302,7 @@ __device__ __forceinline__ void stage_w(SignWarpScratch<P>& ws, SlotPipe& pp, co
     // (No software prefetch of the next matrix polynomial: the register copies it needs cost
     // more issue slots than the L1-resident loads' latency, measured +2 %.)
     const int4* ap = reinterpret_cast<const int4*>(A + (size_t)(i * P::L) * kN) + 2 * lane;
-#pragma unroll 1
+    DLB_SIGN_J_PRAGMA
     for (int j = 0; j < P::L; ++j) {
       const int4 a0 = ld_weak(ap + j * (kN / 4)), a1 = ld_weak(ap + j * (kN / 4) + 1);
       const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
